@@ -1,0 +1,174 @@
+/*
+ * gcgb200 — C ABI of the B200-native GCG hot path (sm_100a, fp64).
+ *
+ * Two tiers of entry points, both plain `extern "C"` with pointers + sizes and
+ * an int status (0 = ok; never a C++ exception across the ABI):
+ *
+ *  1. Reference-FFI mirror (host buffers).  `gcgeig_csr_matvec`,
+ *     `gcgeig_inner_product` and `gcgeig_axpby` take exactly the arguments of
+ *     the reference's kernel-backend functions
+ *         csr_matvec(indptr, indices, data, x, out)        _kernels/__init__.py:54-55, _cy.pyx:11-23
+ *         inner_product(x, y, out, chunk, deterministic)   _kernels/__init__.py:58-59, _cy.pyx:26-50
+ *         axpby(alpha, x, beta, y)                         _kernels/__init__.py:62-63, _cy.pyx:53-65
+ *     (column-major host arrays, int64 CSR indices, a strided `out`), copy to
+ *     HBM, run the device kernels and copy back.  They back the `sm100`
+ *     backend registered in gcgeig._kernels._IMPLS.
+ *
+ *  2. Device tier (device pointers, row-major multivectors, caller stream).
+ *     Element (i, c) of a multivector lives at X[i*ld + c]; small dense
+ *     matrices are row-major with leading dimension ld.  These are the GCGE
+ *     ops surface:
+ *         MatDotMultiVec      -> gcg_spmm_csr          (operators.py:103-111, 149-156)
+ *         MultiVecInnerProd   -> gcg_gram              (multivec.py:84-112)
+ *         MultiVecLinearComb  -> gcg_lincomb           (solver.py:300,333,376; orth.py:144,175,184)
+ *         MultiVecAxpby       -> gcg_axpby             (multivec.py:62-73)
+ *         block CG (STEP 6)   -> gcg_block_cg          (cg.py:33-99)
+ *         dense RR eigensolve -> gcg_syev              (dense.py:74-133, sign rule dense.py:63-71)
+ *     plus fused decision kernels for the B-orthogonalisation
+ *     (orth.py:124-188) and the convergence test (solver.py:129-164).
+ *
+ * Every device entry point is asynchronous on the context's stream and never
+ * allocates user-visible memory (workspace lives in the context).
+ */
+#ifndef GCGB200_H
+#define GCGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GCG_OK = 0,
+  GCG_ERR_ARG = 1,     /* bad argument (maps to InvalidShape / InvalidRange)   */
+  GCG_ERR_CUDA = 2,    /* CUDA runtime error                                    */
+  GCG_ERR_SOLVER = 3,  /* dense eigensolver failure (maps to NoConvergence)     */
+  GCG_ERR_ALLOC = 4,   /* device allocation failed                              */
+  GCG_ERR_NODEV = 5    /* no CUDA device                                        */
+};
+
+#define GCG_ABI_VERSION 1
+
+int gcg_abi_version(void);
+const char* gcg_status_string(int status);
+
+/* ---- context ------------------------------------------------------------ */
+int gcg_ctx_create(void** ctx, void* cuda_stream);
+int gcg_ctx_destroy(void* ctx);
+int gcg_ctx_set_stream(void* ctx, void* cuda_stream);
+int gcg_ctx_sync(void* ctx);
+/* number of kernels this library has launched since load (instrumentation) */
+int64_t gcg_launch_count(void);
+
+/* ---- tier 1: reference-FFI mirror (host buffers, column-major) ----------- */
+/* out[:, c] = A @ x[:, c];  A is nrow x ncol CSR (int64 indptr/indices, f64 data);
+ * x is ncol x k with column stride ldx; out is nrow x k with column stride ldo. */
+int gcgeig_csr_matvec(const int64_t* indptr, const int64_t* indices, const double* data,
+                      int64_t nrow, int64_t ncol, const double* x, int64_t k, int64_t ldx,
+                      double* out, int64_t ldo);
+/* out[r*out_rs + c*out_cs] = sum_i x[i + r*ldx] * y[i + c*ldy]  (x: n x kx, y: n x ky).
+ * Always bit-stable run to run; `chunk`/`deterministic` are accepted for interface parity. */
+int gcgeig_inner_product(const double* x, int64_t n, int64_t kx, int64_t ldx, const double* y,
+                         int64_t ky, int64_t ldy, double* out, int64_t out_rs, int64_t out_cs,
+                         int64_t chunk, int deterministic);
+/* y <- alpha x + beta y on n x k column-major blocks; beta == 0 never reads y. */
+int gcgeig_axpby(double alpha, const double* x, int64_t n, int64_t k, int64_t ldx, double beta,
+                 double* y, int64_t ldy);
+
+/* ---- tier 2: device ops --------------------------------------------------- */
+/* Y = alpha*(A X) + gamma*Z + beta*Yin, rows 0..n-1, k columns; A is CSR with
+ * int32 indices.  beta == 0 never reads Yin; gamma == 0 never reads Z.
+ * dot_mode 0: none; 1: dots[c] = sum_i Y[i,c] W[i,c]; 2: dots[c] = sum_i Y[i,c]^2
+ * (deterministic fixed-order reduction). */
+int gcg_spmm_csr(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                 const double* val, int64_t k, const double* X, int64_t ldx, double alpha,
+                 double gamma, const double* Z, int64_t ldz, double beta, const double* Yin,
+                 int64_t ldyin, double* Y, int64_t ldy, int dot_mode, const double* W,
+                 int64_t ldw, double* dots);
+
+/* G[r*g_rs + c*g_cs] = alpha * sum_i X[i,r] Y[i,c] + beta * G[...]  (beta == 0: no read)
+ * optional fused column dots: dots[c] = sum_i T[i,c] Y[i,c] (T may equal Y). */
+int gcg_gram(void* ctx, int64_t n, int64_t k1, int64_t k2, const double* X, int64_t ldx,
+             const double* Y, int64_t ldy, double alpha, double beta, double* G, int64_t g_rs,
+             int64_t g_cs, const double* T, int64_t ldt, double* dots);
+
+/* Y = alpha * X C + beta * Y;  X: n x m, C: m x d (row-major, ldc), Y: n x d.
+ * Y must not overlap X. */
+int gcg_lincomb(void* ctx, int64_t n, int64_t m, int64_t d, double alpha, const double* X,
+                int64_t ldx, const double* C, int64_t ldc, double beta, double* Y, int64_t ldy);
+
+/* Y = alpha X + beta Y (n x k); beta == 0 never reads Y. */
+int gcg_axpby(void* ctx, int64_t n, int64_t k, double alpha, const double* X, int64_t ldx,
+              double beta, double* Y, int64_t ldy);
+/* Y = X (n x k strided copy). */
+int gcg_copy(void* ctx, int64_t n, int64_t k, const double* X, int64_t ldx, double* Y,
+             int64_t ldy);
+/* X[:, c] *= s[c]  (s on device) */
+int gcg_col_scale(void* ctx, int64_t n, int64_t k, const double* s, double* X, int64_t ldx);
+/* out[c] = sum_i X[i,c] Y[i,c] */
+int gcg_col_dots(void* ctx, int64_t n, int64_t k, const double* X, int64_t ldx, const double* Y,
+                 int64_t ldy, double* out);
+/* fill n x k with 0 */
+int gcg_fill(void* ctx, int64_t n, int64_t k, double value, double* X, int64_t ldx);
+
+/* Block CG on op = A + diag_shift*I (A = the shifted-value CSR A - theta*B when B is
+ * stored on A's pattern).  x holds x0 on entry and the iterate on exit.  Per column:
+ * stop at rel_tol*||r0|| or after max_iters sweeps, freeze on p'op p <= 0 (cg.py:33-99).
+ * Outputs stay on device: *d_sweeps, d_converged[k], d_frozen[k], d_relres[k]. */
+int gcg_block_cg(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                 const double* val, double diag_shift, int64_t k, const double* rhs,
+                 int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
+                 int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres);
+
+/* ---- small dense (device, row-major) -------------------------------------- */
+/* full symmetric eigendecomposition: w ascending, V[:, j] its eigenvector with the
+ * largest-|entry| made positive (dense.py:63-82).  A is read only. */
+int gcg_syev(void* ctx, int64_t m, const double* A, int64_t lda, double* w, double* V,
+             int64_t ldv);
+/* C = alpha op(A) op(B) + beta C, op = transpose when t* != 0. */
+int gcg_dgemm(void* ctx, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+              double* C, int64_t ldc);
+/* A <- (A + A^T)/2 */
+int gcg_symmetrize(void* ctx, int64_t m, double* A, int64_t lda);
+
+/* Leaf SVQB step (orth.py:155-188) for a w x w Gram block G:
+ *   status[0] = max|G - I|, status[1] = #eigenvalues <= dep_tol*max(lambda_max,0),
+ *   status[2] = lambda_max; Q (w x (w - nbad)) = V[:, nbad:] / sqrt(lambda[nbad:]). */
+int gcg_svqb_prepare(void* ctx, int64_t w, const double* G, int64_t ldg, double dep_tol,
+                     double* Q, int64_t ldq, double* status);
+/* Deflation repeat test (orth.py:146-152): R is K x w coefficients, dnew[w] squared norms.
+ *   status[0] = max|R|, status[1] = any(sum_r R[r,c]^2 > dgks * max(dnew[c], 1e-300)). */
+int gcg_deflate_status(void* ctx, int64_t K, int64_t w, const double* R, int64_t ldr,
+                       const double* dnew, int64_t dstride, double dgks, double* status);
+/* out = #{ j : vals[j] <= rel * max(max(vals), 0) } written as a double. */
+int gcg_count_le(void* ctx, int64_t len, const double* vals, double rel, double* out);
+/* out[:, j] = V[:, off + j] / sqrt(w[off + j]) for j < m - off. */
+int gcg_scale_rsqrt(void* ctx, int64_t m, int64_t off, const double* V, int64_t ldv,
+                    const double* w, double* out, int64_t ldo);
+
+/* Structured projected matrix (solver.py:281-290): Abar (m x m, m = d + np + nw) =
+ *   [diag(lam[0:d]) 0 cross[0:d]; 0 Pc cross[d:d+np]; cross^T] then (Abar + Abar^T)/2,
+ * where cross is m x nw (row-major, ldc) and Pc is np x np (ldp). */
+int gcg_abar_assemble(void* ctx, int64_t d, int64_t np, int64_t nw, const double* lam,
+                      const double* Pc, int64_t ldp, const double* cross, int64_t ldc,
+                      double* Abar, int64_t lda);
+/* out[0] = max |A - B| over an m x n block (B == NULL: B = identity). */
+int gcg_max_abs_diff(void* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* out);
+
+/* Ritz residuals (solver.py:129-141): per column j,
+ *   mode 0: ||AX - lam X|| / ||X||                        (reference, B = I)
+ *   mode 1: ||AX - lam BX|| / (lam^+ sqrt(X'BX))          (reference, generalized)
+ *   mode 2: ||AX - lam BX|| / (|lam| ||BX||)              (north-star criterion)
+ * BX may equal X (B = I). */
+int gcg_ritz_residuals(void* ctx, int64_t n, int64_t k, const double* AX, int64_t ldax,
+                       const double* X, int64_t ldx, const double* BX, int64_t ldbx,
+                       const double* lam, int mode, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GCGB200_H */

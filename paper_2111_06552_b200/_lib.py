@@ -1,0 +1,105 @@
+"""ctypes binding of libgcgb200.so (the C ABI in include/gcgb200.h).
+
+The library is the only compute path of this package: if it is missing, or
+there is no CUDA device, every entry point raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import GcgError, InvalidShape, NoConvergence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgcgb200.so")
+
+_i64, _i32, _dbl, _ptr, _int = C.c_int64, C.c_int32, C.c_double, C.c_void_p, C.c_int
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+_SIGS = {
+    "gcg_abi_version": [],
+    "gcg_status_string": [_int],
+    "gcg_launch_count": [],
+    "gcg_ctx_create": [C.POINTER(_ptr), _ptr],
+    "gcg_ctx_destroy": [_ptr],
+    "gcg_ctx_set_stream": [_ptr, _ptr],
+    "gcg_ctx_sync": [_ptr],
+    "gcgeig_csr_matvec": [_ptr, _ptr, _ptr, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64],
+    "gcgeig_inner_product": [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _int],
+    "gcgeig_axpby": [_dbl, _ptr, _i64, _i64, _i64, _dbl, _ptr, _i64],
+    "gcg_spmm_csr": [_ptr, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _dbl,
+                     _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
+    "gcg_gram": [_ptr, _i64, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _i64, _ptr,
+                 _i64, _ptr],
+    "gcg_lincomb": [_ptr, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64],
+    "gcg_axpby": [_ptr, _i64, _i64, _dbl, _ptr, _i64, _dbl, _ptr, _i64],
+    "gcg_copy": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64],
+    "gcg_col_scale": [_ptr, _i64, _i64, _ptr, _ptr, _i64],
+    "gcg_col_dots": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr],
+    "gcg_fill": [_ptr, _i64, _i64, _dbl, _ptr, _i64],
+    "gcg_block_cg": [_ptr, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64, _i32, _dbl,
+                     _ptr, _ptr, _ptr, _ptr],
+    "gcg_syev": [_ptr, _i64, _ptr, _i64, _ptr, _ptr, _i64],
+    "gcg_dgemm": [_ptr, _int, _int, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr,
+                  _i64],
+    "gcg_symmetrize": [_ptr, _i64, _ptr, _i64],
+    "gcg_svqb_prepare": [_ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64, _ptr],
+    "gcg_deflate_status": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _ptr],
+    "gcg_abar_assemble": [_ptr, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64, _ptr, _i64],
+    "gcg_max_abs_diff": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr],
+    "gcg_count_le": [_ptr, _i64, _ptr, _dbl, _ptr],
+    "gcg_scale_rsqrt": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _ptr, _i64],
+    "gcg_ritz_residuals": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
+}
+_RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+class LibraryMissing(GcgError):
+    """libgcgb200.so is not built or cannot be loaded (no CPU fallback exists)."""
+
+
+def load(path=LIB_PATH):
+    """Load and type the shared library (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryMissing(
+            f"{path} not found: build it with `python -m paper_2111_06552_b200.build`"
+        )
+    lib = C.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPE.get(name, _int)
+    _lib = lib
+    return lib
+
+
+class DeviceError(GcgError):
+    """A CUDA runtime error inside the library."""
+
+
+def check(status, what=""):
+    if status == 0:
+        return
+    msg = load().gcg_status_string(status).decode()
+    text = f"{what}: {msg}" if what else msg
+    if status == 1:
+        raise InvalidShape(text)
+    if status == 3:
+        raise NoConvergence(text)
+    raise DeviceError(text)
+
+
+def call(name, *args):
+    check(getattr(load(), name)(*args), name)
+
+
+def launch_count():
+    return int(load().gcg_launch_count())

@@ -1,0 +1,510 @@
+// extern "C" boundary of libgcgb200.so (declared in include/gcgb200.h).
+//
+// No C++ exception crosses this boundary; every entry point returns an int
+// status.  The device tier is asynchronous on the context stream; the
+// reference-FFI tier (gcgeig_*) is synchronous, like the reference's own
+// kernel-backend calls (_cy.pyx:11-65).
+
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gcg {
+
+extern int64_t g_launches;
+
+int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
+                     const double* val, int k, const double* X, long long ldx, double alpha,
+                     double gamma, const double* Z, long long ldz, double beta, const double* Yin,
+                     long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
+                     long long ldw, double* dots, double* partials_ext, int* grid_out,
+                     const int* skip);
+int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                const double* Y, long long ldy, double alpha, double beta, double* G,
+                long long grs, long long gcs);
+int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
+                   long long ldx, const double* C, long long ldc, double beta, double* Y,
+                   long long ldy);
+int axpby_launch(Ctx* c, long long n, int k, double alpha, const double* X, long long ldx,
+                 double beta, double* Y, long long ldy);
+int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, double* Y,
+                long long ldy);
+int fill_launch(Ctx* c, long long n, int k, double v, double* Y, long long ldy);
+int col_scale_launch(Ctx* c, long long n, int k, const double* s, double* X, long long ldx);
+int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, const double* Y,
+                    long long ldy, double* out);
+int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, const double* A,
+                 long long lda, const double* B, long long ldb, double beta, double* C,
+                 long long ldc);
+int symmetrize_launch(Ctx* c, int m, double* A, long long lda);
+int block_cg_launch(Ctx* c, long long n, const int* rowptr, const int* colidx, const double* val,
+                    double shift, int k, const double* rhs, long long ldr, double* x,
+                    long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
+                    int8_t* d_frozen, double* d_relres);
+int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+                        long long ldq, double* status);
+int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
+                          const double* dnew, long long dstride, double dgks, double* status);
+int abar_assemble_launch(Ctx* c, int d, int np, int nw, const double* lam, const double* Pc,
+                         long long ldp, const double* cross, long long ldc, double* Abar,
+                         long long lda);
+int max_abs_diff_launch(Ctx* c, int m, int n, const double* A, long long lda, const double* B,
+                        long long ldb, double* out);
+int count_le_launch(Ctx* c, int len, const double* vals, double rel, double* out);
+int scale_rsqrt_launch(Ctx* c, int m, int off, const double* V, long long ldv, const double* w,
+                       double* out, long long ldo);
+int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long long ldax,
+                          const double* X, long long ldx, const double* BX, long long ldbx,
+                          const double* lam, int mode, double* out);
+
+int ensure(Scratch& s, size_t bytes) {
+  if (bytes <= s.bytes) return GCG_OK;
+  // the scratch may still be in use by queued work on any stream of this ctx
+  cudaDeviceSynchronize();
+  if (s.ptr) cudaFree(s.ptr);
+  s.ptr = nullptr;
+  s.bytes = 0;
+  size_t want = bytes + bytes / 4 + 4096;
+  if (cudaMalloc(&s.ptr, want) != cudaSuccess) {
+    cudaGetLastError();
+    return GCG_ERR_ALLOC;
+  }
+  s.bytes = want;
+  return GCG_OK;
+}
+
+static void release(Scratch& s) {
+  if (s.ptr) cudaFree(s.ptr);
+  s.ptr = nullptr;
+  s.bytes = 0;
+}
+
+// --- transposes used by the column-major reference-FFI tier ----------------
+// out_rm[i*k + c] = in_cm[i + c*ld]
+__global__ void cm_to_rm_kernel(long long n, int k, const double* in, long long ld, double* out) {
+  const long long tot = n * k;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / k;
+    const int c = (int)(e % k);
+    out[e] = in[i + (long long)c * ld];
+  }
+}
+// out_cm[i + c*n] = in_rm[i*k + c]
+__global__ void rm_to_cm_kernel(long long n, int k, const double* in, double* out) {
+  const long long tot = n * k;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const long long i = e % n;
+    out[e] = in[i * k + c];
+  }
+}
+__global__ void i64_to_i32_kernel(long long n, const long long* in, int* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = (int)in[e];
+}
+
+}  // namespace gcg
+
+using namespace gcg;
+
+#define CTX(p) reinterpret_cast<gcg::Ctx*>(p)
+
+extern "C" {
+
+int gcg_abi_version(void) { return GCG_ABI_VERSION; }
+
+const char* gcg_status_string(int status) {
+  switch (status) {
+    case GCG_OK: return "ok";
+    case GCG_ERR_ARG: return "invalid argument";
+    case GCG_ERR_CUDA: return "CUDA error";
+    case GCG_ERR_SOLVER: return "dense eigensolver failure";
+    case GCG_ERR_ALLOC: return "device allocation failed";
+    case GCG_ERR_NODEV: return "no CUDA device";
+    default: return "unknown status";
+  }
+}
+
+int64_t gcg_launch_count(void) { return g_launches; }
+
+int gcg_ctx_create(void** out, void* stream) {
+  if (!out) return GCG_ERR_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return GCG_ERR_NODEV;
+  }
+  Ctx* c = new (std::nothrow) Ctx();
+  if (!c) return GCG_ERR_ALLOC;
+  c->stream = (cudaStream_t)stream;
+  cudaGetDevice(&c->device);
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess &&
+      sms > 0)
+    c->num_sms = sms;
+  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) {
+    delete c;
+    return GCG_ERR_SOLVER;
+  }
+  cusolverDnSetStream(c->solver, c->stream);
+  *out = c;
+  return GCG_OK;
+}
+
+int gcg_ctx_destroy(void* p) {
+  Ctx* c = CTX(p);
+  if (!c) return GCG_OK;
+  cudaStreamSynchronize(c->stream);
+  release(c->partials);
+  release(c->eigwork);
+  release(c->cg);
+  release(c->host_tmp);
+  release(c->host_tmp2);
+  release(c->host_tmp3);
+  release(c->host_tmp4);
+  release(c->dense);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  delete c;
+  return GCG_OK;
+}
+
+int gcg_ctx_set_stream(void* p, void* stream) {
+  Ctx* c = CTX(p);
+  if (!c) return GCG_ERR_ARG;
+  c->stream = (cudaStream_t)stream;
+  cusolverDnSetStream(c->solver, c->stream);
+  return GCG_OK;
+}
+
+int gcg_ctx_sync(void* p) {
+  Ctx* c = CTX(p);
+  if (!c) return GCG_ERR_ARG;
+  return cuda_status(cudaStreamSynchronize(c->stream));
+}
+
+// ---- device tier ------------------------------------------------------------
+
+int gcg_spmm_csr(void* p, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                 const double* val, int64_t k, const double* X, int64_t ldx, double alpha,
+                 double gamma, const double* Z, int64_t ldz, double beta, const double* Yin,
+                 int64_t ldyin, double* Y, int64_t ldy, int dot_mode, const double* W,
+                 int64_t ldw, double* dots) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || (n > 0 && (!rowptr || !X || !Y))) return GCG_ERR_ARG;
+  if (ldx < k || ldy < k) return GCG_ERR_ARG;
+  if (gamma != 0.0 && !Z) return GCG_ERR_ARG;
+  if (beta != 0.0 && !Yin) return GCG_ERR_ARG;
+  if (dot_mode < 0 || dot_mode > 2 || (dot_mode && !dots) || (dot_mode == 1 && !W))
+    return GCG_ERR_ARG;
+  return spmm_launch_impl(c, n, rowptr, colidx, val, (int)k, X, ldx, alpha, gamma, Z, ldz, beta,
+                          Yin, ldyin, Y, ldy, dot_mode, W, ldw, dots, nullptr, nullptr, nullptr);
+}
+
+int gcg_gram(void* p, int64_t n, int64_t k1, int64_t k2, const double* X, int64_t ldx,
+             const double* Y, int64_t ldy, double alpha, double beta, double* G, int64_t g_rs,
+             int64_t g_cs, const double* T, int64_t ldt, double* dots) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k1 < 0 || k2 < 0 || ldx < k1 || ldy < k2) return GCG_ERR_ARG;
+  if (k1 > 0 && k2 > 0 && !G) return GCG_ERR_ARG;
+  if (n == 0) {
+    // empty contraction: G = beta * G
+    if (k1 > 0 && k2 > 0) {
+      if (g_cs == 1) GCG_TRY(axpby_launch(c, k1, (int)k2, 0.0, G, g_rs, beta, G, g_rs));
+      else GCG_TRY(axpby_launch(c, k2, (int)k1, 0.0, G, g_cs, beta, G, g_cs));
+    }
+    if (dots) GCG_TRY(fill_launch(c, 1, (int)k2, 0.0, dots, k2));
+    return GCG_OK;
+  }
+  GCG_TRY(gram_launch(c, n, (int)k1, (int)k2, X, ldx, Y, ldy, alpha, beta, G, g_rs, g_cs));
+  if (dots) GCG_TRY(col_dots_launch(c, n, (int)k2, T ? T : Y, T ? ldt : ldy, Y, ldy, dots));
+  return GCG_OK;
+}
+
+int gcg_lincomb(void* p, int64_t n, int64_t m, int64_t d, double alpha, const double* X,
+                int64_t ldx, const double* C, int64_t ldc, double beta, double* Y, int64_t ldy) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || m < 0 || d < 0 || ldx < m || ldc < d || ldy < d) return GCG_ERR_ARG;
+  if (m == 0) {
+    if (beta == 0.0) return fill_launch(c, n, (int)d, 0.0, Y, ldy);
+    return axpby_launch(c, n, (int)d, 0.0, Y, ldy, beta, Y, ldy);
+  }
+  return lincomb_launch(c, n, (int)m, (int)d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+}
+
+int gcg_axpby(void* p, int64_t n, int64_t k, double alpha, const double* X, int64_t ldx,
+              double beta, double* Y, int64_t ldy) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldy < k || (alpha != 0.0 && ldx < k)) return GCG_ERR_ARG;
+  return axpby_launch(c, n, (int)k, alpha, X, ldx, beta, Y, ldy);
+}
+
+int gcg_copy(void* p, int64_t n, int64_t k, const double* X, int64_t ldx, double* Y,
+             int64_t ldy) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldx < k || ldy < k) return GCG_ERR_ARG;
+  return copy_launch(c, n, (int)k, X, ldx, Y, ldy);
+}
+
+int gcg_col_scale(void* p, int64_t n, int64_t k, const double* s, double* X, int64_t ldx) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldx < k) return GCG_ERR_ARG;
+  return col_scale_launch(c, n, (int)k, s, X, ldx);
+}
+
+int gcg_col_dots(void* p, int64_t n, int64_t k, const double* X, int64_t ldx, const double* Y,
+                 int64_t ldy, double* out) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldx < k || ldy < k) return GCG_ERR_ARG;
+  return col_dots_launch(c, n, (int)k, X, ldx, Y, ldy, out);
+}
+
+int gcg_fill(void* p, int64_t n, int64_t k, double value, double* X, int64_t ldx) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldx < k) return GCG_ERR_ARG;
+  return fill_launch(c, n, (int)k, value, X, ldx);
+}
+
+int gcg_block_cg(void* p, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                 const double* val, double diag_shift, int64_t k, const double* rhs,
+                 int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
+                 int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres) {
+  Ctx* c = CTX(p);
+  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0)
+    return GCG_ERR_ARG;
+  if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
+  return block_cg_launch(c, n, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
+                         max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres);
+}
+
+int gcg_syev(void* p, int64_t m, const double* A, int64_t lda, double* w, double* V,
+             int64_t ldv) {
+  Ctx* c = CTX(p);
+  if (!c || m <= 0 || lda < m || ldv < m) return GCG_ERR_ARG;
+  if (m <= 64) return dense_syev_jacobi(c, (int)m, A, lda, w, V, ldv);
+  return dense_syev_cusolver(c, (int)m, A, lda, w, V, ldv);
+}
+
+int gcg_dgemm(void* p, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+              double* C, int64_t ldc) {
+  Ctx* c = CTX(p);
+  if (!c || M < 0 || N < 0 || K < 0 || ldc < N) return GCG_ERR_ARG;
+  return dgemm_launch(c, ta, tb, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+int gcg_symmetrize(void* p, int64_t m, double* A, int64_t lda) {
+  Ctx* c = CTX(p);
+  if (!c || m < 0 || lda < m) return GCG_ERR_ARG;
+  return symmetrize_launch(c, (int)m, A, lda);
+}
+
+int gcg_svqb_prepare(void* p, int64_t w, const double* G, int64_t ldg, double dep_tol,
+                     double* Q, int64_t ldq, double* status) {
+  Ctx* c = CTX(p);
+  if (!c || w <= 0 || ldg < w || ldq < w || !status) return GCG_ERR_ARG;
+  return svqb_prepare_launch(c, (int)w, G, ldg, dep_tol, Q, ldq, status);
+}
+
+int gcg_deflate_status(void* p, int64_t K, int64_t w, const double* R, int64_t ldr,
+                       const double* dnew, int64_t dstride, double dgks, double* status) {
+  Ctx* c = CTX(p);
+  if (!c || K < 0 || w < 0 || ldr < w || !status) return GCG_ERR_ARG;
+  return deflate_status_launch(c, (int)K, (int)w, R, ldr, dnew, dstride, dgks, status);
+}
+
+int gcg_abar_assemble(void* p, int64_t d, int64_t np, int64_t nw, const double* lam,
+                      const double* Pc, int64_t ldp, const double* cross, int64_t ldc,
+                      double* Abar, int64_t lda) {
+  Ctx* c = CTX(p);
+  const int64_t m = d + np + nw;
+  if (!c || d < 0 || np < 0 || nw < 0 || lda < m || (nw > 0 && ldc < nw) || (np > 0 && ldp < np))
+    return GCG_ERR_ARG;
+  return abar_assemble_launch(c, (int)d, (int)np, (int)nw, lam, Pc, ldp, cross, ldc, Abar, lda);
+}
+
+int gcg_max_abs_diff(void* p, int64_t m, int64_t n, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* out) {
+  Ctx* c = CTX(p);
+  if (!c || m < 0 || n < 0 || lda < n || (B && ldb < n) || !out) return GCG_ERR_ARG;
+  return max_abs_diff_launch(c, (int)m, (int)n, A, lda, B, ldb, out);
+}
+
+int gcg_count_le(void* p, int64_t len, const double* vals, double rel, double* out) {
+  Ctx* c = CTX(p);
+  if (!c || len < 0 || !out) return GCG_ERR_ARG;
+  return count_le_launch(c, (int)len, vals, rel, out);
+}
+
+int gcg_scale_rsqrt(void* p, int64_t m, int64_t off, const double* V, int64_t ldv,
+                    const double* w, double* out, int64_t ldo) {
+  Ctx* c = CTX(p);
+  if (!c || m < 0 || off < 0 || off > m || ldv < m || ldo < m - off) return GCG_ERR_ARG;
+  return scale_rsqrt_launch(c, (int)m, (int)off, V, ldv, w, out, ldo);
+}
+
+int gcg_ritz_residuals(void* p, int64_t n, int64_t k, const double* AX, int64_t ldax,
+                       const double* X, int64_t ldx, const double* BX, int64_t ldbx,
+                       const double* lam, int mode, double* out) {
+  Ctx* c = CTX(p);
+  if (!c || n <= 0 || k < 0 || k > 256 || mode < 0 || mode > 2) return GCG_ERR_ARG;
+  return ritz_residuals_launch(c, n, (int)k, AX, ldax, X, ldx, BX, ldbx, lam, mode, out);
+}
+
+// ---- reference-FFI tier (host buffers) --------------------------------------
+
+static std::mutex g_host_mu;
+static Ctx* g_host_ctx = nullptr;
+
+static int host_ctx(Ctx** out) {
+  if (!g_host_ctx) {
+    void* p = nullptr;
+    int s = gcg_ctx_create(&p, nullptr);
+    if (s != GCG_OK) return s;
+    g_host_ctx = CTX(p);
+  }
+  *out = g_host_ctx;
+  return GCG_OK;
+}
+
+static int h2d_cm(Ctx* c, const double* host, long long rows, long long cols, long long ld,
+                  double* dev) {
+  // pack a column-major host block (rows x cols, column stride ld) densely
+  if (rows == 0 || cols == 0) return GCG_OK;
+  return cuda_status(cudaMemcpy2DAsync(dev, rows * sizeof(double), host, ld * sizeof(double),
+                                       rows * sizeof(double), cols, cudaMemcpyHostToDevice,
+                                       c->stream));
+}
+
+static int d2h_cm(Ctx* c, const double* dev, long long rows, long long cols, double* host,
+                  long long ld) {
+  if (rows == 0 || cols == 0) return GCG_OK;
+  return cuda_status(cudaMemcpy2DAsync(host, ld * sizeof(double), dev, rows * sizeof(double),
+                                       rows * sizeof(double), cols, cudaMemcpyDeviceToHost,
+                                       c->stream));
+}
+
+static int elem_grid_host(Ctx* c, long long tot) { return grid_for(tot, 1024, 8, c->num_sms); }
+
+int gcgeig_csr_matvec(const int64_t* indptr, const int64_t* indices, const double* data,
+                      int64_t nrow, int64_t ncol, const double* x, int64_t k, int64_t ldx,
+                      double* out, int64_t ldo) {
+  if (nrow < 0 || ncol < 0 || k < 0 || ldx < ncol || ldo < nrow) return GCG_ERR_ARG;
+  if (nrow == 0 || k == 0) return GCG_OK;
+  const long long nnz = indptr[nrow] - indptr[0];
+  if (indptr[0] != 0 || nnz < 0 || nnz >= (1LL << 31) || ncol >= (1LL << 31)) return GCG_ERR_ARG;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  Ctx* c;
+  GCG_TRY(host_ctx(&c));
+  // staging: indptr/indices as int64 then int32; values; x (cm, rm); y (rm, cm)
+  const size_t b_idx = sizeof(long long) * ((size_t)nrow + 1 + (size_t)nnz);
+  const size_t b_i32 = sizeof(int) * ((size_t)nrow + 1 + (size_t)nnz);
+  const size_t b_val = sizeof(double) * (size_t)(nnz > 0 ? nnz : 1);
+  const size_t b_x = sizeof(double) * (size_t)ncol * k;
+  const size_t b_y = sizeof(double) * (size_t)nrow * k;
+  GCG_TRY(ensure(c->host_tmp, b_idx + b_i32 + b_val + 64));
+  GCG_TRY(ensure(c->host_tmp2, 2 * b_x + 64));
+  GCG_TRY(ensure(c->host_tmp3, 2 * b_y + 64));
+  char* base = (char*)c->host_tmp.ptr;
+  long long* d_i64 = (long long*)base;
+  int* d_i32 = (int*)(base + b_idx);
+  double* d_val = (double*)(base + b_idx + b_i32 + (8 - (b_idx + b_i32) % 8) % 8);
+  double* d_xcm = (double*)c->host_tmp2.ptr;
+  double* d_xrm = d_xcm + (size_t)ncol * k;
+  double* d_yrm = (double*)c->host_tmp3.ptr;
+  double* d_ycm = d_yrm + (size_t)nrow * k;
+  cudaStream_t s = c->stream;
+  GCG_TRY(cuda_status(cudaMemcpyAsync(d_i64, indptr, sizeof(long long) * (nrow + 1),
+                                      cudaMemcpyHostToDevice, s)));
+  if (nnz > 0) {
+    GCG_TRY(cuda_status(cudaMemcpyAsync(d_i64 + nrow + 1, indices, sizeof(long long) * nnz,
+                                        cudaMemcpyHostToDevice, s)));
+    GCG_TRY(cuda_status(
+        cudaMemcpyAsync(d_val, data, sizeof(double) * nnz, cudaMemcpyHostToDevice, s)));
+  }
+  const long long nidx = nrow + 1 + nnz;
+  i64_to_i32_kernel<<<elem_grid_host(c, nidx), 256, 0, s>>>(nidx, d_i64, d_i32);
+  ++g_launches;
+  GCG_TRY(h2d_cm(c, x, ncol, k, ldx, d_xcm));
+  cm_to_rm_kernel<<<elem_grid_host(c, ncol * k), 256, 0, s>>>(ncol, (int)k, d_xcm, ncol, d_xrm);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(spmm_launch_impl(c, nrow, d_i32, d_i32 + nrow + 1, d_val, (int)k, d_xrm, k, 1.0, 0.0,
+                           nullptr, 0, 0.0, nullptr, 0, d_yrm, k, 0, nullptr, 0, nullptr, nullptr,
+                           nullptr, nullptr));
+  rm_to_cm_kernel<<<elem_grid_host(c, nrow * k), 256, 0, s>>>(nrow, (int)k, d_yrm, d_ycm);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(d2h_cm(c, d_ycm, nrow, k, out, ldo));
+  return cuda_status(cudaStreamSynchronize(s));
+}
+
+int gcgeig_inner_product(const double* x, int64_t n, int64_t kx, int64_t ldx, const double* y,
+                         int64_t ky, int64_t ldy, double* out, int64_t out_rs, int64_t out_cs,
+                         int64_t chunk, int deterministic) {
+  (void)chunk;
+  (void)deterministic;  // the device reduction order is fixed: always bit-stable
+  if (n < 0 || kx < 0 || ky < 0 || ldx < n || ldy < n) return GCG_ERR_ARG;
+  if (kx == 0 || ky == 0) return GCG_OK;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  Ctx* c;
+  GCG_TRY(host_ctx(&c));
+  const size_t bx = (size_t)n * kx, by = (size_t)n * ky, bg = (size_t)kx * ky;
+  GCG_TRY(ensure(c->host_tmp2, sizeof(double) * (2 * bx + 8)));
+  GCG_TRY(ensure(c->host_tmp3, sizeof(double) * (2 * by + 8)));
+  GCG_TRY(ensure(c->host_tmp, sizeof(double) * (bg + 8)));
+  double* d_xcm = (double*)c->host_tmp2.ptr;
+  double* d_xrm = d_xcm + bx;
+  double* d_ycm = (double*)c->host_tmp3.ptr;
+  double* d_yrm = d_ycm + by;
+  double* d_g = (double*)c->host_tmp.ptr;
+  cudaStream_t s = c->stream;
+  GCG_TRY(h2d_cm(c, x, n, kx, ldx, d_xcm));
+  GCG_TRY(h2d_cm(c, y, n, ky, ldy, d_ycm));
+  if (n > 0) {
+    cm_to_rm_kernel<<<elem_grid_host(c, bx), 256, 0, s>>>(n, (int)kx, d_xcm, n, d_xrm);
+    cm_to_rm_kernel<<<elem_grid_host(c, by), 256, 0, s>>>(n, (int)ky, d_ycm, n, d_yrm);
+    g_launches += 2;
+    GCG_CHECK_LAUNCH();
+    GCG_TRY(gram_launch(c, n, (int)kx, (int)ky, d_xrm, kx, d_yrm, ky, 1.0, 0.0, d_g, ky, 1));
+  } else {
+    GCG_TRY(fill_launch(c, kx, (int)ky, 0.0, d_g, ky));
+  }
+  std::vector<double> g(bg);
+  GCG_TRY(cuda_status(
+      cudaMemcpyAsync(g.data(), d_g, sizeof(double) * bg, cudaMemcpyDeviceToHost, s)));
+  GCG_TRY(cuda_status(cudaStreamSynchronize(s)));
+  for (long long r = 0; r < kx; ++r)
+    for (long long cc = 0; cc < ky; ++cc) out[r * out_rs + cc * out_cs] = g[r * ky + cc];
+  return GCG_OK;
+}
+
+int gcgeig_axpby(double alpha, const double* x, int64_t n, int64_t k, int64_t ldx, double beta,
+                 double* y, int64_t ldy) {
+  if (n < 0 || k < 0 || ldx < n || ldy < n) return GCG_ERR_ARG;
+  if (n == 0 || k == 0) return GCG_OK;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  Ctx* c;
+  GCG_TRY(host_ctx(&c));
+  const size_t b = (size_t)n * k;
+  GCG_TRY(ensure(c->host_tmp2, sizeof(double) * (b + 8)));
+  GCG_TRY(ensure(c->host_tmp3, sizeof(double) * (b + 8)));
+  double* d_x = (double*)c->host_tmp2.ptr;
+  double* d_y = (double*)c->host_tmp3.ptr;
+  cudaStream_t s = c->stream;
+  GCG_TRY(h2d_cm(c, x, n, k, ldx, d_x));
+  if (beta != 0.0) GCG_TRY(h2d_cm(c, y, n, k, ldy, d_y));
+  // a packed column-major n x k block is a row-major k x n block with ld n
+  GCG_TRY(axpby_launch(c, k, (int)n, alpha, d_x, n, beta, d_y, n));
+  GCG_TRY(d2h_cm(c, d_y, n, k, y, ldy));
+  return cuda_status(cudaStreamSynchronize(s));
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Shared definitions for the gcgb200 CUDA library (sm_100a, fp64).
+//
+// Layout convention (B200 design): a multivector block is
+// ROW-MAJOR in HBM — element (row i, column c) lives at X[i * ld + c] — so a
+// CSR row gather reads one contiguous run of k doubles per neighbour and a
+// column range [c0, c0+k) of the arena is just the pointer X + c0 with the
+// same ld.  Small dense matrices (projected matrix, Ritz coefficients, Gram
+// blocks) are row-major too.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <stdint.h>
+
+#include "../../include/gcgb200.h"
+
+namespace gcg {
+
+constexpr int kNumSMs = 148;
+
+// Per-context scratch: grows monotonically, never shrinks during a solve.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  int num_sms = kNumSMs;
+  int device = 0;
+  // generic workspaces (slots are owned by one op at a time; ops on one ctx
+  // are stream-ordered so reuse across ops is safe)
+  Scratch partials;   // per-CTA partial sums for deterministic reductions
+  Scratch eigwork;    // cuSOLVER work + info
+  Scratch cg;         // block-CG vectors r, p, q and per-column state
+  Scratch host_tmp;   // device staging for the host-buffer (reference FFI) entry points
+  Scratch host_tmp2;
+  Scratch host_tmp3;
+  Scratch host_tmp4;
+  Scratch dense;      // small dense temporaries (eigensolver staging)
+  int* sync_flag = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+
+int ensure(Scratch& s, size_t bytes);
+
+inline int cuda_status(cudaError_t e) {
+  return e == cudaSuccess ? GCG_OK : GCG_ERR_CUDA;
+}
+
+#define GCG_CHECK_LAUNCH()                                  \
+  do {                                                      \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return GCG_ERR_CUDA;             \
+  } while (0)
+
+#define GCG_TRY(x)                                          \
+  do {                                                      \
+    int _s = (x);                                           \
+    if (_s != GCG_OK) return _s;                            \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// warp / block reduction helpers
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Grid sizing: a multiple of the SM count, capped by the work available.
+inline int grid_for(long long work_items, int items_per_cta, int ctas_per_sm, int num_sms) {
+  long long need = (work_items + items_per_cta - 1) / items_per_cta;
+  long long cap = (long long)num_sms * ctas_per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+// internal launchers shared between translation units
+int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* out,
+                    int out_stride, int mode);
+int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
+                      long long ldv);
+int dense_syev_cusolver(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
+                        long long ldv);
+
+}  // namespace gcg

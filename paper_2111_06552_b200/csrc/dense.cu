@@ -1,0 +1,618 @@
+// Small dense symmetric eigenproblems and the orthogonalisation / convergence
+// decision kernels, all on device (no CPU fallback).
+//
+// Reference: dense.py:63-133 (sym_eig_full / sym_eig_range / gram_svd via
+// LAPACK, eigenvalues ascending, each eigenvector's largest-|entry| made
+// positive, first index on ties), orth.py:155-188 (_leaf_svqb), orth.py:124-152
+// (_deflate_against repeat test), solver.py:129-164 (_rel_residual,
+// _count_converged).
+//
+// B200 design.  Orders <= 64 (SVQB leaves of width <= 16, the post-pass Gram
+// of a block of bs <= 64 columns, the momentum Gram) are solved by one CTA with
+// a parallel cyclic Jacobi sweep in shared memory (round-robin pairing, all
+// m/2 rotations of a round applied at once) — a few tens of microseconds, no
+// library call, fused with the SVQB bookkeeping so one kernel turns a Gram
+// block into the SVQB coefficient matrix plus a 3-double status record.
+// Larger orders (the Rayleigh-Ritz matrix, m <= 1000) use cuSOLVER syevd on
+// the context stream followed by an on-device transpose + sign fix.
+
+#include <math.h>
+
+#include "common.cuh"
+
+namespace gcg {
+
+extern int64_t g_launches;
+
+constexpr int kJacMax = 64;
+
+// Parallel cyclic Jacobi on a[mp][kJacMax+1] (symmetric), accumulating v.
+// mp is even; rows/cols >= m are zero padding.  All threads of the CTA call it.
+__device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJacMax + 1],
+                              double* cs, double* sn, int* pp, int* qq, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int half = mp / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    // convergence: off-diagonal mass vs diagonal mass
+    double off = 0.0, dia = 0.0;
+    for (int e = tid; e < mp * mp; e += nt) {
+      const int i = e / mp, j = e % mp;
+      const double x = a[i][j];
+      if (i == j) dia += x * x;
+      else off += x * x;
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if ((tid & 31) == 0) {
+      red[2 * (tid >> 5)] = off;
+      red[2 * (tid >> 5) + 1] = dia;
+    }
+    __syncthreads();
+    double toff = 0.0, tdia = 0.0;
+    for (int w = 0; w < nt / 32; ++w) {
+      toff += red[2 * w];
+      tdia += red[2 * w + 1];
+    }
+    __syncthreads();
+    if (toff <= 1e-30 * tdia || toff == 0.0) break;
+    for (int round = 0; round < mp - 1; ++round) {
+      if (tid < half) {
+        int p, q;
+        if (tid == 0) {
+          p = round;
+          q = mp - 1;
+        } else {
+          p = (round + tid) % (mp - 1);
+          q = (round - tid + mp - 1) % (mp - 1);
+        }
+        if (p > q) {
+          int t = p;
+          p = q;
+          q = t;
+        }
+        const double apq = a[p][q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double app = a[p][p], aqq = a[q][q];
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+        }
+        cs[tid] = c;
+        sn[tid] = s;
+        pp[tid] = p;
+        qq[tid] = q;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int e = tid; e < half * mp; e += nt) {
+        const int pr = e / mp, j = e % mp;
+        const int p = pp[pr], q = qq[pr];
+        const double c = cs[pr], s = sn[pr];
+        const double ap = a[p][j], aq = a[q][j];
+        a[p][j] = c * ap - s * aq;
+        a[q][j] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < half * mp; e += nt) {
+        const int pr = e / mp, i = e % mp;
+        const int p = pp[pr], q = qq[pr];
+        const double c = cs[pr], s = sn[pr];
+        const double ap = a[i][p], aq = a[i][q];
+        a[i][p] = c * ap - s * aq;
+        a[i][q] = s * ap + c * aq;
+        const double vp = v[i][p], vq = v[i][q];
+        v[i][p] = c * vp - s * vq;
+        v[i][q] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Sort eigenpairs ascending (stable by index) and apply the sign rule;
+// writes w[m] and V (row-major, ldv) from a/v (m x m, padded).
+__device__ void sort_and_sign(int m, double (*a)[kJacMax + 1], double (*v)[kJacMax + 1],
+                              double* wout, double* Vout, long long ldv, int* rank) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < m; i += nt) {
+    const double di = a[i][i];
+    int r = 0;
+    for (int j = 0; j < m; ++j) {
+      const double dj = a[j][j];
+      r += (dj < di) || (dj == di && j < i);
+    }
+    rank[i] = r;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += nt) {
+    const int r = rank[i];
+    wout[r] = a[i][i];
+    // sign rule on source column i
+    int lead = 0;
+    double best = -1.0;
+    for (int row = 0; row < m; ++row) {
+      const double x = fabs(v[row][i]);
+      if (x > best) {
+        best = x;
+        lead = row;
+      }
+    }
+    const double sg = v[lead][i] < 0.0 ? -1.0 : 1.0;
+    for (int row = 0; row < m; ++row) Vout[(long long)row * ldv + r] = sg * v[row][i];
+  }
+  __syncthreads();
+}
+
+struct JacSmem {
+  double a[kJacMax][kJacMax + 1];
+  double v[kJacMax][kJacMax + 1];
+  double cs[kJacMax / 2], sn[kJacMax / 2];
+  int pp[kJacMax / 2], qq[kJacMax / 2];
+  int rank[kJacMax];
+  double red[64];
+  double w[kJacMax];
+  double Vs[kJacMax * kJacMax];
+};
+
+__device__ void jac_load(JacSmem& S, int m, int mp, const double* A, long long lda, bool sym) {
+  for (int e = threadIdx.x; e < mp * mp; e += blockDim.x) {
+    const int i = e / mp, j = e % mp;
+    double x = 0.0;
+    if (i < m && j < m) {
+      x = A[(long long)i * lda + j];
+      if (sym) x = (x + A[(long long)j * lda + i]) / 2.0;
+    }
+    S.a[i][j] = x;
+    S.v[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) syev_jacobi_kernel(int m, const double* A, long long lda,
+                                                          double* w, double* V, long long ldv) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  JacSmem& S = *reinterpret_cast<JacSmem*>(smraw);
+  const int mp = (m + 1) & ~1;
+  jac_load(S, m, mp, A, lda, false);
+  jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
+  sort_and_sign(m, S.a, S.v, w, V, ldv, S.rank);
+}
+
+int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
+                      long long ldv) {
+  if (m <= 0 || m > kJacMax) return GCG_ERR_ARG;
+  const size_t sm = sizeof(JacSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(syev_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  syev_jacobi_kernel<<<1, 256, sm, c->stream>>>(m, A, lda, w, V, ldv);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SVQB leaf step, fused (orth.py:155-188): defect of the raw Gram, Jacobi on
+// its symmetric part, dependence count and the coefficient matrix
+// Q = V[:, nbad:] / sqrt(lambda[nbad:]).
+__global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* G, long long ldg,
+                                                           double dep_tol, double* Q,
+                                                           long long ldq, double* status) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  JacSmem& S = *reinterpret_cast<JacSmem*>(smraw);
+  const int mp = (m + 1) & ~1;
+  // defect = max |G - I| on the raw (unsymmetrised) Gram
+  double dmax = 0.0;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e % m;
+    dmax = fmax(dmax, fabs(G[(long long)i * ldg + j] - (i == j ? 1.0 : 0.0)));
+  }
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t = fmax(t, S.red[w]);
+    status[0] = t;
+  }
+  __syncthreads();
+  jac_load(S, m, mp, G, ldg, true);
+  jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
+  sort_and_sign(m, S.a, S.v, S.w, S.Vs, m, S.rank);
+  __shared__ int nbad_s;
+  if (threadIdx.x == 0) {
+    const double wmax = S.w[m - 1];
+    const double floor = dep_tol * fmax(wmax, 0.0);
+    int nb = 0;
+    while (nb < m && S.w[nb] <= floor) ++nb;  // searchsorted(..., side="right")
+    nbad_s = nb;
+    status[1] = (double)nb;
+    status[2] = wmax;
+  }
+  __syncthreads();
+  const int nb = nbad_s;
+  const int kept = m - nb;
+  for (int e = threadIdx.x; e < m * kept; e += blockDim.x) {
+    const int i = e / kept, j = e % kept;
+    Q[(long long)i * ldq + j] = S.Vs[i * m + nb + j] / sqrt(S.w[nb + j]);
+  }
+}
+
+int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+                       long long ldq, double* status) {
+  const size_t sm = sizeof(JacSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svqb_prepare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr = true;
+  }
+  svqb_prepare_kernel<<<1, 256, sm, c->stream>>>(m, G, ldg, dep_tol, Q, ldq, status);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cuSOLVER path for larger orders
+
+__global__ void sym_copy_kernel(int m, const double* A, long long lda, double* B, int sym,
+                                double* status) {
+  // B (dense m x m, ld m) = A or (A + A^T)/2 ; optional defect max|A - I| into status[0]
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)m * m) return;
+  const int i = (int)(e / m), j = (int)(e % m);
+  const double x = A[(long long)i * lda + j];
+  B[e] = sym ? (x + A[(long long)j * lda + i]) / 2.0 : x;
+}
+
+__global__ void max_offeye_kernel(int m, const double* A, long long lda, double* out) {
+  double dmax = 0.0;
+  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    dmax = fmax(dmax, fabs(A[(long long)i * lda + j] - (i == j ? 1.0 : 0.0)));
+  }
+  dmax = warp_max(dmax);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t = fmax(t, red[w]);
+    *out = t;
+  }
+}
+
+// V_out[i*ldv + j] = sign_j * Vcm[i + j*m]  (sign rule per column j)
+__global__ void vec_fix_kernel(int m, const double* Vcm, double* V, long long ldv) {
+  const int j = blockIdx.x;
+  const double* col = Vcm + (long long)j * m;
+  double best = -1.0;
+  int lead = 0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = fabs(col[i]);
+    if (x > best) {  // strict: first index wins within a thread
+      best = x;
+      lead = i;
+    }
+  }
+  __shared__ double bv[256];
+  __shared__ int bi[256];
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = lead;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double o = bv[threadIdx.x + w];
+      const int oi = bi[threadIdx.x + w];
+      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = o;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  const double sg = col[bi[0]] < 0.0 ? -1.0 : 1.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) V[(long long)i * ldv + j] = sg * col[i];
+}
+
+int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int symmetrize,
+                            double* w, double* V, long long ldv) {
+  if (m <= 0) return GCG_ERR_ARG;
+  cusolverDnSetStream(c->solver, c->stream);
+  int lwork = 0;
+  const size_t mat = (size_t)m * m;
+  GCG_TRY(ensure(c->dense, sizeof(double) * mat + 64));
+  double* B = (double*)c->dense.ptr;
+  if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                                  B, m, w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return GCG_ERR_SOLVER;
+  GCG_TRY(ensure(c->eigwork, sizeof(double) * ((size_t)lwork + 8)));
+  double* work = (double*)c->eigwork.ptr;
+  int* info = (int*)(work + lwork);
+  sym_copy_kernel<<<(unsigned)((mat + 255) / 256), 256, 0, c->stream>>>(m, A, lda, B, symmetrize,
+                                                                        nullptr);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  if (cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m, w,
+                       work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    return GCG_ERR_SOLVER;
+  // row-major symmetric input == its column-major transpose, so B now holds
+  // eigenvector j in column-major column j
+  vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, B, V, ldv);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+int dense_syev_cusolver(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
+                        long long ldv) {
+  return dense_syev_cusolver_sym(c, m, A, lda, 0, w, V, ldv);
+}
+
+// count of vals[j] <= rel * max(max(vals), 0)  (vals ascending; searchsorted side=right)
+__global__ void count_le_kernel(int len, const double* vals, double rel, double* out) {
+  __shared__ double red[32];
+  double mx = -INFINITY;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, vals[i]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;  // max(values.max(initial=0.0), 0.0)
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t = fmax(t, red[w]);
+    const double floor = rel * fmax(t, 0.0);
+    int nb = 0;
+    while (nb < len && vals[nb] <= floor) ++nb;
+    out[0] = (double)nb;
+    out[1] = t;
+  }
+}
+
+// out[i, j] = V[i, off + j] / sqrt(w[off + j])
+__global__ void scale_rsqrt_kernel(int m, int off, const double* V, long long ldv,
+                                   const double* w, double* out, long long ldo) {
+  const int kept = m - off;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)m * kept) return;
+  const int i = (int)(e / kept), j = (int)(e % kept);
+  out[(long long)i * ldo + j] = V[(long long)i * ldv + off + j] / sqrt(w[off + j]);
+}
+
+__global__ void scale_rsqrt_devoff_kernel(int m, const double* offp, const double* V,
+                                          long long ldv, const double* w, double* out,
+                                          long long ldo) {
+  const int off = (int)offp[0];
+  const int kept = m - off;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kept <= 0 || e >= (long long)m * kept) return;
+  const int i = (int)(e / kept), j = (int)(e % kept);
+  out[(long long)i * ldo + j] = V[(long long)i * ldv + off + j] / sqrt(w[off + j]);
+}
+
+int count_le_launch(Ctx* c, int len, const double* vals, double rel, double* out) {
+  count_le_kernel<<<1, 256, 0, c->stream>>>(len, vals, rel, out);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+int scale_rsqrt_launch(Ctx* c, int m, int off, const double* V, long long ldv, const double* w,
+                       double* out, long long ldo) {
+  const long long tot = (long long)m * (m - off);
+  if (tot <= 0) return GCG_OK;
+  scale_rsqrt_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(m, off, V, ldv, w, out,
+                                                                           ldo);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+                        long long ldq, double* status) {
+  if (m <= kJacMax) return svqb_prepare_small(c, m, G, ldg, dep_tol, Q, ldq, status);
+  // large leaf: defect, cuSOLVER on the symmetric part, count, scale
+  max_offeye_kernel<<<1, 256, 0, c->stream>>>(m, G, ldg, status);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  const size_t mat = (size_t)m * m;
+  // V + w staging after the solver's own matrix in a separate scratch
+  GCG_TRY(ensure(c->host_tmp4, sizeof(double) * (mat + m)));
+  double* V = (double*)c->host_tmp4.ptr;
+  double* w = V + mat;
+  GCG_TRY(dense_syev_cusolver_sym(c, m, G, ldg, 1, w, V, m));
+  GCG_TRY(count_le_launch(c, m, w, dep_tol, status + 1));
+  // Q = V[:, nbad:] / sqrt(w[nbad:]) with nbad read on device from status[1]
+  scale_rsqrt_devoff_kernel<<<(unsigned)((mat + 255) / 256), 256, 0, c->stream>>>(
+      m, status + 1, V, m, w, Q, ldq);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+// deflation repeat test (orth.py:138-152)
+__global__ void deflate_status_kernel(int K, int w, const double* R, long long ldr,
+                                      const double* dnew, long long dstride, double dgks,
+                                      double* status) {
+  __shared__ double red[32];
+  __shared__ int anyf;
+  if (threadIdx.x == 0) anyf = 0;
+  double mx = 0.0;
+  for (long long e = threadIdx.x; e < (long long)K * w; e += blockDim.x)
+    mx = fmax(mx, fabs(R[(e / w) * ldr + (e % w)]));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  for (int col = threadIdx.x; col < w; col += blockDim.x) {
+    double lost = 0.0;
+    for (int r = 0; r < K; ++r) {
+      const double x = R[(long long)r * ldr + col];
+      lost += x * x;
+    }
+    if (lost > dgks * fmax(dnew[col * dstride], 1e-300)) atomicExch(&anyf, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)blockDim.x / 32; ++q) t = fmax(t, red[q]);
+    status[0] = t;
+    status[1] = (double)anyf;
+  }
+}
+
+int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
+                          const double* dnew, long long dstride, double dgks, double* status) {
+  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// structured projected matrix (solver.py:281-290) + symmetrisation
+__global__ void abar_assemble_kernel(int d, int np, int nw, const double* lam, const double* Pc,
+                                     long long ldp, const double* cross, long long ldc,
+                                     double* A, long long lda) {
+  const int m = d + np + nw;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)m * m) return;
+  const int i = (int)(e / m), j = (int)(e % m);
+  auto raw = [&](int r, int cc) -> double {
+    if (cc >= d + np) return cross[(long long)r * ldc + (cc - d - np)];
+    if (r >= d + np) return cross[(long long)cc * ldc + (r - d - np)];
+    if (r < d && cc < d) return r == cc ? lam[r] : 0.0;
+    if (r >= d && cc >= d) return Pc[(long long)(r - d) * ldp + (cc - d)];
+    return 0.0;
+  };
+  // abar[d+np:, :] = cross.T overrides the cross rows (solver.py:288-289), then (A + A^T)/2
+  const double a = raw(i, j), b = raw(j, i);
+  A[(long long)i * lda + j] = (a + b) / 2.0;
+}
+
+int abar_assemble_launch(Ctx* c, int d, int np, int nw, const double* lam, const double* Pc,
+                         long long ldp, const double* cross, long long ldc, double* Abar,
+                         long long lda) {
+  const long long m = d + np + nw;
+  if (m <= 0) return GCG_OK;
+  abar_assemble_kernel<<<(unsigned)((m * m + 255) / 256), 256, 0, c->stream>>>(
+      d, np, nw, lam, Pc, ldp, cross, ldc, Abar, lda);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+__global__ void max_abs_diff_kernel(int m, int n, const double* A, long long lda,
+                                    const double* B, long long ldb, double* out) {
+  double mx = 0.0;
+  for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    const double b = B ? B[(long long)i * ldb + j] : (i == j ? 1.0 : 0.0);
+    mx = fmax(mx, fabs(A[(long long)i * lda + j] - b));
+  }
+  mx = warp_max(mx);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t = fmax(t, red[w]);
+    *out = t;
+  }
+}
+
+int max_abs_diff_launch(Ctx* c, int m, int n, const double* A, long long lda, const double* B,
+                        long long ldb, double* out) {
+  max_abs_diff_kernel<<<1, 1024, 0, c->stream>>>(m, n, A, lda, B, ldb, out);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Ritz residuals (solver.py:129-141); per-CTA partials of
+// s0 = ||AX - lam BX||^2 (or AX - lam X), s1 = X.X, s2 = X.BX, s3 = BX.BX
+__global__ void __launch_bounds__(256) ritz_partials_kernel(long long n, int k,
+                                                            const double* AX, long long ldax,
+                                                            const double* X, long long ldx,
+                                                            const double* BX, long long ldbx,
+                                                            const double* lam, int mode,
+                                                            long long rows_per_cta,
+                                                            double* part) {
+  __shared__ double sm[4][256];
+  const int kc = k;  // <= 256
+  const int lanes = 256 / kc;
+  const int c = threadIdx.x % kc, rl = threadIdx.x / kc;
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  long long r1 = r0 + rows_per_cta;
+  if (r1 > n) r1 = n;
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  if (rl < lanes) {
+    const double l = lam[c];
+    for (long long i = r0 + rl; i < r1; i += lanes) {
+      const double ax = AX[i * ldax + c], x = X[i * ldx + c], bx = BX[i * ldbx + c];
+      const double res = (mode == 0) ? ax - l * x : ax - l * bx;
+      s0 = fma(res, res, s0);
+      s1 = fma(x, x, s1);
+      s2 = fma(x, bx, s2);
+      s3 = fma(bx, bx, s3);
+    }
+  }
+  sm[0][threadIdx.x] = s0;
+  sm[1][threadIdx.x] = s1;
+  sm[2][threadIdx.x] = s2;
+  sm[3][threadIdx.x] = s3;
+  __syncthreads();
+  if (threadIdx.x < kc) {
+    for (int q = 0; q < 4; ++q) {
+      double t = 0.0;
+      for (int l = 0; l < lanes; ++l) t += sm[q][l * kc + threadIdx.x];
+      part[((long long)blockIdx.x * 4 + q) * k + threadIdx.x] = t;
+    }
+  }
+}
+
+__global__ void ritz_finish_kernel(int k, int nparts, const double* part, const double* lam,
+                                   int mode, double* out) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double s[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nparts; ++b)
+      for (int q = 0; q < 4; ++q) s[q] += part[((long long)b * 4 + q) * k + c];
+    const double l = lam[c];
+    double den;
+    if (mode == 2) {
+      den = fabs(l) * sqrt(s[3]);
+    } else if (mode == 1) {
+      den = sqrt(fmax(s[2], 0.0));
+      if (l > 0.0) den *= l;
+    } else {
+      den = sqrt(s[1]);
+    }
+    if (den == 0.0) den = 1.0;
+    out[c] = sqrt(s[0]) / den;
+  }
+}
+
+int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long long ldax,
+                          const double* X, long long ldx, const double* BX, long long ldbx,
+                          const double* lam, int mode, double* out) {
+  if (k <= 0) return GCG_OK;
+  if (k > 256) return GCG_ERR_ARG;
+  int grid = grid_for(n, 1024, 4, c->num_sms);
+  long long rpc = (n + grid - 1) / grid;
+  grid = (int)((n + rpc - 1) / rpc);
+  GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * 4 * k));
+  double* part = (double*)c->partials.ptr;
+  ritz_partials_kernel<<<grid, 256, 0, c->stream>>>(n, k, AX, ldax, X, ldx, BX, ldbx, lam, mode,
+                                                     rpc, part);
+  ritz_finish_kernel<<<1, 256, 0, c->stream>>>(k, grid, part, lam, mode, out);
+  g_launches += 2;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+}  // namespace gcg

@@ -1,0 +1,304 @@
+// MatDotMultiVec on B200: fp64 CSR x row-major multivector (SpMM).
+//
+// Reference: CsrOperator.apply (operators.py:103-111) -> kernels.csr_matvec
+// (_cy.pyx:11-23: column-by-column scalar CSR loop) and ShiftedOperator.apply
+// (operators.py:149-156: A x - theta (B x or x)).
+//
+// B200 design.  X is row-major, so the k values a nonzero (i, j) needs are one
+// contiguous run X[j*ldx : j*ldx+k]: a group of LPR lanes owns one row and
+// reads those runs with 16-byte vector loads (coalesced, L2-resident for the
+// stencil's plane-distance reuse).  The row's (column index, value) stream is
+// loaded once, cooperatively, one nonzero per lane, and broadcast inside the
+// group with shuffles — 12 B/nnz from HBM instead of k separate index loads.
+// The epilogue fuses the shifted-operator term (gamma*Z, Z = X for A - theta*I),
+// an axpby with a second input (beta*Yin, used for r = rhs - op x) and an
+// optional per-column dot product reduced deterministically (p'q and ||r||^2
+// for block CG), so CG never makes a separate pass for them.
+//
+// Roofline: HBM.  Algorithmic bytes per launch = 12*nnz + 4*(n+1) + 16*n*k
+// (+8*n*k per extra epilogue stream); flops = 2*nnz*k.
+
+#include "common.cuh"
+
+namespace gcg {
+
+struct SpmmArgs {
+  long long n;
+  const int* __restrict__ rowptr;
+  const int* __restrict__ colidx;
+  const double* __restrict__ val;
+  int k;
+  const double* __restrict__ X;
+  long long ldx;
+  double alpha, gamma, beta;
+  const double* __restrict__ Z;
+  long long ldz;
+  const double* Yin;
+  long long ldyin;
+  double* Y;
+  long long ldy;
+  int dot_mode;
+  const double* __restrict__ W;
+  long long ldw;
+  double* partials;  // [gridDim.x][k]
+  const int* skip;   // device flag: nonzero -> kernel is a no-op (CG early exit)
+};
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<1> {
+  using T = double;
+  static __device__ __forceinline__ void load(const double* p, double* o) { o[0] = __ldg(p); }
+};
+template <>
+struct VecT<2> {
+  static __device__ __forceinline__ void load(const double* p, double* o) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = v.x;
+    o[1] = v.y;
+  }
+};
+
+constexpr int kSpmmThreads = 256;
+
+template <int LPR, int VEC, int NV>
+__global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(SpmmArgs a) {
+  if (a.skip != nullptr && *a.skip) return;
+  constexpr int G = 32 / LPR;  // row groups per warp
+  constexpr int COLS = LPR * VEC * NV;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int g = lane / LPR;
+  const int sub = lane % LPR;
+  const int nwarps = kSpmmThreads / 32;
+  const long long stride = (long long)gridDim.x * nwarps * G;
+  const int k = a.k;
+
+  __shared__ double sdot[kSpmmThreads / 32][COLS];
+  double dacc[NV][VEC];
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) dacc[q][v] = 0.0;
+
+  // This kernel handles one column pass [c0, c0 + COLS); wider blocks are
+  // split by the launcher into several launches with offset pointers.
+  for (long long rb = ((long long)blockIdx.x * nwarps + warp) * G; rb < a.n; rb += stride) {
+    const long long r = rb + g;
+    const bool valid = r < a.n;
+    int start = 0, len = 0;
+    if (valid) {
+      start = __ldg(a.rowptr + r);
+      len = __ldg(a.rowptr + r + 1) - start;
+    }
+    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+    double acc[NV][VEC];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[q][v] = 0.0;
+
+    for (int off = 0; off < maxlen; off += LPR) {
+      int mycol = 0;
+      double myval = 0.0;
+      if (off + sub < len) {
+        mycol = __ldg(a.colidx + start + off + sub);
+        myval = __ldg(a.val + start + off + sub);
+      }
+      const int tmax = min(LPR, maxlen - off);
+#pragma unroll 4
+      for (int t = 0; t < tmax; ++t) {
+        const int j = __shfl_sync(0xffffffffu, mycol, t, LPR);
+        const double v = __shfl_sync(0xffffffffu, myval, t, LPR);
+        if (off + t < len) {
+          const double* xr = a.X + (long long)j * a.ldx;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            const int c = (q * LPR + sub) * VEC;
+            if (c < k) {
+              double xv[VEC];
+              VecT<VEC>::load(xr + c, xv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v, xv[e], acc[q][e]);
+            }
+          }
+        }
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int c = (q * LPR + sub) * VEC;
+        if (c < k) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            double y = a.alpha * acc[q][e];
+            if (a.gamma != 0.0) y = fma(a.gamma, a.Z[r * a.ldz + c + e], y);
+            if (a.beta != 0.0) y = fma(a.beta, a.Yin[r * a.ldyin + c + e], y);
+            a.Y[r * a.ldy + c + e] = y;
+            if (a.dot_mode == 1) dacc[q][e] = fma(y, a.W[r * a.ldw + c + e], dacc[q][e]);
+            else if (a.dot_mode == 2) dacc[q][e] = fma(y, y, dacc[q][e]);
+          }
+        }
+      }
+    }
+  }
+
+  if (a.dot_mode == 0) return;
+  // reduce over the row groups of the warp (lanes with equal `sub`)
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      double v = dacc[q][e];
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      dacc[q][e] = v;
+    }
+  if (g == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) sdot[warp][(q * LPR + sub) * VEC + e] = dacc[q][e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k && c < COLS; c += kSpmmThreads) {
+    double s = 0.0;
+    for (int w = 0; w < nwarps; ++w) s += sdot[w][c];
+    a.partials[(long long)blockIdx.x * k + c] = s;
+  }
+}
+
+// out[c*out_stride] = sum_b partials[b*k + c] in fixed b order (deterministic).
+__global__ void reduce_partials_kernel(const double* __restrict__ partials, int nparts, int k,
+                                       double* out, int out_stride, int mode) {
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) s += partials[(long long)b * k + c];
+  // fixed-shape tree over the 128 threads
+  __shared__ double sm[128];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 64; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double v = sm[0];
+    if (mode == 1) v += out[(long long)c * out_stride];
+    out[(long long)c * out_stride] = v;
+  }
+}
+
+int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* out,
+                    int out_stride, int mode) {
+  if (k <= 0) return GCG_OK;
+  reduce_partials_kernel<<<k, 128, 0, c->stream>>>(partials, nparts, k, out, out_stride, mode);
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+extern int64_t g_launches;
+
+template <int LPR, int VEC>
+static int launch_nv(Ctx* c, SpmmArgs a, int nv, int grid) {
+  switch (nv) {
+    case 1: spmm_csr_kernel<LPR, VEC, 1><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
+    case 2: spmm_csr_kernel<LPR, VEC, 2><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
+    case 3: spmm_csr_kernel<LPR, VEC, 3><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
+    default: spmm_csr_kernel<LPR, VEC, 4><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
+  }
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+template <int VEC>
+static int launch_lpr(Ctx* c, SpmmArgs a, int lpr, int nv, int grid) {
+  switch (lpr) {
+    case 4: return launch_nv<4, VEC>(c, a, nv, grid);
+    case 8: return launch_nv<8, VEC>(c, a, nv, grid);
+    case 16: return launch_nv<16, VEC>(c, a, nv, grid);
+    default: return launch_nv<32, VEC>(c, a, nv, grid);
+  }
+}
+
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int spmm_grid(Ctx* c, long long n) { return grid_for(n, 64, 8, c->num_sms); }
+
+// One SpMM over all k columns, split into passes of at most 256 columns.  With
+// dot_mode != 0 and `partials` given, per-CTA partials ([grid][k], k <= 256)
+// are left for the caller to reduce; otherwise they are reduced into `dots`.
+int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
+                     const double* val, int k, const double* X, long long ldx, double alpha,
+                     double gamma, const double* Z, long long ldz, double beta, const double* Yin,
+                     long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
+                     long long ldw, double* dots, double* partials_ext, int* grid_out,
+                     const int* skip) {
+  if (n <= 0 || k <= 0) return GCG_OK;
+  constexpr int kMaxPass = 256;
+  const int grid = spmm_grid(c, n);
+  if (grid_out) *grid_out = grid;
+  if (partials_ext && k > kMaxPass) return GCG_ERR_ARG;
+  double* partials = partials_ext;
+  if (dot_mode && !partials) {
+    GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * (size_t)kMaxPass));
+    partials = (double*)c->partials.ptr;
+  }
+  for (int c0 = 0; c0 < k; c0 += kMaxPass) {
+    const int kc = (k - c0) < kMaxPass ? (k - c0) : kMaxPass;
+    bool vec2 = (kc % 2 == 0) && (ldx % 2 == 0) && aligned16(X + c0);
+    const int vec = vec2 ? 2 : 1;
+    const int lanes_needed = (kc + vec - 1) / vec;
+    int lpr = 4;
+    while (lpr < 32 && lpr * 2 < lanes_needed) lpr <<= 1;
+    int nv = (lanes_needed + lpr - 1) / lpr;
+    while (nv > 4 && lpr < 32) {
+      lpr <<= 1;
+      nv = (lanes_needed + lpr - 1) / lpr;
+    }
+    SpmmArgs a;
+    a.n = n;
+    a.rowptr = rowptr;
+    a.colidx = colidx;
+    a.val = val;
+    a.k = kc;
+    a.X = X + c0;
+    a.ldx = ldx;
+    a.alpha = alpha;
+    a.gamma = gamma;
+    a.Z = Z ? Z + c0 : nullptr;
+    a.ldz = ldz;
+    a.beta = beta;
+    a.Yin = Yin ? Yin + c0 : nullptr;
+    a.ldyin = ldyin;
+    a.Y = Y + c0;
+    a.ldy = ldy;
+    a.dot_mode = dot_mode;
+    a.W = W ? W + c0 : nullptr;
+    a.ldw = ldw;
+    a.partials = partials;
+    a.skip = skip;
+    int s = vec2 ? launch_lpr<2>(c, a, lpr, nv, grid) : launch_lpr<1>(c, a, lpr, nv, grid);
+    if (s != GCG_OK) return s;
+    if (dot_mode && !partials_ext) {
+      GCG_TRY(reduce_partials(c, partials, grid, kc, dots + c0, 1, 0));
+      ++g_launches;
+    }
+  }
+  return GCG_OK;
+}
+
+int spmm_launch_parts(Ctx* c, long long n, const int* rowptr, const int* colidx,
+                      const double* val, int k, const double* X, long long ldx, double alpha,
+                      double gamma, const double* Z, long long ldz, double beta,
+                      const double* Yin, long long ldyin, double* Y, long long ldy, int dot_mode,
+                      const double* W, long long ldw, double* partials, int* grid_out,
+                      const int* skip) {
+  return spmm_launch_impl(c, n, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta, Yin,
+                          ldyin, Y, ldy, dot_mode, W, ldw, nullptr, partials, grid_out, skip);
+}
+
+}  // namespace gcg

@@ -1,0 +1,533 @@
+"""GCG eigensolver driver with every long-vector operation on the B200.
+
+Drop-in for the reference entry point ``gcg_solve(a, b=None, config=None) ->
+SolverReport`` (solver.py:226-486): same SolverConfig fields and defaults,
+same control flow (Alg. 1 STEPs 2-6, locking, dynamic shift, moving window),
+same report.  The multivector arena V = [X | P | W] (n x (sx + 2 bs)) lives in
+HBM, row-major; the host only ever sees m x m-sized decisions (eigenvalues,
+residual norms, dependence counts) read back as a handful of doubles.
+
+Two parity switches that the reference does not have:
+``init`` ("uniform" = reference mv_set_random, "normal" = BASELINE N(0,1)) and
+``residual`` ("reference" = solver._rel_residual, "relative" = north-star
+||Ax - lam Bx|| / (|lam| ||Bx||)).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .cg import block_cg
+from .dense import sym_eig_full
+from .errors import AllDependent, InvalidShape
+from .operators import DeviceProblem, as_device_problem
+from .orth import OrthConfig, orth_against, recursive_orth_svd
+
+__all__ = [
+    "SolverConfig",
+    "IterationRecord",
+    "SolverReport",
+    "gcg_solve",
+    "select_shift",
+    "moving_memory_budget",
+]
+
+BACKEND_NAME = "sm100"
+_TIMING_KEYS = ("t_step2", "t_step3", "t_step4", "t_step5", "t_step6")
+_RESIDUAL_MODES = {"reference": None, "relative": 2}
+
+
+@dataclass
+class SolverConfig:
+    """solver.SolverConfig (solver.py:56-74) + the two parity switches."""
+
+    num_eigen: int = 1
+    tol: float = 1e-8
+    block_size: int | None = None
+    size_x: int | None = None
+    max_gcg_iters: int = 1000
+    cg_max_iters: int = 30
+    cg_rel_tol: float = 0.01
+    shift_mode: str = "dynamic"
+    moving: bool = False
+    seed: int = 0
+    deterministic: bool = False
+    orth: OrthConfig = field(default_factory=OrthConfig)
+    collect_history: bool = True
+    stall_window: int = 50
+    instrument_orth: bool = False
+    cross_check_abar: bool = False
+    # B200 drop-in extensions
+    init: str = "uniform"          # "uniform" (reference) | "normal" (BASELINE)
+    residual: str = "reference"    # "reference" | "relative" (north-star)
+    validate: bool = True          # host symmetry/finiteness check of the input matrices
+    return_device: bool = False    # keep eigenvectors as a device tensor (row-major n x nev)
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    num_converged: int
+    first_unconverged_residual: float
+    theta: float
+    cg_iterations: int
+    basis_size: int
+    orth_reductions: int
+    timings: dict = field(default_factory=dict)
+    basis_defect: float | None = None
+    abar_defect: float | None = None
+
+
+@dataclass
+class SolverReport:
+    status: str
+    eigenvalues: np.ndarray
+    eigenvectors: object
+    num_converged: int
+    iterations: int
+    residuals: np.ndarray
+    history: list
+    stagnated: bool
+    max_projection_dim: int
+    total_reductions: int
+    backend: str
+
+
+def moving_memory_budget(size_x, block_size):
+    """solver.moving_memory_budget (solver.py:106-110)."""
+    mpd = size_x + 2 * block_size
+    return (size_x + 2 * block_size) + 2 * mpd * mpd + 10 * mpd + size_x * block_size
+
+
+def select_shift(mode, lam, num_locked, store_vals=()):
+    """solver.select_shift (solver.py:113-126): largest locked eigenvalue, else 0."""
+    if mode not in ("dynamic", "none"):
+        raise InvalidShape(f"unknown shift mode {mode!r}")
+    if mode == "none":
+        return 0.0
+    best = None
+    if num_locked > 0:
+        best = float(lam[num_locked - 1])
+    for vals in store_vals:
+        if len(vals):
+            top = float(vals[-1])
+            best = top if best is None or top > best else best
+    return 0.0 if best is None else best
+
+
+def _stagnation_flag(history, window):
+    """solver._stagnation_flag (solver.py:202-210)."""
+    if window <= 0 or len(history) < window:
+        return False
+    tail = history[-window:]
+    if tail[-1].num_converged != tail[0].num_converged:
+        return False
+    return not (tail[-1].first_unconverged_residual < 0.9 * tail[0].first_unconverged_residual)
+
+
+class _Timer:
+    def __init__(self, enabled):
+        self.enabled = enabled
+        self.marks = {k: 0.0 for k in _TIMING_KEYS}
+        self._last = time.perf_counter()
+
+    def lap(self, key):
+        now = time.perf_counter()
+        if self.enabled:
+            self.marks[key] += now - self._last
+        self._last = now
+
+
+class _Solve:
+    """State of one device solve (the body of solver.py:226-486)."""
+
+    def __init__(self, dev, prob, cfg):
+        self.dev = dev
+        self.prob = prob
+        self.cfg = cfg
+        self.n = prob.n
+        self.generalized = prob.B is not None
+        mode = _RESIDUAL_MODES.get(cfg.residual, "bad")
+        if mode == "bad":
+            raise InvalidShape(f"unknown residual kind {cfg.residual!r}")
+        self.res_mode = mode if mode is not None else (1 if self.generalized else 0)
+        self.scalar = dev.empty(8)
+
+    # -- small helpers -------------------------------------------------------
+    def set_random(self, block, seed):
+        """multivec.mv_set_random (multivec.py:46-50) drawn on host, uploaded (parity)."""
+        rng = np.random.Generator(np.random.PCG64(seed))
+        shape = tuple(block.shape)
+        if self.cfg.init == "normal":
+            host = rng.standard_normal(shape)
+        else:
+            host = rng.uniform(-1.0, 1.0, size=shape)
+        src = torch.from_numpy(host).to(self.dev.device)
+        D.copy(self.dev, src, block)
+
+    def apply_a(self, x):
+        out = self.dev.empty(x.shape[0], x.shape[1])
+        return D.spmm(self.dev, self.prob.A, x, out)
+
+    def apply_b(self, x):
+        if self.prob.B is None:
+            return x
+        out = self.dev.empty(x.shape[0], x.shape[1])
+        return D.spmm(self.dev, self.prob.B, x, out)
+
+    def residuals(self, x, lam_dev):
+        """Per-column relative residuals of Ritz pairs (solver.py:129-141), device -> host."""
+        k = x.shape[1]
+        out = np.empty(k)
+        for s in range(0, k, 256):
+            e = min(s + 256, k)
+            xc = x[:, s:e]
+            ax = self.apply_a(xc)
+            bx = self.apply_b(xc)
+            r = self.dev.empty(e - s)
+            D.ritz_residuals(self.dev, ax, xc, bx, lam_dev[s:e], self.res_mode, r)
+            out[s:e] = r.cpu().numpy()
+        return out
+
+    def count_converged(self, x_new, lam_new_dev, lam_new, limit, chunk, tol):
+        """solver._count_converged (solver.py:144-164): prefix of Ritz pairs below tol."""
+        count = 0
+        for start in range(0, limit, chunk):
+            stop = min(start + chunk, limit)
+            rel = self.residuals(x_new[:, start:stop], lam_new_dev[start:stop])
+            for j in range(stop - start):
+                if rel[j] < tol:
+                    count += 1
+                else:
+                    return count, float(rel[j])
+        return count, 0.0
+
+    def build_p(self, coeffs, num_x_rows, group_start, group_width, dep_tol):
+        """solver._build_p (solver.py:167-199) on device; returns phat (m x np) or None."""
+        dev = self.dev
+        m = coeffs.shape[0]
+        if group_width <= 0 or m <= num_x_rows:
+            return None
+        d = coeffs.shape[1]
+        pt = dev.empty(m, group_width)
+        D.copy(dev, coeffs[:, group_start:group_start + group_width], pt)
+        D.fill(dev, pt[:num_x_rows], 0.0)
+        tmp = dev.empty(d, group_width)
+        for _ in range(2):
+            D.dgemm(dev, coeffs, pt, tmp, ta=True)
+            D.dgemm(dev, coeffs, tmp, pt, alpha=-1.0, beta=1.0)
+        q, kept = self._orthonormalize_small(pt, dep_tol)
+        if q is None:
+            return None
+        tmp = dev.empty(d, kept)
+        D.dgemm(dev, coeffs, q, tmp, ta=True)
+        D.dgemm(dev, coeffs, tmp, q, alpha=-1.0, beta=1.0)
+        q2, _ = self._orthonormalize_small(q, 1e-4)
+        return q2
+
+    def _orthonormalize_small(self, pt, rel):
+        """g = pt'pt; symmetric eig; drop eigenvalues <= rel*max; pt V/sqrt(w)."""
+        dev = self.dev
+        gw = pt.shape[1]
+        g = dev.empty(gw, gw)
+        D.dgemm(dev, pt, pt, g, ta=True)
+        D.symmetrize(dev, g)
+        dec = sym_eig_full(dev, g)
+        D.count_le(dev, dec.values, rel, self.scalar)
+        bad = int(self.scalar[0].item())
+        if bad >= gw:
+            return None, 0
+        kept = gw - bad
+        scaled = dev.empty(gw, kept)
+        D.scale_rsqrt(dev, dec.vectors, dec.values, bad, scaled)
+        q = dev.empty(pt.shape[0], kept)
+        D.dgemm(dev, pt, scaled, q)
+        return q, kept
+
+
+def gcg_solve(a, b=None, config=None):
+    """Run the block eigensolver on the B200; returns a :class:`SolverReport`."""
+    cfg = config if config is not None else SolverConfig()
+    dev = D.default_context()
+    if isinstance(a, DeviceProblem):
+        prob = a
+    else:
+        prob = as_device_problem(dev, a, b, validate=cfg.validate)
+    S = _Solve(dev, prob, cfg)
+    n = prob.n
+    ne = int(cfg.num_eigen)
+    if not (1 <= ne <= n):
+        raise InvalidShape(f"num_eigen must be in 1..{n}, got {ne}")
+    if cfg.shift_mode not in ("dynamic", "none"):
+        raise InvalidShape(f"unknown shift mode {cfg.shift_mode!r}")
+    bs = cfg.block_size if cfg.block_size is not None else max(1, math.ceil(ne / 5))
+    bs = min(bs, n)
+    if cfg.moving:
+        sx = min(3 * bs, n)
+    else:
+        sx = cfg.size_x if cfg.size_x is not None else min(ne + 3 * bs, n)
+        sx = min(max(sx, ne), n)
+    ocfg = cfg.orth
+    det = cfg.deterministic
+    Bop = prob.B
+
+    v = dev.zeros(n, sx + 2 * bs)
+    lam = np.zeros(sx + 2 * bs)
+    S.set_random(v[:, :sx], cfg.seed)
+    out = recursive_orth_svd(dev, v, 1, sx, b=Bop, cfg=ocfg)
+    total_red = out.reduction_count
+    if out.num_kept < sx:
+        S.set_random(v[:, out.num_kept:sx], cfg.seed + 9973)
+        out = recursive_orth_svd(dev, v, 1, sx, b=Bop, cfg=ocfg)
+        total_red += out.reduction_count
+        if out.num_kept < sx:
+            raise AllDependent("could not build a full-rank starting block")
+
+    locked = 0
+    np_, nw = 0, 0
+    abar_prev = None
+    p_coupling = None
+    store_x, store_vals = [], []
+    history = []
+    pending_cg = []
+    max_m = 0
+    status = "max_iterations"
+    iters_run = 0
+
+    for it in range(1, cfg.max_gcg_iters + 1):
+        iters_run = it
+        timer = _Timer(not det)
+        d = sx - locked
+        m = d + np_ + nw
+        max_m = max(max_m, m)
+        basis = v[:, locked:sx + np_ + nw]
+
+        # STEP 3: projected matrix (solver.py:277-294)
+        abar = dev.empty(m, m)
+        if abar_prev is None:
+            ab = S.apply_a(basis)
+            D.gram(dev, basis, ab, abar)
+            D.symmetrize(dev, abar)
+        else:
+            cross = None
+            if nw:
+                aw = S.apply_a(v[:, sx + np_:sx + np_ + nw])
+                cross = dev.empty(m, nw)
+                D.gram(dev, basis, aw, cross)
+            lam_x = torch.from_numpy(lam[locked:sx].copy()).to(dev.device)
+            D.abar_assemble(dev, d, lam_x, p_coupling if np_ else None, cross, abar)
+        abar_defect = None
+        if cfg.cross_check_abar and abar_prev is not None:
+            naive = dev.empty(m, m)
+            D.gram(dev, basis, S.apply_a(basis), naive)
+            D.symmetrize(dev, naive)
+            D.max_abs_diff(dev, abar, naive, S.scalar)
+            abar_defect = float(S.scalar[0].item())
+        timer.lap("t_step3")
+
+        full = sym_eig_full(dev, abar)
+        lam_new_dev = full.values[:d]
+        coeffs = full.vectors[:, :d]
+        x_new = dev.empty(n, d)
+        D.lincomb(dev, basis, coeffs, x_new)
+        lam_new = lam_new_dev.cpu().numpy()
+        timer.lap("t_step3")
+
+        stored = sum(len(vv) for vv in store_vals)
+        limit = max(0, min(sx - locked, ne - stored - locked))
+        newly, first_res = S.count_converged(x_new, lam_new_dev, lam_new, limit, bs, cfg.tol)
+        c = locked + newly
+        total_locked = stored + c
+        timer.lap("t_step4")
+
+        if total_locked >= ne:
+            D.copy(dev, x_new, v[:, locked:sx])
+            lam[locked:sx] = lam_new
+            locked = c
+            status = "converged"
+            if cfg.collect_history:
+                theta = select_shift(cfg.shift_mode, lam, locked, store_vals)
+                history.append(IterationRecord(it, total_locked, first_res, theta, 0, m, 0,
+                                               timer.marks, None, abar_defect))
+            break
+
+        compacted = refilled = False
+        iter_red = 0
+        if cfg.moving and c > 0 and (c >= 2 * bs or c >= sx):
+            # window slide (solver.py:325-363)
+            lam_all = full.values.cpu().numpy()
+            x_all = dev.empty(n, m)
+            D.lincomb(dev, basis, full.vectors, x_all)
+            blk = dev.empty(n, locked + newly)
+            if locked:
+                D.copy(dev, v[:, :locked], blk[:, :locked])
+            if newly:
+                D.copy(dev, x_all[:, :newly], blk[:, locked:])
+            store_x.append(blk)
+            store_vals.append(np.concatenate([lam[:locked], lam_all[:newly]]))
+            stored += c
+            sx = m - newly
+            if sx:
+                D.copy(dev, x_all[:, newly:], v[:, :sx])
+                lam[:sx] = lam_all[newly:]
+            locked = 0
+            np_, nw = 0, 0
+            p_coupling = None
+            compacted = True
+            c = 0
+            if sx < bs:
+                add = min(3 * bs, n - stored) - sx
+                if add > 0:
+                    S.set_random(v[:, sx:sx + add], cfg.seed + 104729 * it)
+                    defl = _hstack(dev, store_x + [v[:, :sx]])
+                    ro = orth_against(dev, v[:, sx:sx + add], defl, b=Bop, cfg=ocfg)
+                    iter_red += ro.reduction_count
+                    sx += ro.num_kept
+                refilled = True
+                if sx <= 0:
+                    raise AllDependent("moving window could not be refilled")
+        timer.lap("t_step4")
+
+        theta = select_shift(cfg.shift_mode, lam, locked, store_vals)
+        cg_rep = None
+        if not refilled:
+            if compacted:
+                bs_eff = max(1, min(bs, ne - stored, sx))
+            else:
+                bs_eff = max(1, min(bs, ne - stored - c, sx - c))
+                phat = S.build_p(coeffs, d, c - locked, bs_eff, ocfg.dependence_tol)
+                p_new = None
+                if phat is None:
+                    p_coupling = None
+                else:
+                    p_new = dev.empty(n, phat.shape[1])
+                    D.lincomb(dev, basis, phat, p_new)
+                    ap = dev.empty(m, phat.shape[1])
+                    D.dgemm(dev, abar, phat, ap)
+                    p_coupling = dev.empty(phat.shape[1], phat.shape[1])
+                    D.dgemm(dev, phat, ap, p_coupling, ta=True)
+                D.copy(dev, x_new, v[:, locked:sx])
+                lam[locked:sx] = lam_new
+                locked = c
+                np_ = 0 if p_new is None else p_new.shape[1]
+                if np_:
+                    D.copy(dev, p_new, v[:, sx:sx + np_])
+            timer.lap("t_step5")
+
+            # STEP 6: damped inverse power via block CG (solver.py:386-396)
+            x_act = v[:, locked:locked + bs_eff]
+            w_region = v[:, sx + np_:sx + np_ + bs_eff]
+            scale = torch.from_numpy(lam[locked:locked + bs_eff] - theta).to(dev.device)
+            rhs = dev.empty(n, bs_eff)
+            if Bop is not None:
+                D.spmm(dev, Bop, x_act, rhs)
+            else:
+                D.copy(dev, x_act, rhs)
+            D.col_scale(dev, scale, rhs)
+            D.copy(dev, x_act, w_region)
+            _, cg_rep = block_cg(dev, prob, theta, rhs, w_region,
+                                 max_iters=cfg.cg_max_iters, rel_tol=cfg.cg_rel_tol)
+            timer.lap("t_step6")
+
+            # STEP 2: W against [store, X, P] (solver.py:398-420)
+            if store_x:
+                defl = _hstack(dev, store_x + [v[:, :sx + np_]])
+            else:
+                defl = v[:, :sx + np_]
+            try:
+                w_out = orth_against(dev, w_region, defl, b=Bop, cfg=ocfg)
+                nw = w_out.num_kept
+                iter_red += w_out.reduction_count
+            except AllDependent:
+                nw = 0
+            if nw == 0:
+                S.set_random(w_region, cfg.seed + 7919 * it)
+                try:
+                    w_out = orth_against(dev, w_region, defl, b=Bop, cfg=ocfg)
+                    nw = w_out.num_kept
+                    iter_red += w_out.reduction_count
+                except AllDependent:
+                    nw = 0
+            timer.lap("t_step2")
+
+        total_red += iter_red
+
+        basis_defect = None
+        if cfg.instrument_orth:
+            fb = v[:, :sx + np_ + nw]
+            g = dev.empty(fb.shape[1], fb.shape[1])
+            D.gram(dev, fb, S.apply_b(fb), g)
+            D.max_abs_diff(dev, g, None, S.scalar)
+            basis_defect = float(S.scalar[0].item())
+
+        abar_prev = None if refilled else abar
+        if cfg.collect_history:
+            rec = IterationRecord(it, total_locked, first_res, theta, 0, m, iter_red,
+                                  timer.marks, basis_defect, abar_defect)
+            history.append(rec)
+            if cg_rep is not None:
+                pending_cg.append((rec, cg_rep))
+
+    for rec, rep in pending_cg:  # resolve CG sweep counts (one D2H each, after the loop)
+        rec.cg_iterations = rep.iterations
+
+    # result assembly (solver.py:447-472)
+    if store_x:
+        parts = store_x + [v[:, :locked]]
+        all_vals = np.concatenate(store_vals + [lam[:locked]])
+        n_conv = all_vals.shape[0]
+        if n_conv < ne:
+            extra = min(ne - n_conv, sx - locked)
+            parts.append(v[:, locked:locked + extra])
+            all_vals = np.concatenate([all_vals, lam[locked:locked + extra]])
+        take = min(ne, all_vals.shape[0])
+        values = all_vals[:take].copy()
+        vectors = _hstack(dev, parts)[:, :take]
+    else:
+        n_conv = locked
+        values = lam[:ne].copy()
+        vectors = v[:, :ne]
+
+    residuals = np.empty(values.shape[0])
+    if values.shape[0]:
+        vd = torch.from_numpy(values).to(dev.device)
+        residuals = S.residuals(vectors, vd)
+
+    if cfg.return_device:
+        evecs = vectors
+    else:
+        # one on-device layout transpose, then a single D2H of an F-order block
+        evecs = vectors.t().contiguous().cpu().numpy().T
+
+    return SolverReport(
+        status=status,
+        eigenvalues=values,
+        eigenvectors=evecs,
+        num_converged=min(n_conv, ne),
+        iterations=iters_run,
+        residuals=residuals,
+        history=history,
+        stagnated=_stagnation_flag(history, cfg.stall_window),
+        max_projection_dim=max_m,
+        total_reductions=total_red,
+        backend=BACKEND_NAME,
+    )
+
+
+def _hstack(dev, parts):
+    """Contiguous copy of column blocks (the reference's np.hstack, solver.py:337,356,401,450)."""
+    parts = [p for p in parts if p.shape[1] > 0]
+    n = parts[0].shape[0] if parts else 0
+    width = sum(p.shape[1] for p in parts)
+    out = dev.empty(n, width)
+    c = 0
+    for p in parts:
+        D.copy(dev, p, out[:, c:c + p.shape[1]])
+        c += p.shape[1]
+    return out

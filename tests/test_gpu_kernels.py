@@ -1,0 +1,271 @@
+"""Kernel parity on the B200: every device op against the CPU oracle / numpy.
+
+Tolerances follow north_star ("SpMM/Gram kernels to 1e-12 relative against the
+reference ops") measured normwise and the reference's own
+kernel tests (test_kernels.py:43-102).
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse
+import torch
+
+from oracle import gcg_oracle as O
+from paper_2111_06552_b200 import _lib
+from paper_2111_06552_b200 import device as D
+from paper_2111_06552_b200 import problems as P
+from paper_2111_06552_b200 import refbackend
+from paper_2111_06552_b200.operators import DeviceCsr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return D.default_context()
+
+
+def rm(dev, a):
+    """host array -> row-major device tensor"""
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev.device)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rel_err(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+def random_sym_csr(n, density, seed):
+    m = scipy.sparse.random(n, n, density=density, random_state=np.random.RandomState(seed))
+    m = (m + m.T).tocsr()
+    m.sum_duplicates()
+    return m
+
+
+SPMM_CASES = [
+    ("lap3d16", lambda: P.laplacian_3d(16)),
+    ("27pt10", lambda: P.stencil27(10)),
+    ("fem5", lambda: P.fem_p1_cube(5)[1]),
+    ("rand300", lambda: random_sym_csr(300, 0.05, 1)),
+]
+
+
+@pytest.mark.parametrize("name,mk", SPMM_CASES)
+@pytest.mark.parametrize("k", [1, 3, 7, 20, 40, 100, 200, 300])
+def test_spmm_vs_oracle(dev, name, mk, k):
+    a = mk()
+    A = DeviceCsr.from_scipy(dev, a)
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((a.shape[0], k))
+    want = O.csr_matvec(a.indptr, a.indices, a.data, np.asfortranarray(x))
+    y = dev.empty(a.shape[0], k)
+    D.spmm(dev, A, rm(dev, x), y)
+    assert rel_err(host(y), want) <= 1e-13
+
+
+def test_spmm_strided_views_and_epilogue(dev):
+    a = P.laplacian_3d(12)
+    n = a.shape[0]
+    A = DeviceCsr.from_scipy(dev, a)
+    rng = np.random.default_rng(3)
+    arena = rng.standard_normal((n, 57))
+    xa = rm(dev, arena)
+    x = xa[:, 5:26]          # odd offset, odd width: scalar path
+    z = xa[:, 30:51]
+    yin = rng.standard_normal((n, 21))
+    out = dev.zeros(n, 40)[:, 3:24]
+    dots = dev.empty(21)
+    D.spmm(dev, A, x, out, alpha=-1.5, gamma=0.25, Z=z, beta=2.0, Yin=rm(dev, yin), dot_mode=1,
+           W=z, dots=dots)
+    xs, zs = arena[:, 5:26], arena[:, 30:51]
+    want = -1.5 * (a @ xs) + 0.25 * zs + 2.0 * yin
+    assert rel_err(host(out), want) <= 1e-13
+    assert rel_err(host(dots), (want * zs).sum(0)) <= 1e-12
+    dots2 = dev.empty(21)
+    D.spmm(dev, A, x, out, dot_mode=2, dots=dots2)
+    w2 = a @ xs
+    assert rel_err(host(dots2), (w2 * w2).sum(0)) <= 1e-12
+
+
+@pytest.mark.parametrize("n,k1,k2", [(1, 1, 1), (23, 4, 3), (5000, 6, 4), (262144, 200, 20),
+                                      (100003, 80, 80), (4097, 17, 33), (70000, 120, 7)])
+def test_gram_vs_numpy(dev, n, k1, k2):
+    rng = np.random.default_rng(n + k1)
+    x = rng.standard_normal((n, k1))
+    y = rng.standard_normal((n, k2))
+    g = dev.empty(k1, k2)
+    D.gram(dev, rm(dev, x), rm(dev, y), g)
+    want = x.T @ y
+    scale = np.sqrt((x * x).sum(0)).max() * np.sqrt((y * y).sum(0)).max()
+    assert np.abs(host(g) - want).max() / scale <= 1e-13
+    g2 = dev.empty(k1, k2)
+    D.gram(dev, rm(dev, x), rm(dev, y), g2)
+    assert torch.equal(g, g2)  # deterministic: bit-stable run to run (test_kernels.py:74-85)
+
+
+def test_gram_strided_out_and_accumulate(dev):
+    rng = np.random.default_rng(9)
+    x, y = rng.standard_normal((300, 3)), rng.standard_normal((300, 2))
+    parent = dev.zeros(6, 5) + 7.5
+    view = parent[1:4, 1:3]
+    D.gram(dev, rm(dev, x), rm(dev, y), view)
+    p = host(parent)
+    assert np.abs(p[1:4, 1:3] - x.T @ y).max() < 1e-12
+    mask = np.ones_like(p, dtype=bool)
+    mask[1:4, 1:3] = False
+    assert np.all(p[mask] == 7.5)
+    gt = dev.zeros(2, 3)
+    D.gram(dev, rm(dev, x), rm(dev, y), gt, transpose_out=True)
+    assert np.abs(host(gt) - (x.T @ y).T).max() < 1e-12
+
+
+@pytest.mark.parametrize("n,m,d", [(1000, 16, 16), (262144, 200, 160), (5000, 7, 3),
+                                    (77777, 64, 100), (3000, 300, 20)])
+def test_lincomb_vs_numpy(dev, n, m, d):
+    rng = np.random.default_rng(m * d)
+    x = rng.standard_normal((n, m))
+    c = rng.standard_normal((m, d))
+    y0 = rng.standard_normal((n, d))
+    y = rm(dev, y0)
+    D.lincomb(dev, rm(dev, x), rm(dev, c), y, alpha=-0.5, beta=1.25)
+    want = -0.5 * (x @ c) + 1.25 * y0
+    assert rel_err(host(y), want) <= 1e-13
+
+
+def test_axpby_copy_scale_dots(dev):
+    rng = np.random.default_rng(5)
+    x, y = rng.standard_normal((999, 7)), rng.standard_normal((999, 7))
+    for al, bt in [(0.0, 0.0), (1.0, 0.0), (0.0, 1.0), (2.5, 1.0), (2.5, -0.5)]:
+        yt = rm(dev, y)
+        D.axpby(dev, al, rm(dev, x), bt, yt)
+        assert np.abs(host(yt) - (al * x + bt * y)).max() <= 1e-14
+    nan = dev.empty(999, 7).fill_(float("nan"))
+    D.axpby(dev, 3.0, rm(dev, x), 0.0, nan)  # beta == 0 never reads y
+    assert np.array_equal(host(nan), 3.0 * x)
+    s = rng.standard_normal(7)
+    xt = rm(dev, x)
+    D.col_scale(dev, rm(dev, s), xt)
+    assert np.abs(host(xt) - x * s).max() <= 1e-15
+    out = dev.empty(7)
+    D.col_dots(dev, rm(dev, x), rm(dev, y), out)
+    assert rel_err(host(out), (x * y).sum(0)) <= 1e-12
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 16, 33, 64, 65, 120, 200])
+def test_syev_vs_lapack(dev, m):
+    rng = np.random.default_rng(m)
+    a = rng.standard_normal((m, m))
+    a = (a + a.T) / 2
+    w = dev.empty(m)
+    v = dev.empty(m, m)
+    D.syev(dev, rm(dev, a), w, v)
+    ww, vv = O.eig_full(a)
+    assert np.abs(host(w) - ww).max() <= 1e-12 * max(1.0, np.abs(ww).max())
+    V = host(v)
+    assert np.abs(a @ V - V * host(w)).max() <= 1e-12 * max(1.0, np.abs(ww).max())
+    assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12
+    # sign rule of dense.py:63-71 (non-degenerate random spectrum => columns match LAPACK's)
+    assert np.abs(V - vv).max() <= 1e-9
+
+
+def test_syev_golden_m8(dev, golden):
+    w = dev.empty(8)
+    v = dev.empty(8, 8)
+    D.syev(dev, rm(dev, golden["m8"]), w, v)
+    assert np.abs(host(w) - golden["m8_values"]).max() < 1e-13
+    assert np.abs(host(v) - golden["m8_vectors"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("w,rank", [(6, 6), (16, 16), (16, 11), (40, 40), (100, 100), (90, 60)])
+def test_svqb_prepare(dev, w, rank):
+    rng = np.random.default_rng(w + rank)
+    blk = rng.standard_normal((500, rank)) @ rng.standard_normal((rank, w))
+    g = blk.T @ blk
+    q = dev.empty(w, w)
+    st = dev.empty(4)
+    D.svqb_prepare(dev, rm(dev, g), 1e-10, q, st)
+    defect, nbad, wmax = host(st)[:3]
+    ww, vv = O.gram_eig((g + g.T) / 2)
+    floor = 1e-10 * max(ww.max(), 0.0)
+    assert int(nbad) == int(np.searchsorted(ww, floor, side="right")) == w - rank
+    assert abs(defect - np.abs(g - np.eye(w)).max()) <= 1e-12 * np.abs(g).max()
+    kept = w - int(nbad)
+    Q = host(q)[:, :kept]
+    nb = blk @ Q
+    assert np.abs(nb.T @ nb - np.eye(kept)).max() <= 1e-8
+
+
+def test_block_cg_vs_oracle(dev, golden):
+    a = P.stencil_csr((60,), [(0,), (-1,), (1,)], [2.0, -1.0, -1.0])
+    from paper_2111_06552_b200.cg import block_cg
+    from paper_2111_06552_b200.operators import DeviceProblem
+
+    prob = DeviceProblem(dev, a)
+    x = rm(dev, golden["cg_x0"])
+    _, rep = block_cg(dev, prob, 0.05, rm(dev, golden["cg_rhs"]), x, 30, 0.01)
+    assert rep.iterations == int(golden["cg_meta"][0])
+    assert rep.converged.sum() == int(golden["cg_meta"][1])
+    assert rel_err(host(x), golden["cg_w"]) <= 1e-10
+    assert np.abs(rep.relative_residuals - golden["cg_relres"]).max() <= 1e-10
+
+
+def test_block_cg_semantics(dev):
+    """test_cg.py cases: zero-rhs column, indefinite freeze, iteration cap."""
+    from paper_2111_06552_b200.cg import block_cg
+    from paper_2111_06552_b200.operators import DeviceProblem
+
+    prob = DeviceProblem(dev, scipy.sparse.diags([1.0, -1.0]).tocsr())
+    rhs = np.zeros((2, 2))
+    rhs[0, 0] = rhs[1, 1] = 1.0
+    x = dev.zeros(2, 2)
+    _, rep = block_cg(dev, prob, 0.0, rm(dev, rhs), x, 10, 1e-12)
+    assert rep.converged[0] and rep.frozen[1] and not rep.converged[1]
+    assert np.isfinite(host(x)).all()
+    prob = DeviceProblem(dev, scipy.sparse.diags([1.0, 2.0, 3.0]).tocsr())
+    rhs = np.zeros((3, 2))
+    rhs[:, 1] = [1.0, 0.0, 0.0]
+    x = dev.zeros(3, 2)
+    _, rep = block_cg(dev, prob, 0.0, rm(dev, rhs), x, 10, 1e-12)
+    assert rep.converged.all() and np.all(host(x)[:, 0] == 0.0)
+    assert rep.relative_residuals[0] == 0.0
+    t = P.stencil_csr((100,), [(0,), (-1,), (1,)], [2.0, -1.0, -1.0])
+    prob = DeviceProblem(dev, t)
+    rhs = np.zeros((100, 1))
+    rhs[0, 0] = 1.0
+    x = dev.zeros(100, 1)
+    _, rep = block_cg(dev, prob, 0.0, rm(dev, rhs), x, 3, 1e-14)
+    assert rep.iterations == 3 and not rep.converged.any()
+
+
+def test_reference_ffi_tier_golden(golden):
+    """gcgeig_* host-buffer entry points against the reference's KAT outputs."""
+    g = golden
+    out = np.zeros((120, 7), order="F")
+    refbackend.csr_matvec(g["k_csr_indptr"], g["k_csr_indices"], g["k_csr_data"], g["k_csr_x"], out)
+    assert np.abs(out - g["k_csr_out_numpy"]).max() <= 1e-13
+    for det in (0, 1):
+        ip = np.empty((6, 4), order="F")
+        refbackend.inner_product(g["k_ip_x"], g["k_ip_y"], ip, 512, bool(det))
+        assert np.abs(ip - g[f"k_ip_out_numpy_{det}"]).max() <= 1e-11
+    for i, (al, bt) in enumerate([(0.0, 0.0), (1.0, 0.0), (0.0, 1.0), (2.5, 1.0), (2.5, -0.5)]):
+        y = g["k_axpby_y"].copy(order="F")
+        refbackend.axpby(al, g["k_axpby_x"], bt, y)
+        assert np.abs(y - g[f"k_axpby_out_numpy_{i}"]).max() <= 1e-14
+    # strided out view, guard bytes untouched (test_multivec.py:129-139)
+    parent = np.full((8, 7), 7.5, order="F")
+    view = parent[1:7, 2:6]
+    refbackend.inner_product(g["k_ip_x"], g["k_ip_y"], view, 8, True)
+    assert np.abs(view - g["k_ip_out_numpy_0"]).max() <= 1e-11
+    mask = np.ones_like(parent, dtype=bool)
+    mask[1:7, 2:6] = False
+    assert np.all(parent[mask] == 7.5)
+
+
+def test_launch_counter_moves(dev):
+    before = _lib.launch_count()
+    y = dev.empty(10, 2)
+    D.fill(dev, y, 1.0)
+    assert _lib.launch_count() > before

@@ -1,0 +1,212 @@
+"""End-to-end parity of the device GCG solver against the reference (via golden
+vectors produced by the unmodified reference) and the reference's own solver
+test cases (test_solver.py, test_acceptance.py).
+
+Acceptance (north_star): eigenvalues to relative 1e-9, every returned pair
+with residual <= tol, eigenvectors within 1e-6 subspace angle per eigenvalue
+cluster; iteration counts within a small slack.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+import scipy.sparse
+
+from paper_2111_06552_b200 import SolverConfig, gcg_solve
+from paper_2111_06552_b200 import problems as P
+from paper_2111_06552_b200.errors import InvalidShape
+from tests.cases import SOLVER_CASES, problem, tri
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def host_residuals(a, b, vals, vecs, kind):
+    ax = a @ vecs
+    bx = vecs if b is None else b @ vecs
+    r = np.linalg.norm(ax - bx * vals, axis=0)
+    if kind == "relative":
+        return r / (np.abs(vals) * np.linalg.norm(bx, axis=0))
+    if b is None:
+        return r / np.linalg.norm(vecs, axis=0)
+    den = np.sqrt(np.einsum("ij,ij->j", vecs, bx))
+    return r / np.where(vals > 0, vals * den, den)
+
+
+def cluster_angles(vals, u, w, b=None, gap=1e-8):
+    """max sin(principal angle) between span(u_J) and span(w_J) per eigenvalue cluster J,
+    skipping a cluster that touches the last index (it may be cut by nev)."""
+    worst = 0.0
+    j = 0
+    k = len(vals)
+    while j < k:
+        e = j + 1
+        while e < k and abs(vals[e] - vals[e - 1]) <= gap * max(1.0, abs(vals[e])):
+            e += 1
+        if e < k:
+            bw = w[:, j:e] if b is None else b @ w[:, j:e]
+            m = u[:, j:e].T @ bw
+            s = np.linalg.svd(m, compute_uv=False)
+            worst = max(worst, float(np.sqrt(max(0.0, 1.0 - s.min() ** 2))))
+        j = e
+    return worst
+
+
+@pytest.mark.parametrize("name", SOLVER_CASES)
+def test_solver_matches_reference_golden(golden, golden_meta, name):
+    meta = golden_meta["solver"][name]
+    a, b = problem(name)
+    kw = dict(meta["kw"])
+    kind = "reference"
+    if meta["baseline_patch"]:
+        kw.update(init="normal", residual="relative")
+        kind = "relative"
+    rep = gcg_solve(a, b, SolverConfig(**kw))
+    tol = kw.get("tol", 1e-8)
+    want = golden[f"s_{name}_values"]
+    assert rep.status == meta["status"] == "converged"
+    assert rep.backend == "sm100"
+    assert rep.eigenvalues.shape == want.shape
+    assert np.abs(rep.eigenvalues - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+    assert rep.residuals.max() < tol
+    hres = host_residuals(a, b, rep.eigenvalues, rep.eigenvectors, kind)
+    assert hres.max() < 1.01 * tol
+    assert abs(rep.iterations - meta["iterations"]) <= max(3, meta["iterations"] // 10)
+    if f"s_{name}_vectors" in golden:
+        ang = cluster_angles(want, golden[f"s_{name}_vectors"], rep.eigenvectors, b)
+        assert ang <= 1e-6
+
+
+def test_cfg1_baseline_full_against_analytic():
+    pr = P.baseline_problem(1)
+    rep = gcg_solve(pr.a, None, SolverConfig(num_eigen=20, block_size=20, tol=1e-8, seed=0,
+                                             init="normal", residual="relative"))
+    exact = P.analytic_eigenvalues(1, 20)
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - exact).max() / exact.max() <= 1e-9
+    assert host_residuals(pr.a, None, rep.eigenvalues, rep.eigenvectors, "relative").max() <= 1e-8
+
+
+@pytest.mark.slow
+def test_cfg2_baseline_against_reference_run():
+    path = os.path.join(HERE, "golden", "golden_cfg2.json")
+    if not os.path.exists(path):
+        pytest.skip("golden_cfg2.json not generated")
+    ref = json.load(open(path))
+    pr = P.baseline_problem(2)
+    rep = gcg_solve(pr.a, None, SolverConfig(num_eigen=100, tol=1e-8, seed=0, init="normal",
+                                             residual="relative", validate=False))
+    want = np.array(ref["eigenvalues"])
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - want).max() / np.abs(want).max() <= 1e-9
+    exact = P.analytic_eigenvalues(2, 100)
+    assert np.abs(rep.eigenvalues - exact).max() / exact.max() <= 1e-9
+    assert rep.residuals.max() <= 1e-8
+    assert abs(rep.iterations - ref["iterations"]) <= 5
+
+
+# ---- reference solver test cases (test_solver.py) ---------------------------------
+
+
+def random_sym(n, seed):
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(-1, 1, (n, n))
+    return (m + m.T) / 2.0
+
+
+def test_diagonal_standard_problem():
+    d = np.arange(1.0, 101.0)
+    rep = gcg_solve(np.diag(d), config=SolverConfig(num_eigen=10, tol=1e-9, seed=4))
+    assert rep.status == "converged" and rep.num_converged == 10
+    assert np.abs(rep.eigenvalues - np.arange(1.0, 11.0)).max() <= 1e-7
+    assert rep.residuals.max() <= 1e-9
+    for j in range(10):
+        assert abs(rep.eigenvectors[j, j]) >= 1.0 - 1e-6
+
+
+def test_dense_standard_and_generalized():
+    a = random_sym(60, seed=10)
+    rep = gcg_solve(a, config=SolverConfig(num_eigen=8, tol=1e-10, seed=1))
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - scipy.linalg.eigh(a, eigvals_only=True)[:8]).max() <= 1e-8
+    a = random_sym(50, seed=20)
+    bm = random_sym(50, seed=21) + 50.0 * np.eye(50)
+    rep = gcg_solve(a, bm, SolverConfig(num_eigen=6, tol=1e-10, seed=2))
+    ref = scipy.linalg.eigh(a, bm, eigvals_only=True)[:6]
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - ref).max() <= 1e-8 * max(1.0, np.abs(ref).max())
+    g = rep.eigenvectors.T @ bm @ rep.eigenvectors
+    assert np.abs(g - np.eye(6)).max() <= 1e-8
+
+
+def test_sparse_laplacian_analytic():
+    n = 300
+    rep = gcg_solve(tri(n), config=SolverConfig(num_eigen=12, tol=1e-9, seed=5))
+    exact = 2.0 - 2.0 * np.cos(np.arange(1, 13) * np.pi / (n + 1))
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - exact).max() <= 1e-8
+
+
+def test_shift_modes_and_moving():
+    a = tri(150)
+    r_dyn = gcg_solve(a, config=SolverConfig(num_eigen=6, seed=6, shift_mode="dynamic"))
+    r_non = gcg_solve(a, config=SolverConfig(num_eigen=6, seed=6, shift_mode="none"))
+    assert np.abs(r_dyn.eigenvalues - r_non.eigenvalues).max() <= 1e-7
+    assert any(h.theta > 0 for h in r_dyn.history)
+    assert all(h.theta == 0 for h in r_non.history)
+    a = tri(200)
+    plain = gcg_solve(a, config=SolverConfig(num_eigen=30, block_size=8, seed=7))
+    moving = gcg_solve(a, config=SolverConfig(num_eigen=30, block_size=8, seed=7, moving=True))
+    assert plain.status == moving.status == "converged"
+    assert np.abs(plain.eigenvalues - moving.eigenvalues).max() <= 1e-7
+    assert moving.max_projection_dim <= 5 * 8
+    assert moving.residuals.max() <= 1e-7
+
+
+def test_max_iterations_and_validation():
+    rep = gcg_solve(np.diag(np.arange(1.0, 40.0)),
+                    config=SolverConfig(num_eigen=5, tol=1e-12, max_gcg_iters=2, seed=8))
+    assert rep.status == "max_iterations" and rep.iterations == 2 and len(rep.history) == 2
+    a = np.diag(np.arange(1.0, 11.0))
+    for cfg in (SolverConfig(num_eigen=0), SolverConfig(num_eigen=11),
+                SolverConfig(num_eigen=2, shift_mode="bogus")):
+        with pytest.raises(InvalidShape):
+            gcg_solve(a, config=cfg)
+    with pytest.raises(InvalidShape):
+        gcg_solve(a, np.ones(7), SolverConfig(num_eigen=2))
+
+
+def test_deterministic_bitwise_repeat():
+    a = tri(120)
+    cfg = lambda: SolverConfig(num_eigen=5, seed=13, deterministic=True)  # noqa: E731
+    r1, r2 = gcg_solve(a, config=cfg()), gcg_solve(a, config=cfg())
+    assert np.array_equal(r1.eigenvalues, r2.eigenvalues)
+    assert np.array_equal(r1.eigenvectors, r2.eigenvectors)
+    assert r1.iterations == r2.iterations
+    assert all(h.timings == {k: 0.0 for k in h.timings} for h in r1.history)
+
+
+def test_instrumentation_defects_are_tiny():
+    a = tri(100)
+    b = scipy.sparse.diags([np.ones(99), 4.0 * np.ones(100), np.ones(99)], [-1, 0, 1], format="csr")
+    rep = gcg_solve(a, b, SolverConfig(num_eigen=6, seed=14, instrument_orth=True,
+                                       cross_check_abar=True))
+    assert rep.status == "converged"
+    defects = [h.basis_defect for h in rep.history if h.basis_defect is not None]
+    cross = [h.abar_defect for h in rep.history if h.abar_defect is not None]
+    assert defects and max(defects) <= 1e-9
+    assert cross and max(cross) <= 1e-10
+
+
+def test_history_bookkeeping():
+    rep = gcg_solve(np.diag(np.arange(1.0, 41.0)), config=SolverConfig(num_eigen=6, seed=11))
+    iters = [h.iteration for h in rep.history]
+    assert iters == list(range(1, len(iters) + 1))
+    conv = [h.num_converged for h in rep.history]
+    assert all(y >= x for x, y in zip(conv, conv[1:]))
+    assert rep.total_reductions >= sum(h.orth_reductions for h in rep.history)
+    assert rep.max_projection_dim <= 14 + 2 * 2 or rep.max_projection_dim <= 40

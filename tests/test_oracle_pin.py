@@ -12,6 +12,7 @@ import pytest
 
 from oracle import gcg_oracle as O
 from paper_2111_06552_b200 import problems as P
+from tests.cases import SOLVER_CASES, problem as _problem
 
 
 def test_kernel_kats(golden):
@@ -66,26 +67,6 @@ def test_dense(golden):
     w, v = O.eig_full(golden["m8"])
     assert np.abs(w - golden["m8_values"]).max() < 1e-14
     assert np.abs(v - golden["m8_vectors"]).max() < 1e-13
-
-
-def _problem(name):
-    fem_a, fem_b = P.fem_p1_cube(6)
-    tri = lambda n: P.stencil_csr((n,), [(0,), (-1,), (1,)], [2.0, -1.0, -1.0])  # noqa: E731
-    return {
-        "tri120": (tri(120), None),
-        "lap2d20": (P.laplacian_2d(20), None),
-        "fem6": (fem_a, fem_b),
-        "tri200_moving": (tri(200), None),
-        "lap3d10_noshift": (P.laplacian_3d(10), None),
-        "lap3d12_baseline": (P.laplacian_3d(12), None),
-        "fem8_baseline": P.fem_p1_cube(8),
-        "varcoef10_moving": (P.varcoef_diffusion_3d(10, seed=0), None),
-        "cfg1_baseline": (P.laplacian_2d(100), None),
-    }[name]
-
-
-SOLVER_CASES = ["tri120", "lap2d20", "fem6", "tri200_moving", "lap3d10_noshift",
-                "lap3d12_baseline", "fem8_baseline", "varcoef10_moving", "cfg1_baseline"]
 
 
 @pytest.mark.parametrize("name", SOLVER_CASES)
