@@ -1,0 +1,362 @@
+"""Benchmark: time-to-nev of the GCG eigensolver on the B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+
+A step is one complete solve (time-to-nev) of BASELINE config 2 — the 3-D
+7-point Laplacian on 64^3 (n = 262,144), nev = 100, tol 1e-8, N(0,1) initial
+block from seed 0, north-star residual criterion — through the drop-in
+`gcg_solve`.  `value` is the device-timed solve with the matrix and the seeded
+initial block already resident in HBM; `e2e` times the public call with host
+buffers (CSR + initial block H2D, eigenpairs D2H inside the timed region).
+
+--impl reference times the reference's own CPU implementation (the unmodified
+gcgeig built into oracle/_ref by oracle/build_ref.sh, else the oracle port) on
+a bounded sample (a few GCG iterations per step) and extrapolates to the
+reference's full iteration count; see DESIGN.md §6.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-nev (s)"
+UNIT = "s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def solver_kwargs(pr):
+    return dict(num_eigen=pr.num_eigen, block_size=pr.block_size, tol=pr.tol, moving=pr.moving,
+                seed=0)
+
+
+def initial_block(pr):
+    """The seeded N(0,1) block both arms start from."""
+    n = pr.a.shape[0]
+    bs = pr.block_size or max(1, -(-pr.num_eigen // 5))
+    sx = min(3 * bs, n) if pr.moving else min(pr.num_eigen + 3 * bs, n)
+    return np.random.Generator(np.random.PCG64(0)).standard_normal((n, sx))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+        0x2: "applications_clocks_setting", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm
+
+
+def reference_solver():
+    """(gcg_solve, SolverConfig, kind) of the reference, patched per BASELINE.md §3."""
+    import oracle
+
+    g = oracle.load_reference()
+    if g is not None:
+        import math
+
+        from gcgeig import SolverConfig, gcg_solve
+        from gcgeig import _kernels as K
+        from gcgeig import solver as S
+
+        def normal(x, seed):
+            x[...] = np.random.Generator(np.random.PCG64(seed)).standard_normal(x.shape)
+            return x
+
+        def rel(ax, x, bx, lam, generalized):
+            r = ax - lam * bx
+            den = abs(lam) * math.sqrt(float(bx @ bx))
+            return math.sqrt(float(r @ r)) / (den if den != 0.0 else 1.0)
+
+        S.mv_set_random, S._rel_residual = normal, rel
+        K.use_backend("numpy")  # multithreaded BLAS beats the 1-thread Cython core at scale
+
+        def run(a, b, kw):
+            return gcg_solve(a, b, SolverConfig(**kw))
+
+        return run, "reference"
+    from oracle import gcg_oracle as O
+
+    def run(a, b, kw):
+        return O.gcg_solve(a, b, O.OracleConfig(**kw, init="normal", residual="relative"))
+
+    return run, "port"
+
+
+def reference_iterations(cfg):
+    """Full-solve GCG iteration count of the reference (committed golden run), if known."""
+    path = os.path.join(ROOT, "tests", "golden", f"golden_cfg{cfg}.json")
+    if os.path.exists(path):
+        return int(json.load(open(path))["iterations"]), "reference full solve (tests/golden)"
+    return None, None
+
+
+def cpu_sample(pr, iters, cfg):
+    """Time `iters` GCG iterations of the reference on this host; extrapolate time-to-nev."""
+    run, kind = reference_solver()
+    kw = solver_kwargs(pr)
+    kw["max_gcg_iters"] = iters
+    t0 = time.perf_counter()
+    run(pr.a, pr.b, kw)
+    dt = time.perf_counter() - t0
+    full, src = reference_iterations(cfg)
+    return dt, kind, full, src
+
+
+def run_reference_arm(args, pr, rank, world):
+    if rank != 0:
+        return
+    total = args.steps + args.warmup
+    iters = 2 if total <= 6 else 1
+    times = []
+    kind = full = src = None
+    for s in range(total):
+        dt, kind, full, src = cpu_sample(pr, iters, args.config)
+        if s >= args.warmup:
+            times.append(dt)
+    per_iter = statistics.mean(times) / iters
+    if full is None:
+        full = 43
+        src = "assumed 43 iterations"
+    value = per_iter * full
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE generator, seeded N(0,1) initial block)",
+        "config": {"workload": pr.name, "n": pr.a.shape[0], "nnz": int(pr.a.nnz),
+                   "nev": pr.num_eigen, "tol": pr.tol},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{iters} GCG iteration(s) per step, {per_iter:.2f} s/iter, "
+                                   f"x {full} iterations ({src})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gcg_iters_per_s": 1.0 / per_iter,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2111_06552_b200 import problems as P
+
+    pr = P.baseline_problem(args.config)
+    if args.impl == "reference":
+        run_reference_arm(args, pr, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2111_06552_b200 import SolverConfig, _lib, gcg_solve
+    from paper_2111_06552_b200 import device as D
+    from paper_2111_06552_b200.operators import as_device_problem
+
+    ctx = D.default_context()
+    kw = solver_kwargs(pr)
+    x0_host = initial_block(pr)
+    prob = as_device_problem(ctx, pr.a, pr.b, validate=False)
+    x0_dev = torch.from_numpy(x0_host).to(ctx.device)
+    cfg = SolverConfig(**kw, init="normal", residual="relative", validate=False, return_device=True,
+                       collect_history=True)
+
+    def step():
+        return gcg_solve(prob, None, cfg, x0=x0_dev)
+
+    for _ in range(args.warmup):
+        rep = step()
+    barrier = (lambda: dist.barrier()) if world > 1 else (lambda: None)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    iters = []
+    with ClockSampler(local) as clk, D.KernelProfile(ctx) as prof:
+        ev0.record(ctx.stream)
+        for _ in range(args.steps):
+            rep = step()
+            iters.append(rep.iterations)
+        ev1.record(ctx.stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=ctx.device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    t_solve = ms / 1e3 / args.steps
+    assert rep.status == "converged" and rep.residuals.max() <= pr.tol, (rep.status, rep.residuals.max())
+
+    # end-to-end through the public call with host buffers (pinned CSR + x0 in, eigenpairs out)
+    e2e = None
+    if not args.no_e2e:
+        import scipy.sparse
+
+        a_pinned = scipy.sparse.csr_matrix(pr.a)
+        x0_pin = torch.from_numpy(x0_host).pin_memory()
+        cfg_h = SolverConfig(**kw, init="normal", residual="relative", validate=False)
+        h2d = (a_pinned.data.nbytes + a_pinned.indices.astype(np.int32).nbytes
+               + a_pinned.indptr.astype(np.int32).nbytes + x0_pin.numel() * 8)
+        torch.cuda.synchronize()
+        barrier()
+        te = []
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rh = gcg_solve(a_pinned, pr.b, cfg_h, x0=x0_pin)
+            torch.cuda.synchronize()
+            te.append(time.perf_counter() - t0)
+        d2h = rh.eigenvectors.nbytes + rh.eigenvalues.nbytes + rh.residuals.nbytes
+        e_val = statistics.mean(te)
+        if world > 1:
+            t = torch.tensor([e_val], device=ctx.device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_val = float(t.item())
+        e2e = {"value": e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # roofline of the dominant kernel class (live CUDA-event timing inside the timed region)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    res = prof.result
+    dom = max(res, key=lambda k: res[k]["ms"])
+    r = res[dom]
+    achieved = (r["bytes"] / r["launches"]) / (r["ms"] / r["launches"] / 1e3) / 1e9 if r["launches"] else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                   "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
+               for k, v in res.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            dt, kind, full, src = cpu_sample(pr, 2, args.config)
+            if full is None:
+                full, src = rep.iterations, "this run's GPU iteration count"
+            cpu = {"value": dt / 2 * full, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                   "sample": f"2 GCG iterations of {pr.name} in {dt:.1f} s "
+                             f"({'gcgeig numpy backend' if kind == 'reference' else 'oracle port'}), "
+                             f"extrapolated to {full} iterations ({src})"}
+        except Exception as exc:  # keep the GPU line even if the CPU leg fails
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": t_solve, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE generator, seeded N(0,1) initial block)",
+            "config": {"workload": pr.name, "n": pr.a.shape[0], "nnz": int(pr.a.nnz),
+                       "nev": pr.num_eigen, "tol": pr.tol, "criterion": "north-star relative",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "working set > 126 MB L2 (V arena 0.42 GB + CG blocks), no flush"},
+            "iterations": iters[-1], "gcg_iters_per_s": iters[-1] / t_solve,
+            "max_residual": float(rep.residuals.max()),
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "kernels": kernels,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -60,6 +60,12 @@ int gcg_ctx_set_stream(void* ctx, void* cuda_stream);
 int gcg_ctx_sync(void* ctx);
 /* number of kernels this library has launched since load (instrumentation) */
 int64_t gcg_launch_count(void);
+/* Live kernel timing: between begin and end every SpMM / Gram / LinComb / CG-update /
+ * CG-p-update launch on this ctx is bracketed by CUDA events on the ctx stream.
+ * end() synchronises and writes out[3*cls + {0,1,2}] = {total ms, launches,
+ * algorithmic HBM bytes} for cls = 0..4 in that order. */
+int gcg_prof_begin(void* ctx);
+int gcg_prof_end(void* ctx, double* out);
 
 /* ---- tier 1: reference-FFI mirror (host buffers, column-major) ----------- */
 /* out[:, c] = A @ x[:, c];  A is nrow x ncol CSR (int64 indptr/indices, f64 data);
@@ -81,7 +87,7 @@ int gcgeig_axpby(double alpha, const double* x, int64_t n, int64_t k, int64_t ld
  * int32 indices.  beta == 0 never reads Yin; gamma == 0 never reads Z.
  * dot_mode 0: none; 1: dots[c] = sum_i Y[i,c] W[i,c]; 2: dots[c] = sum_i Y[i,c]^2
  * (deterministic fixed-order reduction). */
-int gcg_spmm_csr(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+int gcg_spmm_csr(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
                  const double* val, int64_t k, const double* X, int64_t ldx, double alpha,
                  double gamma, const double* Z, int64_t ldz, double beta, const double* Yin,
                  int64_t ldyin, double* Y, int64_t ldy, int dot_mode, const double* W,
@@ -116,7 +122,7 @@ int gcg_fill(void* ctx, int64_t n, int64_t k, double value, double* X, int64_t l
  * stored on A's pattern).  x holds x0 on entry and the iterate on exit.  Per column:
  * stop at rel_tol*||r0|| or after max_iters sweeps, freeze on p'op p <= 0 (cg.py:33-99).
  * Outputs stay on device: *d_sweeps, d_converged[k], d_frozen[k], d_relres[k]. */
-int gcg_block_cg(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+int gcg_block_cg(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
                  const double* val, double diag_shift, int64_t k, const double* rhs,
                  int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
                  int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres);

@@ -28,8 +28,10 @@ _SIGS = {
     "gcgeig_csr_matvec": [_ptr, _ptr, _ptr, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64],
     "gcgeig_inner_product": [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _int],
     "gcgeig_axpby": [_dbl, _ptr, _i64, _i64, _i64, _dbl, _ptr, _i64],
-    "gcg_spmm_csr": [_ptr, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _dbl,
-                     _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
+    "gcg_prof_begin": [_ptr],
+    "gcg_prof_end": [_ptr, _ptr],
+    "gcg_spmm_csr": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64,
+                     _dbl, _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
     "gcg_gram": [_ptr, _i64, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _i64, _ptr,
                  _i64, _ptr],
     "gcg_lincomb": [_ptr, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64],
@@ -38,8 +40,8 @@ _SIGS = {
     "gcg_col_scale": [_ptr, _i64, _i64, _ptr, _ptr, _i64],
     "gcg_col_dots": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr],
     "gcg_fill": [_ptr, _i64, _i64, _dbl, _ptr, _i64],
-    "gcg_block_cg": [_ptr, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64, _i32, _dbl,
-                     _ptr, _ptr, _ptr, _ptr],
+    "gcg_block_cg": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64, _i32,
+                     _dbl, _ptr, _ptr, _ptr, _ptr],
     "gcg_syev": [_ptr, _i64, _ptr, _i64, _ptr, _ptr, _i64],
     "gcg_dgemm": [_ptr, _int, _int, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr,
                   _i64],

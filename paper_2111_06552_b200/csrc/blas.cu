@@ -130,10 +130,12 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
   GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)nslab * k1 * k2));
   double* part = (double*)c->partials.ptr;
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, (unsigned)nslab);
+  const int ps = prof_start(c, PROF_GRAM, 8.0 * n * (X == Y ? k1 : k1 + k2));
   if (big)
     gram_kernel<64, 64, 4, 4><<<grid, 256, 0, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
   else
     gram_kernel<32, 32, 2, 2><<<grid, 256, 0, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+  prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   const long long tot = (long long)k1 * k2;
@@ -210,6 +212,7 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
                    long long ldx, const double* C, long long ldc, double beta, double* Y,
                    long long ldy) {
   if (n <= 0 || d <= 0) return GCG_OK;
+  const int ps = prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
   if (d <= 32) {
     dim3 grid((unsigned)((n + 127) / 128), (d + 31) / 32);
     lincomb_kernel<128, 32, 4, 4><<<grid, 256, 0, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc,
@@ -219,6 +222,7 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
     lincomb_kernel<64, 64, 4, 4><<<grid, 256, 0, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc,
                                                                beta, Y, ldy);
   }
+  prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;

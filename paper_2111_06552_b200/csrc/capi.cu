@@ -18,7 +18,7 @@ namespace gcg {
 
 extern int64_t g_launches;
 
-int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
+int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                      const double* val, int k, const double* X, long long ldx, double alpha,
                      double gamma, const double* Z, long long ldz, double beta, const double* Yin,
                      long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
@@ -42,7 +42,7 @@ int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, cons
                  long long lda, const double* B, long long ldb, double beta, double* C,
                  long long ldc);
 int symmetrize_launch(Ctx* c, int m, double* A, long long lda);
-int block_cg_launch(Ctx* c, long long n, const int* rowptr, const int* colidx, const double* val,
+int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx, const double* val,
                     double shift, int k, const double* rhs, long long ldr, double* x,
                     long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
                     int8_t* d_frozen, double* d_relres);
@@ -76,6 +76,46 @@ int ensure(Scratch& s, size_t bytes) {
   }
   s.bytes = want;
   return GCG_OK;
+}
+
+int prof_start(Ctx* c, int cls, double bytes) {
+  Prof& p = c->prof;
+  if (!p.on) return -1;
+  if (p.used == p.cap) {
+    // grow: only between profiled regions is the device flag array reallocated safely,
+    // so allocate generously up front and stop recording when full
+    return -1;
+  }
+  const int slot = p.used++;
+  p.cls[slot] = cls;
+  p.bytes[slot] = bytes;
+  cudaEventRecord(p.ev[2 * slot], c->stream);
+  return slot;
+}
+
+int* prof_skip_slot(Ctx* c, int slot) {
+  return slot < 0 ? nullptr : c->prof.d_skipped + slot;
+}
+
+static int prof_reserve(Prof& p, int cap) {
+  if (p.cap >= cap) return GCG_OK;
+  cudaEvent_t* ev = (cudaEvent_t*)realloc(p.ev, sizeof(cudaEvent_t) * 2 * cap);
+  int* cl = (int*)realloc(p.cls, sizeof(int) * cap);
+  double* by = (double*)realloc(p.bytes, sizeof(double) * cap);
+  if (!ev || !cl || !by) return GCG_ERR_ALLOC;
+  for (int i = 2 * p.cap; i < 2 * cap; ++i) cudaEventCreate(&ev[i]);
+  p.ev = ev;
+  p.cls = cl;
+  p.bytes = by;
+  if (p.d_skipped) cudaFree(p.d_skipped);
+  if (cudaMalloc(&p.d_skipped, sizeof(int) * cap) != cudaSuccess) return GCG_ERR_ALLOC;
+  p.cap = cap;
+  return GCG_OK;
+}
+
+void prof_stop(Ctx* c, int slot) {
+  if (slot < 0) return;
+  cudaEventRecord(c->prof.ev[2 * slot + 1], c->stream);
 }
 
 static void release(Scratch& s) {
@@ -190,9 +230,50 @@ int gcg_ctx_sync(void* p) {
   return cuda_status(cudaStreamSynchronize(c->stream));
 }
 
+int gcg_prof_begin(void* p) {
+  Ctx* c = CTX(p);
+  if (!c) return GCG_ERR_ARG;
+  cudaStreamSynchronize(c->stream);
+  GCG_TRY(prof_reserve(c->prof, 1 << 18));
+  GCG_TRY(cuda_status(cudaMemsetAsync(c->prof.d_skipped, 0, sizeof(int) * c->prof.cap,
+                                      c->stream)));
+  c->prof.on = true;
+  c->prof.used = 0;
+  return GCG_OK;
+}
+
+int gcg_prof_end(void* p, double* out) {
+  Ctx* c = CTX(p);
+  if (!c || !out) return GCG_ERR_ARG;
+  Prof& pr = c->prof;
+  pr.on = false;
+  GCG_TRY(cuda_status(cudaStreamSynchronize(c->stream)));
+  double ms[PROF_NCLASS] = {0}, by[PROF_NCLASS] = {0}, nl[PROF_NCLASS] = {0};
+  std::vector<int> skipped(pr.used > 0 ? pr.used : 1, 0);
+  if (pr.used > 0)
+    GCG_TRY(cuda_status(cudaMemcpy(skipped.data(), pr.d_skipped, sizeof(int) * pr.used,
+                                   cudaMemcpyDeviceToHost)));
+  for (int s = 0; s < pr.used; ++s) {
+    if (skipped[s]) continue;  // CG early-exit no-op: no work, no bytes
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, pr.ev[2 * s], pr.ev[2 * s + 1]) == cudaSuccess) {
+      ms[pr.cls[s]] += t;
+      by[pr.cls[s]] += pr.bytes[s];
+      nl[pr.cls[s]] += 1.0;
+    }
+  }
+  cudaGetLastError();
+  for (int i = 0; i < PROF_NCLASS; ++i) {
+    out[3 * i + 0] = ms[i];
+    out[3 * i + 1] = nl[i];
+    out[3 * i + 2] = by[i];
+  }
+  return GCG_OK;
+}
+
 // ---- device tier ------------------------------------------------------------
 
-int gcg_spmm_csr(void* p, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+int gcg_spmm_csr(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
                  const double* val, int64_t k, const double* X, int64_t ldx, double alpha,
                  double gamma, const double* Z, int64_t ldz, double beta, const double* Yin,
                  int64_t ldyin, double* Y, int64_t ldy, int dot_mode, const double* W,
@@ -204,7 +285,7 @@ int gcg_spmm_csr(void* p, int64_t n, const int32_t* rowptr, const int32_t* colid
   if (beta != 0.0 && !Yin) return GCG_ERR_ARG;
   if (dot_mode < 0 || dot_mode > 2 || (dot_mode && !dots) || (dot_mode == 1 && !W))
     return GCG_ERR_ARG;
-  return spmm_launch_impl(c, n, rowptr, colidx, val, (int)k, X, ldx, alpha, gamma, Z, ldz, beta,
+  return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, (int)k, X, ldx, alpha, gamma, Z, ldz, beta,
                           Yin, ldyin, Y, ldy, dot_mode, W, ldw, dots, nullptr, nullptr, nullptr);
 }
 
@@ -272,7 +353,7 @@ int gcg_fill(void* p, int64_t n, int64_t k, double value, double* X, int64_t ldx
   return fill_launch(c, n, (int)k, value, X, ldx);
 }
 
-int gcg_block_cg(void* p, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+int gcg_block_cg(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
                  const double* val, double diag_shift, int64_t k, const double* rhs,
                  int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
                  int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres) {
@@ -280,7 +361,7 @@ int gcg_block_cg(void* p, int64_t n, const int32_t* rowptr, const int32_t* colid
   if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
-  return block_cg_launch(c, n, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
+  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
                          max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres);
 }
 
@@ -436,7 +517,7 @@ int gcgeig_csr_matvec(const int64_t* indptr, const int64_t* indices, const doubl
   cm_to_rm_kernel<<<elem_grid_host(c, ncol * k), 256, 0, s>>>(ncol, (int)k, d_xcm, ncol, d_xrm);
   ++g_launches;
   GCG_CHECK_LAUNCH();
-  GCG_TRY(spmm_launch_impl(c, nrow, d_i32, d_i32 + nrow + 1, d_val, (int)k, d_xrm, k, 1.0, 0.0,
+  GCG_TRY(spmm_launch_impl(c, nrow, nnz, d_i32, d_i32 + nrow + 1, d_val, (int)k, d_xrm, k, 1.0, 0.0,
                            nullptr, 0, 0.0, nullptr, 0, d_yrm, k, 0, nullptr, 0, nullptr, nullptr,
                            nullptr, nullptr));
   rm_to_cm_kernel<<<elem_grid_host(c, nrow * k), 256, 0, s>>>(nrow, (int)k, d_yrm, d_ycm);

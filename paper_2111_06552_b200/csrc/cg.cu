@@ -20,7 +20,7 @@
 namespace gcg {
 
 extern int64_t g_launches;
-int spmm_launch_parts(Ctx* c, long long n, const int* rowptr, const int* colidx,
+int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                       const double* val, int k, const double* X, long long ldx, double alpha,
                       double gamma, const double* Z, long long ldz, double beta,
                       const double* Yin, long long ldyin, double* Y, long long ldy, int dot_mode,
@@ -129,8 +129,11 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
                                                         const double* __restrict__ p,
                                                         const double* __restrict__ q,
                                                         long long rows_per_cta, double* part,
-                                                        CgState s) {
-  if (*s.skip) return;
+                                                        CgState s, int* prof_skipped) {
+  if (*s.skip) {
+    if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
+    return;
+  }
   __shared__ double sm[256];
   const int kc = k;  // k <= 256 (checked by the launcher)
   const int lanes = 256 / kc;
@@ -163,8 +166,11 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
 
 // p = r + beta p for columns still iterating
 __global__ void cg_pupdate_kernel(long long n, int k, const double* __restrict__ r, double* p,
-                                  CgState s) {
-  if (*s.skip) return;
+                                  CgState s, int* prof_skipped) {
+  if (*s.skip) {
+    if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
+    return;
+  }
   const long long tot = n * k;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
        e += (long long)gridDim.x * blockDim.x) {
@@ -184,7 +190,7 @@ __global__ void cg_final(int k, CgState s, int* d_sweeps, int8_t* conv, int8_t* 
   if (threadIdx.x == 0) *d_sweeps = *s.sweeps;
 }
 
-int block_cg_launch(Ctx* c, long long n, const int* rowptr, const int* colidx, const double* val,
+int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx, const double* val,
                     double shift, int k, const double* rhs, long long ldr, double* x,
                     long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
                     int8_t* d_frozen, double* d_relres) {
@@ -222,7 +228,7 @@ int block_cg_launch(Ctx* c, long long n, const int* rowptr, const int* colidx, c
 
   // r = rhs - op(x) = -(A x) - shift*x + rhs ; ||r0||^2 partials
   int g = 0;
-  GCG_TRY(spmm_launch_parts(c, n, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0, rhs,
+  GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0, rhs,
                             ldr, R, k, 2, nullptr, 0, part, &g, nullptr));
   cg_init_fin<<<1, fin_threads, 0, c->stream>>>(k, part, g, rel_tol, s);
   ++g_launches;
@@ -230,12 +236,17 @@ int block_cg_launch(Ctx* c, long long n, const int* rowptr, const int* colidx, c
   GCG_TRY(copy_launch(c, n, k, R, k, P, k));
   const int pgrid = grid_for(n * k, 1024, 8, c->num_sms);
   for (int it = 0; it < max_iters; ++it) {
-    GCG_TRY(spmm_launch_parts(c, n, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0, nullptr,
+    GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0, nullptr,
                               0, Q, k, 1, P, k, part, &g, s.skip));
     cg_fin1<<<1, fin_threads, 0, c->stream>>>(k, part, g, s);
-    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, Q, rpc, part, s);
+    int ps = prof_start(c, PROF_CG_UPDATE, 48.0 * n * k);
+    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, Q, rpc, part, s,
+                                                   prof_skip_slot(c, ps));
+    prof_stop(c, ps);
     cg_fin2<<<1, fin_threads, 0, c->stream>>>(k, part, ugrid, s);
-    cg_pupdate_kernel<<<pgrid, 256, 0, c->stream>>>(n, k, R, P, s);
+    ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
+    cg_pupdate_kernel<<<pgrid, 256, 0, c->stream>>>(n, k, R, P, s, prof_skip_slot(c, ps));
+    prof_stop(c, ps);
     g_launches += 4;
     GCG_CHECK_LAUNCH();
   }

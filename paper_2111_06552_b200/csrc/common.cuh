@@ -24,7 +24,23 @@ struct Scratch {
   size_t bytes = 0;
 };
 
+// Live per-kernel-class timing (CUDA events on the ctx stream around each
+// launch) + algorithmic byte counts, for bench.py's roofline.  Off by default.
+enum ProfClass { PROF_SPMM = 0, PROF_GRAM, PROF_LINCOMB, PROF_CG_UPDATE, PROF_CG_PUPDATE,
+                 PROF_NCLASS };
+
+struct Prof {
+  bool on = false;
+  cudaEvent_t* ev = nullptr;   // pool of events, pairs (start, stop)
+  int* cls = nullptr;          // class of each pair
+  double* bytes = nullptr;     // algorithmic bytes of each pair
+  int* d_skipped = nullptr;    // device flags: the launch was a CG early-exit no-op
+  int cap = 0;                 // pairs
+  int used = 0;
+};
+
 struct Ctx {
+  Prof prof;
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   int num_sms = kNumSMs;
@@ -83,6 +99,12 @@ inline int grid_for(long long work_items, int items_per_cta, int ctas_per_sm, in
   if (need < 1) need = 1;
   return (int)(need < cap ? need : cap);
 }
+
+// profiling: prof_start returns a pair slot (or -1 when off), prof_stop closes it
+int prof_start(Ctx* c, int cls, double bytes);
+void prof_stop(Ctx* c, int slot);
+// device flag slot of a prof_start pair (nullptr when profiling is off)
+int* prof_skip_slot(Ctx* c, int slot);
 
 // internal launchers shared between translation units
 int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* out,

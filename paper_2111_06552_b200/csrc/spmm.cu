@@ -42,6 +42,7 @@ struct SpmmArgs {
   long long ldw;
   double* partials;  // [gridDim.x][k]
   const int* skip;   // device flag: nonzero -> kernel is a no-op (CG early exit)
+  int* prof_skipped; // profiling: set when the launch was a no-op
 };
 
 template <int VEC>
@@ -64,7 +65,10 @@ constexpr int kSpmmThreads = 256;
 
 template <int LPR, int VEC, int NV>
 __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(SpmmArgs a) {
-  if (a.skip != nullptr && *a.skip) return;
+  if (a.skip != nullptr && *a.skip) {
+    if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
+    return;
+  }
   constexpr int G = 32 / LPR;  // row groups per warp
   constexpr int COLS = LPR * VEC * NV;
   const int lane = threadIdx.x & 31;
@@ -231,7 +235,7 @@ int spmm_grid(Ctx* c, long long n) { return grid_for(n, 64, 8, c->num_sms); }
 // One SpMM over all k columns, split into passes of at most 256 columns.  With
 // dot_mode != 0 and `partials` given, per-CTA partials ([grid][k], k <= 256)
 // are left for the caller to reduce; otherwise they are reduced into `dots`.
-int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
+int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                      const double* val, int k, const double* X, long long ldx, double alpha,
                      double gamma, const double* Z, long long ldz, double beta, const double* Yin,
                      long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
@@ -281,7 +285,15 @@ int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
     a.ldw = ldw;
     a.partials = partials;
     a.skip = skip;
+    // algorithmic bytes: index/value stream + X once + Y once + each extra distinct stream
+    double bytes = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * kc;
+    if (gamma != 0.0 && Z != X) bytes += 8.0 * n * kc;
+    if (beta != 0.0) bytes += 8.0 * n * kc;
+    if (dot_mode == 1 && W != X && W != Z) bytes += 8.0 * n * kc;
+    const int ps = prof_start(c, PROF_SPMM, bytes);
+    a.prof_skipped = prof_skip_slot(c, ps);
     int s = vec2 ? launch_lpr<2>(c, a, lpr, nv, grid) : launch_lpr<1>(c, a, lpr, nv, grid);
+    prof_stop(c, ps);
     if (s != GCG_OK) return s;
     if (dot_mode && !partials_ext) {
       GCG_TRY(reduce_partials(c, partials, grid, kc, dots + c0, 1, 0));
@@ -291,13 +303,13 @@ int spmm_launch_impl(Ctx* c, long long n, const int* rowptr, const int* colidx,
   return GCG_OK;
 }
 
-int spmm_launch_parts(Ctx* c, long long n, const int* rowptr, const int* colidx,
+int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                       const double* val, int k, const double* X, long long ldx, double alpha,
                       double gamma, const double* Z, long long ldz, double beta,
                       const double* Yin, long long ldyin, double* Y, long long ldy, int dot_mode,
                       const double* W, long long ldw, double* partials, int* grid_out,
                       const int* skip) {
-  return spmm_launch_impl(c, n, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta, Yin,
+  return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta, Yin,
                           ldyin, Y, ldy, dot_mode, W, ldw, nullptr, partials, grid_out, skip);
 }
 

@@ -72,6 +72,34 @@ class Context:
         return t.to(self.device, non_blocking=False)
 
 
+PROF_CLASSES = ("spmm", "gram", "lincomb", "cg_update", "cg_pupdate")
+
+
+class KernelProfile:
+    """Live CUDA-event timing of the library's hot kernels on the ctx stream.
+
+        with KernelProfile(ctx) as prof: ...      # prof.result after exit
+    result[cls] = {"ms": total ms, "launches": n, "bytes": algorithmic HBM bytes}.
+    """
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.result = None
+
+    def __enter__(self):
+        _lib.call("gcg_prof_begin", self.ctx.h)
+        return self
+
+    def __exit__(self, *exc):
+        out = (C.c_double * (3 * len(PROF_CLASSES)))()
+        _lib.call("gcg_prof_end", self.ctx.h, out)
+        self.result = {
+            name: {"ms": out[3 * i], "launches": int(out[3 * i + 1]), "bytes": out[3 * i + 2]}
+            for i, name in enumerate(PROF_CLASSES)
+        }
+        return False
+
+
 def default_context():
     ctx = getattr(_tls, "ctx", None)
     if ctx is None:
@@ -107,7 +135,7 @@ def spmm(ctx, A, X, Y, alpha=1.0, gamma=0.0, Z=None, beta=0.0, Yin=None, dot_mod
     if X.shape != (A.n, k):
         raise InvalidShape(f"spmm: X {tuple(X.shape)} vs operator dim {A.n}, {k} cols")
     v = A.val if vals is None else vals
-    _lib.call("gcg_spmm_csr", ctx.h, n, _p(A.rowptr), _p(A.colidx), _p(v), k, _p(X), _ld(X),
+    _lib.call("gcg_spmm_csr", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(v), k, _p(X), _ld(X),
               float(alpha), float(gamma), _p(Z), _ld(Z), float(beta), _p(Yin), _ld(Yin), _p(Y),
               _ld(Y), int(dot_mode), _p(W), _ld(W), _p(dots))
     return Y
@@ -239,6 +267,6 @@ def ritz_residuals(ctx, AX, X, BX, lam, mode, out):
 
 def block_cg(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
     n, k = x.shape
-    _lib.call("gcg_block_cg", ctx.h, n, _p(A.rowptr), _p(A.colidx), _p(vals), float(shift), k,
+    _lib.call("gcg_block_cg", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(vals), float(shift), k,
               _p(rhs), _ld(rhs), _p(x), _ld(x), int(max_iters), float(rel_tol), _p(sweeps),
               _p(conv), _p(frozen), _p(relres))

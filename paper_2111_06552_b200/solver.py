@@ -251,8 +251,14 @@ class _Solve:
         return q, kept
 
 
-def gcg_solve(a, b=None, config=None):
-    """Run the block eigensolver on the B200; returns a :class:`SolverReport`."""
+def gcg_solve(a, b=None, config=None, *, x0=None):
+    """Run the block eigensolver on the B200; returns a :class:`SolverReport`.
+
+    ``a``/``b``: scipy sparse or dense host matrices, or a prepared DeviceProblem
+    (matrices already in HBM).  ``x0`` (optional, n x size_x, host array or device
+    tensor) replaces the seeded initial draw — for callers that generate the
+    seeded block once and reuse it (bench.py); the seeded refills are unchanged.
+    """
     cfg = config if config is not None else SolverConfig()
     dev = D.default_context()
     if isinstance(a, DeviceProblem):
@@ -279,7 +285,15 @@ def gcg_solve(a, b=None, config=None):
 
     v = dev.zeros(n, sx + 2 * bs)
     lam = np.zeros(sx + 2 * bs)
-    S.set_random(v[:, :sx], cfg.seed)
+    if x0 is None:
+        S.set_random(v[:, :sx], cfg.seed)
+    else:
+        if tuple(x0.shape) != (n, sx):
+            raise InvalidShape(f"x0 shape {tuple(x0.shape)} != ({n}, {sx})")
+        src = x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(np.asarray(x0))
+        if src.device != dev.device:
+            src = src.to(dev.device, non_blocking=True)
+        D.copy(dev, src.contiguous(), v[:, :sx])
     out = recursive_orth_svd(dev, v, 1, sx, b=Bop, cfg=ocfg)
     total_red = out.reduction_count
     if out.num_kept < sx:
