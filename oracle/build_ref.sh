@@ -20,6 +20,8 @@ rm -rf "$here/_ref"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
   --target "$here/_ref" "$tmp/pkg"
 rm -rf "$here/_ref/bin"
+# the reference's own test-suite, so the GPU box can run it against the sm100 backend
+cp -r "$src/tests" "$here/_ref/tests"
 python - <<PY
 import sys; sys.path.insert(0, "$here/_ref")
 import gcgeig

@@ -27,207 +27,6 @@ int64_t g_launches = 0;
 // ---------------------------------------------------------------------------
 // Gram
 
-template <int BM, int BN, int TM, int TN>
-__global__ void __launch_bounds__(256) gram_kernel(long long n, int k1, int k2,
-                                                   const double* __restrict__ X, long long ldx,
-                                                   const double* __restrict__ Y, long long ldy,
-                                                   long long rows_per_slab, double* part) {
-  constexpr int BK = 16;
-  constexpr int TX = BN / TN;  // threads along columns
-  constexpr int TY = BM / TM;
-  static_assert(TX * TY == 256, "256 threads");
-  __shared__ double Xs[BK][BM];
-  __shared__ double Ys[BK][BN];
-  const int tm0 = blockIdx.x * BM;
-  const int tn0 = blockIdx.y * BN;
-  const int slab = blockIdx.z;
-  const long long r0 = (long long)slab * rows_per_slab;
-  long long r1 = r0 + rows_per_slab;
-  if (r1 > n) r1 = n;
-  const int tx = threadIdx.x % TX;
-  const int ty = threadIdx.x / TX;
-  double acc[TM][TN];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
-
-  for (long long rb = r0; rb < r1; rb += BK) {
-    // cooperative loads (coalesced along the contiguous column direction)
-    for (int e = threadIdx.x; e < BK * BM; e += 256) {
-      const int rr = e / BM, cc = e % BM;
-      const long long row = rb + rr;
-      const int col = tm0 + cc;
-      Xs[rr][cc] = (row < r1 && col < k1) ? __ldg(X + row * ldx + col) : 0.0;
-    }
-    for (int e = threadIdx.x; e < BK * BN; e += 256) {
-      const int rr = e / BN, cc = e % BN;
-      const long long row = rb + rr;
-      const int col = tn0 + cc;
-      Ys[rr][cc] = (row < r1 && col < k2) ? __ldg(Y + row * ldy + col) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double xv[TM], yv[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) xv[i] = Xs[kk][ty + i * TY];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) yv[j] = Ys[kk][tx + j * TX];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fma(xv[i], yv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-  double* out = part + (long long)slab * k1 * k2;
-#pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const int r = tm0 + ty + i * TY;
-    if (r >= k1) continue;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int c = tn0 + tx + j * TX;
-      if (c < k2) out[(long long)r * k2 + c] = acc[i][j];
-    }
-  }
-}
-
-// G[r*grs + c*gcs] = alpha * sum_s part[s][r][c] + beta * G  (fixed slab order)
-__global__ void gram_finish_kernel(int k1, int k2, int nslab, const double* __restrict__ part,
-                                   double alpha, double beta, double* G, long long grs,
-                                   long long gcs) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)k1 * k2) return;
-  const int r = (int)(e / k2), c = (int)(e % k2);
-  double s = 0.0;
-  for (int q = 0; q < nslab; ++q) s += part[(long long)q * k1 * k2 + e];
-  double* g = G + r * grs + c * gcs;
-  *g = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * *g);
-}
-
-int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, const double* Y,
-                    long long ldy, double* out);
-
-int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
-                const double* Y, long long ldy, double alpha, double beta, double* G,
-                long long grs, long long gcs) {
-  if (k1 <= 0 || k2 <= 0) return GCG_OK;
-  const bool big = (k1 > 32 && k2 > 32);
-  const int BM = big ? 64 : 32, BN = big ? 64 : 32;
-  const int tiles = ((k1 + BM - 1) / BM) * ((k2 + BN - 1) / BN);
-  // enough slabs for ~4 CTAs per SM, but keep >= 256 rows per slab
-  long long nslab = (4LL * c->num_sms + tiles - 1) / tiles;
-  long long max_slab = (n + 255) / 256;
-  if (nslab > max_slab) nslab = max_slab;
-  if (nslab < 1) nslab = 1;
-  if (nslab > 65535) nslab = 65535;
-  long long rps = (n + nslab - 1) / nslab;
-  rps = (rps + 15) / 16 * 16;
-  nslab = (n + rps - 1) / rps;
-  if (nslab < 1) nslab = 1;
-  GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)nslab * k1 * k2));
-  double* part = (double*)c->partials.ptr;
-  dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, (unsigned)nslab);
-  const int ps = prof_start(c, PROF_GRAM, 8.0 * n * (X == Y ? k1 : k1 + k2));
-  if (big)
-    gram_kernel<64, 64, 4, 4><<<grid, 256, 0, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
-  else
-    gram_kernel<32, 32, 2, 2><<<grid, 256, 0, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
-  prof_stop(c, ps);
-  ++g_launches;
-  GCG_CHECK_LAUNCH();
-  const long long tot = (long long)k1 * k2;
-  gram_finish_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(
-      k1, k2, (int)nslab, part, alpha, beta, G, grs, gcs);
-  ++g_launches;
-  GCG_CHECK_LAUNCH();
-  return GCG_OK;
-}
-
-// ---------------------------------------------------------------------------
-// LinComb  Y = alpha X C + beta Y
-
-template <int BM, int BN, int TM, int TN>
-__global__ void __launch_bounds__(256) lincomb_kernel(long long n, int m, int d, double alpha,
-                                                      const double* __restrict__ X, long long ldx,
-                                                      const double* __restrict__ C, long long ldc,
-                                                      double beta, double* Y, long long ldy) {
-  constexpr int BK = 16;
-  constexpr int TX = BN / TN;
-  constexpr int TY = BM / TM;
-  static_assert(TX * TY == 256, "256 threads");
-  __shared__ double Xs[BK][BM + 1];
-  __shared__ double Cs[BK][BN];
-  const long long r0 = (long long)blockIdx.x * BM;
-  const int c0 = blockIdx.y * BN;
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  double acc[TM][TN];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
-  for (int kb = 0; kb < m; kb += BK) {
-    for (int e = threadIdx.x; e < BM * BK; e += 256) {
-      const int rr = e / BK, kk = e % BK;
-      const long long row = r0 + rr;
-      Xs[kk][rr] = (row < n && kb + kk < m) ? __ldg(X + row * ldx + kb + kk) : 0.0;
-    }
-    for (int e = threadIdx.x; e < BK * BN; e += 256) {
-      const int kk = e / BN, cc = e % BN;
-      Cs[kk][cc] = (kb + kk < m && c0 + cc < d) ? __ldg(C + (long long)(kb + kk) * ldc + c0 + cc)
-                                                : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double xv[TM], cv[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) xv[i] = Xs[kk][ty + i * TY];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) cv[j] = Cs[kk][tx + j * TX];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fma(xv[i], cv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const long long row = r0 + ty + i * TY;
-    if (row >= n) continue;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int col = c0 + tx + j * TX;
-      if (col >= d) continue;
-      double* y = Y + row * ldy + col;
-      *y = (beta == 0.0) ? alpha * acc[i][j] : fma(alpha, acc[i][j], beta * *y);
-    }
-  }
-}
-
-int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
-                   long long ldx, const double* C, long long ldc, double beta, double* Y,
-                   long long ldy) {
-  if (n <= 0 || d <= 0) return GCG_OK;
-  const int ps = prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
-  if (d <= 32) {
-    dim3 grid((unsigned)((n + 127) / 128), (d + 31) / 32);
-    lincomb_kernel<128, 32, 4, 4><<<grid, 256, 0, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc,
-                                                                beta, Y, ldy);
-  } else {
-    dim3 grid((unsigned)((n + 63) / 64), (d + 63) / 64);
-    lincomb_kernel<64, 64, 4, 4><<<grid, 256, 0, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc,
-                                                               beta, Y, ldy);
-  }
-  prof_stop(c, ps);
-  ++g_launches;
-  GCG_CHECK_LAUNCH();
-  return GCG_OK;
-}
-
 // ---------------------------------------------------------------------------
 // elementwise multivector kernels: one thread per element, grid-stride
 

@@ -43,47 +43,79 @@ struct CgState {
   int* pup;
   int* skip;
   int* sweeps;
+  int* nact;
+  int* ticket;
 };
 
-__device__ __forceinline__ double sum_parts(const double* part, int nparts, int k, int c) {
-  double s = 0.0;
-  for (int b = 0; b < nparts; ++b) s += part[(long long)b * k + c];
-  return s;
+// Fixed-order reduction of one column's per-CTA partials by a 128-thread block:
+// thread t sums partials t, t+128, ... then a fixed tree — deterministic.
+__device__ double block_sum_parts(const double* part, int nparts, int k, int c, double* sm) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) v += part[(long long)b * k + c];
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double t = sm[0];
+  __syncthreads();
+  return t;
 }
 
-__global__ void cg_init_fin(int k, const double* part, int nparts, double rel_tol, CgState s) {
-  __shared__ int nact;
-  if (threadIdx.x == 0) nact = 0;
+// Last-block epilogue: block-level counts are combined with an atomic ticket;
+// the block that arrives last publishes the skip flag and resets the counters.
+__device__ void publish_active(const CgState& s, int k, int my_active, bool reset_sweeps) {
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    if (my_active) atomicAdd(s.nact, 1);
+    __threadfence();
+    last = (atomicAdd(s.ticket, 1) == k - 1);
+  }
   __syncthreads();
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    const double rr = sum_parts(part, nparts, k, c);
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const int na = atomicAdd(s.nact, 0);
+    if (na == 0) *s.skip = 1;
+    if (reset_sweeps) *s.sweeps = 0;
+    *s.nact = 0;
+    *s.ticket = 0;
+  }
+}
+
+// one block per column: ||r0||, target, initial flags
+__global__ void cg_init_fin(int k, const double* part, int nparts, double rel_tol, CgState s) {
+  __shared__ double sm[128];
+  const int c = blockIdx.x;
+  const double rr = block_sum_parts(part, nparts, k, c, sm);
+  int cv = 0;
+  if (threadIdx.x == 0) {
     const double r0 = sqrt(rr);
     s.rn0[c] = r0;
     s.rn[c] = r0;
     s.target[c] = rel_tol * r0;
-    const int cv = r0 <= rel_tol * r0;
+    cv = r0 <= rel_tol * r0;
     s.conv[c] = cv;
     s.frozen[c] = 0;
     s.rz[c] = rr;
     s.upd[c] = 0;
     s.pup[c] = 0;
-    if (!cv) atomicAdd(&nact, 1);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *s.skip = (nact == 0);
-    *s.sweeps = 0;
-  }
+  if (c == 0 && threadIdx.x == 0) *s.skip = 0;
+  // skip is only raised by the last block, after every block passed this point
+  publish_active(s, k, !cv, true);
 }
 
 // den = p'q per active column; freeze on den <= 0, else alpha = rz / den.
 __global__ void cg_fin1(int k, const double* part, int nparts, CgState s) {
   if (*s.skip) return;
-  if (threadIdx.x == 0) *s.sweeps += 1;
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+  __shared__ double sm[128];
+  const int c = blockIdx.x;
+  const double den = block_sum_parts(part, nparts, k, c, sm);
+  if (threadIdx.x == 0) {
+    if (c == 0) *s.sweeps += 1;
     int u = 0;
     if (!s.conv[c] && !s.frozen[c]) {
-      const double den = sum_parts(part, nparts, k, c);
       if (den <= 0.0) {
         s.frozen[c] = 1;
       } else {
@@ -95,17 +127,17 @@ __global__ void cg_fin1(int k, const double* part, int nparts, CgState s) {
   }
 }
 
-// rn = ||r||; converge, else beta = rz_new / rz.  Sets the skip flag when no
+// rn = ||r||; converge, else beta = rz_new / rz.  Raises the skip flag when no
 // column remains active (the reference's loop exit, cg.py:67-69).
 __global__ void cg_fin2(int k, const double* part, int nparts, CgState s) {
   if (*s.skip) return;
-  __shared__ int nact;
-  if (threadIdx.x == 0) nact = 0;
-  __syncthreads();
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+  __shared__ double sm[128];
+  const int c = blockIdx.x;
+  const double rr = block_sum_parts(part, nparts, k, c, sm);
+  int active = 0;
+  if (threadIdx.x == 0) {
     int p = 0;
     if (s.upd[c]) {
-      const double rr = sum_parts(part, nparts, k, c);
       const double rn = sqrt(rr);
       s.rn[c] = rn;
       if (rn <= s.target[c]) {
@@ -117,10 +149,9 @@ __global__ void cg_fin2(int k, const double* part, int nparts, CgState s) {
       }
     }
     s.pup[c] = p;
-    if (!s.conv[c] && !s.frozen[c]) atomicAdd(&nact, 1);
+    active = !s.conv[c] && !s.frozen[c];
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && nact == 0) *s.skip = 1;
+  publish_active(s, k, active, false);
 }
 
 // x += alpha p ; r -= alpha q ; partial ||r||^2 (updated columns only)
@@ -147,11 +178,32 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
     const int u = s.upd[c];
     const double al = s.alpha[c];
     if (u) {
-      for (long long i = r0 + rl; i < r1; i += lanes) {
+      constexpr int U = 4;  // rows in flight per thread
+      long long i = r0 + rl;
+      for (; i + (U - 1) * lanes < r1; i += U * lanes) {
+        double xv[U], pv[U], qv[U], rv[U];
+#pragma unroll
+        for (int q4 = 0; q4 < U; ++q4) {
+          const long long ii = i + q4 * lanes;
+          xv[q4] = x[ii * ldx + c];
+          pv[q4] = p[ii * k + c];
+          qv[q4] = q[ii * k + c];
+          rv[q4] = r[ii * k + c];
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < U; ++q4) {
+          const long long ii = i + q4 * lanes;
+          x[ii * ldx + c] = fma(al, pv[q4], xv[q4]);
+          const double nr = fma(-al, qv[q4], rv[q4]);
+          r[ii * k + c] = nr;
+          acc = fma(nr, nr, acc);
+        }
+      }
+      for (; i < r1; i += lanes) {
         x[i * ldx + c] = fma(al, p[i * k + c], x[i * ldx + c]);
-        const double rv = fma(-al, q[i * k + c], r[i * k + c]);
-        r[i * k + c] = rv;
-        acc = fma(rv, rv, acc);
+        const double nr = fma(-al, q[i * k + c], r[i * k + c]);
+        r[i * k + c] = nr;
+        acc = fma(nr, nr, acc);
       }
     }
   }
@@ -203,7 +255,7 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
   // workspace: R, P, Q (n x k) + partials + state
   const size_t vec = (size_t)n * k;
   const size_t bytes = sizeof(double) * (3 * vec + (size_t)nparts_max * k + 6 * (size_t)k) +
-                       sizeof(int) * (4 * (size_t)k + 2) + 256;
+                       sizeof(int) * (4 * (size_t)k + 4) + 256;
   GCG_TRY(ensure(c->cg, bytes));
   double* R = (double*)c->cg.ptr;
   double* P = R + vec;
@@ -224,13 +276,16 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
   s.pup = si + 3 * k;
   s.skip = si + 4 * k;
   s.sweeps = si + 4 * k + 1;
+  s.nact = si + 4 * k + 2;
+  s.ticket = si + 4 * k + 3;
+  GCG_TRY(cuda_status(cudaMemsetAsync(s.skip, 0, 4 * sizeof(int), c->stream)));
   const int fin_threads = k < 32 ? 32 : (k + 31) / 32 * 32;
 
   // r = rhs - op(x) = -(A x) - shift*x + rhs ; ||r0||^2 partials
   int g = 0;
   GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0, rhs,
                             ldr, R, k, 2, nullptr, 0, part, &g, nullptr));
-  cg_init_fin<<<1, fin_threads, 0, c->stream>>>(k, part, g, rel_tol, s);
+  cg_init_fin<<<k, 128, 0, c->stream>>>(k, part, g, rel_tol, s);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   GCG_TRY(copy_launch(c, n, k, R, k, P, k));
@@ -238,12 +293,12 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
   for (int it = 0; it < max_iters; ++it) {
     GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0, nullptr,
                               0, Q, k, 1, P, k, part, &g, s.skip));
-    cg_fin1<<<1, fin_threads, 0, c->stream>>>(k, part, g, s);
+    cg_fin1<<<k, 128, 0, c->stream>>>(k, part, g, s);
     int ps = prof_start(c, PROF_CG_UPDATE, 48.0 * n * k);
     cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, Q, rpc, part, s,
                                                    prof_skip_slot(c, ps));
     prof_stop(c, ps);
-    cg_fin2<<<1, fin_threads, 0, c->stream>>>(k, part, ugrid, s);
+    cg_fin2<<<k, 128, 0, c->stream>>>(k, part, ugrid, s);
     ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
     cg_pupdate_kernel<<<pgrid, 256, 0, c->stream>>>(n, k, R, P, s, prof_skip_slot(c, ps));
     prof_stop(c, ps);
