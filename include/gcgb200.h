@@ -143,7 +143,9 @@ int gcg_symmetrize(void* ctx, int64_t m, double* A, int64_t lda);
  *   status[0] = max|G - I|, status[1] = #eigenvalues <= dep_tol*max(lambda_max,0),
  *   status[2] = lambda_max; Q (w x (w - nbad)) = V[:, nbad:] / sqrt(lambda[nbad:]). */
 int gcg_svqb_prepare(void* ctx, int64_t w, const double* G, int64_t ldg, double dep_tol,
-                     double* Q, int64_t ldq, double* status);
+                     double skip_tol, double* Q, int64_t ldq, double* status);
+/* (skip_tol: when max|G - I| <= skip_tol the caller is done — orth.py:170-171 — and
+ *  only status[0] is written; pass a negative value to always factorise) */
 /* Deflation repeat test (orth.py:146-152): R is K x w coefficients, dnew[w] squared norms.
  *   status[0] = max|R|, status[1] = any(sum_r R[r,c]^2 > dgks * max(dnew[c], 1e-300)). */
 int gcg_deflate_status(void* ctx, int64_t K, int64_t w, const double* R, int64_t ldr,

@@ -46,7 +46,7 @@ _SIGS = {
     "gcg_dgemm": [_ptr, _int, _int, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr,
                   _i64],
     "gcg_symmetrize": [_ptr, _i64, _ptr, _i64],
-    "gcg_svqb_prepare": [_ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64, _ptr],
+    "gcg_svqb_prepare": [_ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _ptr],
     "gcg_deflate_status": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _ptr],
     "gcg_abar_assemble": [_ptr, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64, _ptr, _i64],
     "gcg_max_abs_diff": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr],

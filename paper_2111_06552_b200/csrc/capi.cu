@@ -46,7 +46,8 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
                     double shift, int k, const double* rhs, long long ldr, double* x,
                     long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
                     int8_t* d_frozen, double* d_relres);
-int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
+                        double skip_tol, double* Q,
                         long long ldq, double* status);
 int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
                           const double* dnew, long long dstride, double dgks, double* status);
@@ -190,6 +191,8 @@ int gcg_ctx_create(void** out, void* stream) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess &&
       sms > 0)
     c->num_sms = sms;
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device) == cudaSuccess) c->l2_bytes = l2;
   if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) {
     delete c;
     return GCG_ERR_SOLVER;
@@ -388,10 +391,10 @@ int gcg_symmetrize(void* p, int64_t m, double* A, int64_t lda) {
 }
 
 int gcg_svqb_prepare(void* p, int64_t w, const double* G, int64_t ldg, double dep_tol,
-                     double* Q, int64_t ldq, double* status) {
+                     double skip_tol, double* Q, int64_t ldq, double* status) {
   Ctx* c = CTX(p);
   if (!c || w <= 0 || ldg < w || ldq < w || !status) return GCG_ERR_ARG;
-  return svqb_prepare_launch(c, (int)w, G, ldg, dep_tol, Q, ldq, status);
+  return svqb_prepare_launch(c, (int)w, G, ldg, dep_tol, skip_tol, Q, ldq, status);
 }
 
 int gcg_deflate_status(void* p, int64_t K, int64_t w, const double* R, int64_t ldr,

@@ -15,6 +15,8 @@
 // by the caller.  Per sweep HBM traffic ~ SpMM + 48nk (x,r,p,q update) + 24nk
 // (p = r + beta p).
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace gcg {
@@ -239,14 +241,42 @@ __global__ void cg_final(int k, CgState s, int* d_sweeps, int8_t* conv, int8_t* 
     conv[c] = (int8_t)s.conv[c];
     frozen[c] = (int8_t)s.frozen[c];
   }
-  if (threadIdx.x == 0) *d_sweeps = *s.sweeps;
+  if (threadIdx.x == 0) atomicMax(d_sweeps, *s.sweeps);  // max over column chunks
 }
 
-int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx, const double* val,
-                    double shift, int k, const double* rhs, long long ldr, double* x,
-                    long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
-                    int8_t* d_frozen, double* d_relres) {
+int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
+                   const double* val, double shift, int k, const double* rhs, long long ldr,
+                   double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
+                   int8_t* d_conv, int8_t* d_frozen, double* d_relres);
+
+// The k CG recurrences are independent, so they can run in column chunks (each
+// chunk's sweep count is the same as in the joint run).  GCG_CG_CHUNK=w forces
+// chunks of w columns — e.g. to keep a chunk's x, r, p, q and the CSR streams
+// resident in the 126 MB L2.  Measured at cfg2 (k = 20) that is slower (the
+// sweep is latency-bound, and chunking multiplies launches), so the default
+// is one chunk.
+int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
+                    const double* val, double shift, int k, const double* rhs, long long ldr,
+                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
+                    int8_t* d_conv, int8_t* d_frozen, double* d_relres) {
   if (k <= 0 || k > 256 || n <= 0) return GCG_ERR_ARG;
+  GCG_TRY(cuda_status(cudaMemsetAsync(d_sweeps, 0, sizeof(int), c->stream)));
+  static const char* env = getenv("GCG_CG_CHUNK");
+  int kc = env ? atoi(env) : k;
+  if (kc < 1 || kc > k) kc = k;
+  for (int c0 = 0; c0 < k; c0 += kc) {
+    const int w = (k - c0) < kc ? (k - c0) : kc;
+    GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr, x + c0, ldx,
+                           max_iters, rel_tol, d_sweeps, d_conv + c0, d_frozen + c0,
+                           d_relres + c0));
+  }
+  return GCG_OK;
+}
+
+int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
+                   const double* val, double shift, int k, const double* rhs, long long ldr,
+                   double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
+                   int8_t* d_conv, int8_t* d_frozen, double* d_relres) {
   const int sgrid = spmm_grid(c, n);
   int ugrid = grid_for(n, 512, 4, c->num_sms);
   long long rpc = (n + ugrid - 1) / ugrid;

@@ -45,6 +45,7 @@ struct Ctx {
   cusolverDnHandle_t solver = nullptr;
   int num_sms = kNumSMs;
   int device = 0;
+  long long l2_bytes = 0;
   // generic workspaces (slots are owned by one op at a time; ops on one ctx
   // are stream-ordered so reuse across ops is safe)
   Scratch partials;   // per-CTA partial sums for deterministic reductions

@@ -17,6 +17,7 @@
 // the context stream followed by an on-device transpose + sign fix.
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -54,7 +55,9 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
       tdia += red[2 * w + 1];
     }
     __syncthreads();
-    if (toff <= 1e-30 * tdia || toff == 0.0) break;
+    // relative off-diagonal norm <= 1e-14: eigenvalues/vectors at rounding level
+    // (a tighter test can stall on the rounding floor of the parallel rotations)
+    if (toff <= 1e-28 * tdia || toff == 0.0) break;
     for (int round = 0; round < mp - 1; ++round) {
       if (tid < half) {
         int p, q;
@@ -72,8 +75,9 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
         }
         const double apq = a[p][q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double app = a[p][p], aqq = a[q][q];
+        const double app = a[p][p], aqq = a[q][q];
+        // skip rotations whose off-diagonal entry is negligible against the diagonal
+        if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq)) && apq != 0.0) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -83,6 +87,10 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
         sn[tid] = s;
         pp[tid] = p;
         qq[tid] = q;
+        // exact post-rotation diagonal (Rutishauser); a_pq itself becomes exactly 0
+        const double tt = (c != 1.0 || s != 0.0) ? s / c : 0.0;
+        red[64 + 2 * tid] = app - tt * apq;
+        red[64 + 2 * tid + 1] = aqq + tt * apq;
       }
       __syncthreads();
       // rows: A <- J^T A
@@ -101,8 +109,18 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
         const int p = pp[pr], q = qq[pr];
         const double c = cs[pr], s = sn[pr];
         const double ap = a[i][p], aq = a[i][q];
-        a[i][p] = c * ap - s * aq;
-        a[i][q] = s * ap + c * aq;
+        if (s == 0.0 && c == 1.0) {
+          // no rotation for this pair: entries unchanged
+        } else if (i == p) {
+          a[p][p] = red[64 + 2 * pr];
+          a[p][q] = 0.0;
+        } else if (i == q) {
+          a[q][p] = 0.0;
+          a[q][q] = red[64 + 2 * pr + 1];
+        } else {
+          a[i][p] = c * ap - s * aq;
+          a[i][q] = s * ap + c * aq;
+        }
         const double vp = v[i][p], vq = v[i][q];
         v[i][p] = c * vp - s * vq;
         v[i][q] = s * vp + c * vq;
@@ -152,7 +170,7 @@ struct JacSmem {
   double cs[kJacMax / 2], sn[kJacMax / 2];
   int pp[kJacMax / 2], qq[kJacMax / 2];
   int rank[kJacMax];
-  double red[64];
+  double red[128];  // [0,64): block reductions; [64,128): exact post-rotation diagonals
   double w[kJacMax];
   double Vs[kJacMax * kJacMax];
 };
@@ -190,6 +208,7 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
     cudaFuncSetAttribute(syev_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
+
   syev_jacobi_kernel<<<1, 256, sm, c->stream>>>(m, A, lda, w, V, ldv);
   ++g_launches;
   GCG_CHECK_LAUNCH();
@@ -201,7 +220,8 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
 // its symmetric part, dependence count and the coefficient matrix
 // Q = V[:, nbad:] / sqrt(lambda[nbad:]).
 __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* G, long long ldg,
-                                                           double dep_tol, double* Q,
+                                                           double dep_tol, double skip_tol,
+                                                           double* Q,
                                                            long long ldq, double* status) {
   extern __shared__ __align__(16) unsigned char smraw[];
   JacSmem& S = *reinterpret_cast<JacSmem*>(smraw);
@@ -219,8 +239,12 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
     double t = 0.0;
     for (int w = 0; w < (int)blockDim.x / 32; ++w) t = fmax(t, S.red[w]);
     status[0] = t;
+    S.red[127] = t;
   }
   __syncthreads();
+  // the caller stops when the Gram is already the identity to reorth_tol
+  // (orth.py:170-171): skip the factorisation then
+  if (S.red[127] <= skip_tol) return;
   jac_load(S, m, mp, G, ldg, true);
   jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
   sort_and_sign(m, S.a, S.v, S.w, S.Vs, m, S.rank);
@@ -243,7 +267,8 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
   }
 }
 
-int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
+                       double skip_tol, double* Q,
                        long long ldq, double* status) {
   const size_t sm = sizeof(JacSmem);
   static bool attr = false;
@@ -252,7 +277,8 @@ int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep
                          (int)sm);
     attr = true;
   }
-  svqb_prepare_kernel<<<1, 256, sm, c->stream>>>(m, G, ldg, dep_tol, Q, ldq, status);
+  svqb_prepare_kernel<<<1, 256, sm, c->stream>>>(m, G, ldg, dep_tol, skip_tol, Q, ldq,
+                                                                 status);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -332,6 +358,19 @@ int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int s
   if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
                                   B, m, w, &lwork) != CUSOLVER_STATUS_SUCCESS)
     return GCG_ERR_SOLVER;
+  // GCG_SYEV=syevj selects cuSOLVER's Jacobi driver (A/B experiment); default syevd
+  static const char* impl = getenv("GCG_SYEV");
+  const bool jac = impl && impl[0] == 's' && impl[4] == 'j';
+  static syevjInfo_t jparams = nullptr;
+  if (jac && !jparams) {
+    cusolverDnCreateSyevjInfo(&jparams);
+    cusolverDnXsyevjSetTolerance(jparams, 1e-15);
+    cusolverDnXsyevjSetMaxSweeps(jparams, 30);
+  }
+  if (jac && cusolverDnDsyevj_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                         CUBLAS_FILL_MODE_LOWER, m, B, m, w, &lwork,
+                                         jparams) != CUSOLVER_STATUS_SUCCESS)
+    return GCG_ERR_SOLVER;
   GCG_TRY(ensure(c->eigwork, sizeof(double) * ((size_t)lwork + 8)));
   double* work = (double*)c->eigwork.ptr;
   int* info = (int*)(work + lwork);
@@ -339,9 +378,12 @@ int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int s
                                                                         nullptr);
   ++g_launches;
   GCG_CHECK_LAUNCH();
-  if (cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m, w,
-                       work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
-    return GCG_ERR_SOLVER;
+  const cusolverStatus_t st =
+      jac ? cusolverDnDsyevj(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m,
+                             w, work, lwork, info, jparams)
+          : cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m,
+                             w, work, lwork, info);
+  if (st != CUSOLVER_STATUS_SUCCESS) return GCG_ERR_SOLVER;
   // row-major symmetric input == its column-major transpose, so B now holds
   // eigenvector j in column-major column j
   vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, B, V, ldv);
@@ -413,9 +455,10 @@ int scale_rsqrt_launch(Ctx* c, int m, int off, const double* V, long long ldv, c
   return GCG_OK;
 }
 
-int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol, double* Q,
+int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
+                        double skip_tol, double* Q,
                         long long ldq, double* status) {
-  if (m <= kJacMax) return svqb_prepare_small(c, m, G, ldg, dep_tol, Q, ldq, status);
+  if (m <= kJacMax) return svqb_prepare_small(c, m, G, ldg, dep_tol, skip_tol, Q, ldq, status);
   // large leaf: defect, cuSOLVER on the symmetric part, count, scale
   max_offeye_kernel<<<1, 256, 0, c->stream>>>(m, G, ldg, status);
   ++g_launches;

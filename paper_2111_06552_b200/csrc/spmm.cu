@@ -5,11 +5,19 @@
 // (operators.py:149-156: A x - theta (B x or x)).
 //
 // B200 design.  X is row-major, so the k values a nonzero (i, j) needs are one
-// contiguous run X[j*ldx : j*ldx+k]: a group of LPR lanes owns one row and
-// reads those runs with 16-byte vector loads (coalesced, L2-resident for the
-// stencil's plane-distance reuse).  The row's (column index, value) stream is
-// loaded once, cooperatively, one nonzero per lane, and broadcast inside the
-// group with shuffles — 12 B/nnz from HBM instead of k separate index loads.
+// contiguous run X[j*ldx : j*ldx+k].  A group of LPR lanes owns one row and
+// reads those runs with 16-byte vector loads (NV column chunks per lane); a
+// warp holds 32/LPR rows.  The row's (column index, value) stream is loaded
+// once, cooperatively (one nonzero per lane, 12 B/nnz from HBM), and broadcast
+// inside the group with shuffles.
+//
+// At the BASELINE shapes the kernel is latency-bound (a row is a 3-deep chain:
+// row pointer -> index/value -> X gathers), so it is software-pipelined: while
+// a warp gathers X for its current rows it already holds the row pointers and
+// the index/value chunk of its NEXT rows in registers, leaving only the X
+// gathers on the critical path; all gathers of a row batch (up to 8 nonzeros)
+// are issued before the first FMA.
+//
 // The epilogue fuses the shifted-operator term (gamma*Z, Z = X for A - theta*I),
 // an axpby with a second input (beta*Yin, used for r = rhs - op x) and an
 // optional per-column dot product reduced deterministically (p'q and ||r||^2
@@ -23,6 +31,8 @@
 #include "common.cuh"
 
 namespace gcg {
+
+extern int64_t g_launches;
 
 struct SpmmArgs {
   long long n;
@@ -42,99 +52,133 @@ struct SpmmArgs {
   int dot_mode;
   const double* __restrict__ W;
   long long ldw;
-  double* partials;  // [gridDim.x][k]
-  const int* skip;   // device flag: nonzero -> kernel is a no-op (CG early exit)
-  int* prof_skipped; // profiling: set when the launch was a no-op
-  long long nnz;     // total nonzeros (clips the bulk copies of the last tile)
-  int cap;           // nonzeros per shared-memory stage (tiled kernel)
+  double* partials;   // [gridDim.x][k]
+  const int* skip;    // device flag: nonzero -> kernel is a no-op (CG early exit)
+  int* prof_skipped;  // profiling: set when the launch was a no-op
 };
 
 template <int VEC>
 struct VecT;
 template <>
 struct VecT<1> {
-  using T = double;
   static __device__ __forceinline__ void load(const double* p, double* o) { o[0] = __ldg(p); }
 };
 template <>
 struct VecT<2> {
   static __device__ __forceinline__ void load(const double* p, double* o) {
-    double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
     o[0] = v.x;
     o[1] = v.y;
   }
 };
 
 constexpr int kSpmmThreads = 256;
+constexpr int kSpmmMinBlocks = 4;  // <= 64 registers: 32 resident warps per SM
 
 template <int LPR, int VEC, int NV>
-__global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(SpmmArgs a) {
+__global__ void __launch_bounds__(kSpmmThreads, kSpmmMinBlocks) spmm_csr_kernel(SpmmArgs a) {
   if (a.skip != nullptr && *a.skip) {
     if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
     return;
   }
-  constexpr int G = 32 / LPR;  // row groups per warp
+  constexpr int G = 32 / LPR;  // rows per warp step
   constexpr int COLS = LPR * VEC * NV;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int g = lane / LPR;
-  const int sub = lane % LPR;
-  const int nwarps = kSpmmThreads / 32;
-  const long long stride = (long long)gridDim.x * nwarps * G;
+  // gathers in flight per batch: <= 16 doubles of X per lane, a power of 2 dividing LPR
+  constexpr int UB = 16 / (NV * VEC);
+  constexpr int U0 = UB >= 8 ? 8 : (UB >= 4 ? 4 : 2);
+  constexpr int U = U0 < LPR ? U0 : LPR;
+  constexpr int NW = kSpmmThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / LPR, sub = lane % LPR;
+  const long long stride = (long long)gridDim.x * NW * G;
   const int k = a.k;
 
-  __shared__ double sdot[kSpmmThreads / 32][COLS];
+  __shared__ double sdot[NW][COLS];
   double dacc[NV][VEC];
 #pragma unroll
   for (int q = 0; q < NV; ++q)
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) dacc[q][v] = 0.0;
+    for (int e = 0; e < VEC; ++e) dacc[q][e] = 0.0;
 
-  // This kernel handles one column pass [c0, c0 + COLS); wider blocks are
-  // split by the launcher into several launches with offset pointers.
-  for (long long rb = ((long long)blockIdx.x * nwarps + warp) * G; rb < a.n; rb += stride) {
-    const long long r = rb + g;
-    const bool valid = r < a.n;
-    int start = 0, len = 0;
-    if (valid) {
-      start = __ldg(a.rowptr + r);
-      len = __ldg(a.rowptr + r + 1) - start;
+  // prefetched state of the row this lane group handles next
+  long long rb = ((long long)blockIdx.x * NW + warp) * G;
+  int nstart = 0, nlen = 0, ncol = 0;
+  double nval = 0.0;
+  auto fetch_rowptr = [&](long long base, int& st, int& ln) {
+    const long long r = base + g;
+    st = 0;
+    ln = 0;
+    if (r < a.n) {
+      st = __ldg(a.rowptr + r);
+      ln = __ldg(a.rowptr + r + 1) - st;
     }
+  };
+  auto fetch_chunk = [&](int st, int ln, int off, int& cidx, double& cval) {
+    cidx = 0;
+    cval = 0.0;
+    if (off + sub < ln) {
+      cidx = __ldg(a.colidx + st + off + sub);
+      cval = __ldg(a.val + st + off + sub);
+    }
+  };
+  if (rb < a.n) {
+    fetch_rowptr(rb, nstart, nlen);
+    fetch_chunk(nstart, nlen, 0, ncol, nval);
+  }
+
+  for (; rb < a.n; rb += stride) {
+    const long long r = rb + g;
+    const int start = nstart, len = nlen;
+    int mycol = ncol;
+    double myval = nval;
+    const long long rbn = rb + stride;
+    if (rbn < a.n) fetch_rowptr(rbn, nstart, nlen);  // lands during the gathers below
     const int maxlen = __reduce_max_sync(0xffffffffu, len);
     double acc[NV][VEC];
 #pragma unroll
     for (int q = 0; q < NV; ++q)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[q][v] = 0.0;
+      for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
 
     for (int off = 0; off < maxlen; off += LPR) {
-      int mycol = 0;
-      double myval = 0.0;
-      if (off + sub < len) {
-        mycol = __ldg(a.colidx + start + off + sub);
-        myval = __ldg(a.val + start + off + sub);
-      }
+      if (off > 0) fetch_chunk(start, len, off, mycol, myval);  // rows longer than LPR
       const int tmax = min(LPR, maxlen - off);
-#pragma unroll 4
-      for (int t = 0; t < tmax; ++t) {
-        const int j = __shfl_sync(0xffffffffu, mycol, t, LPR);
-        const double v = __shfl_sync(0xffffffffu, myval, t, LPR);
-        if (off + t < len) {
-          const double* xr = a.X + (long long)j * a.ldx;
+      for (int t0 = 0; t0 < tmax; t0 += U) {
+        int j[U];
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          j[u] = __shfl_sync(0xffffffffu, mycol, t0 + u, LPR);
+          v[u] = __shfl_sync(0xffffffffu, myval, t0 + u, LPR);
+          if (t0 + u >= tmax || off + t0 + u >= len) v[u] = 0.0;
+        }
+        double xv[U][NV][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = (t0 + u < tmax) && (off + t0 + u < len);
+          const double* xr = a.X + (long long)j[u] * a.ldx;
 #pragma unroll
           for (int q = 0; q < NV; ++q) {
             const int c = (q * LPR + sub) * VEC;
-            if (c < k) {
-              double xv[VEC];
-              VecT<VEC>::load(xr + c, xv);
+            if (ok && c < k) {
+              VecT<VEC>::load(xr + c, xv[u][q]);
+            } else {
 #pragma unroll
-              for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v, xv[e], acc[q][e]);
+              for (int e = 0; e < VEC; ++e) xv[u][q][e] = 0.0;
             }
           }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NV; ++q)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
       }
     }
-    if (valid) {
+    // first index/value chunk of the next rows (their row pointers have arrived)
+    if (rbn < a.n) fetch_chunk(nstart, nlen, 0, ncol, nval);
+    if (r < a.n) {
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         const int c = (q * LPR + sub) * VEC;
@@ -154,7 +198,7 @@ __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(SpmmArgs a) {
   }
 
   if (a.dot_mode == 0) return;
-  // reduce over the row groups of the warp (lanes with equal `sub`)
+  // reduce over the row groups of the warp (lanes with equal `sub`), then warps
 #pragma unroll
   for (int q = 0; q < NV; ++q)
 #pragma unroll
@@ -173,7 +217,7 @@ __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(SpmmArgs a) {
   __syncthreads();
   for (int c = threadIdx.x; c < k && c < COLS; c += kSpmmThreads) {
     double s = 0.0;
-    for (int w = 0; w < nwarps; ++w) s += sdot[w][c];
+    for (int w = 0; w < NW; ++w) s += sdot[w][c];
     a.partials[(long long)blockIdx.x * k + c] = s;
   }
 }
@@ -184,8 +228,7 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partials, int 
   const int c = blockIdx.x;
   double s = 0.0;
   for (int b = threadIdx.x; b < nparts; b += blockDim.x) s += partials[(long long)b * k + c];
-  // fixed-shape tree over the 128 threads
-  __shared__ double sm[128];
+  __shared__ double sm[128];  // fixed-shape tree over the 128 threads
   sm[threadIdx.x] = s;
   __syncthreads();
   for (int w = 64; w > 0; w >>= 1) {
@@ -205,254 +248,6 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
   reduce_partials_kernel<<<k, 128, 0, c->stream>>>(partials, nparts, k, out, out_stride, mode);
   GCG_CHECK_LAUNCH();
   return GCG_OK;
-}
-
-extern int64_t g_launches;
-
-// ---------------------------------------------------------------------------
-// Tiled SpMM: persistent CTAs walk tiles of kTileRows rows.  The tile's
-// (column index, value) streams are one contiguous nonzero range, so it is
-// brought into shared memory with two 1-D TMA bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx) one tile AHEAD of the compute: the
-// HBM index/value stream never sits in the dependent load chain of a row.
-// Rows then read their (col, val) pairs as shared-memory broadcasts and issue
-// all X-row gathers of an unrolled group at once.
-
-constexpr int kTileRows = 128;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, int bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, int phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, int bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-struct TileStage {
-  int rp[kTileRows + 1];  // row pointers of the tile (absolute)
-  int c0;                 // first nonzero held in smem (index alignment base)
-  int v0;                 // value alignment base
-  int cend, vend;         // smem holds [c0, cend) / [v0, vend); the rest is read from global
-};
-
-template <int LPR, int VEC, int NV>
-__global__ void __launch_bounds__(kSpmmThreads) spmm_tiled_kernel(SpmmArgs a) {
-  if (a.skip != nullptr && *a.skip) {
-    if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
-    return;
-  }
-  constexpr int G = 32 / LPR;
-  constexpr int COLS = LPR * VEC * NV;
-  constexpr int NW = kSpmmThreads / 32;
-  constexpr int U = 4;  // nonzeros per unrolled gather group
-  extern __shared__ __align__(16) unsigned char sm_raw[];
-  __shared__ TileStage st[2];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double sdot[NW][COLS];
-  const int cap = a.cap;
-  // stage s: values at sval0 + s*(cap+2), indices at scol0 + s*(cap+4)
-  double* const sval0 = reinterpret_cast<double*>(sm_raw);
-  int* const scol0 = reinterpret_cast<int*>(sval0 + 2 * (cap + 2));
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane / LPR, sub = lane % LPR;
-  const int k = a.k;
-  const long long ntiles = (a.n + kTileRows - 1) / kTileRows;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  double dacc[NV][VEC];
-#pragma unroll
-  for (int q = 0; q < NV; ++q)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) dacc[q][e] = 0.0;
-
-  // stage the row pointers of tile t into st[s] (all threads), then thread 0
-  // issues the bulk copies of its index/value ranges
-  auto stage_rp = [&](long long t, int s) {
-    const long long r0 = t * kTileRows;
-    const int nr = (int)min((long long)kTileRows, a.n - r0);
-    for (int i = threadIdx.x; i <= nr; i += kSpmmThreads) st[s].rp[i] = __ldg(a.rowptr + r0 + i);
-  };
-  auto bulk = [&](long long t, int s) {
-    const long long r0 = t * kTileRows;
-    const int nr = (int)min((long long)kTileRows, a.n - r0);
-    const int beg = st[s].rp[0], end = st[s].rp[nr];
-    int c0 = beg & ~3, c1 = (end + 3) & ~3;
-    const int cmax = (int)(a.nnz & ~3LL);
-    if (c1 > cmax) c1 = cmax > c0 ? cmax : c0;
-    if (c1 - c0 > cap) c1 = c0 + (cap & ~3);  // overflow beyond the stage: read from global
-    int v0 = beg & ~1, v1 = (end + 1) & ~1;
-    const int vmax = (int)(a.nnz & ~1LL);
-    if (v1 > vmax) v1 = vmax > v0 ? vmax : v0;
-    if (v1 - v0 > cap) v1 = v0 + (cap & ~1);
-    st[s].c0 = c0;
-    st[s].cend = c1;
-    st[s].v0 = v0;
-    st[s].vend = v1;
-    const int bytes = (c1 - c0) * 4 + (v1 - v0) * 8;
-    mbar_arrive_tx(&bar[s], bytes);
-    if (c1 > c0) tma_load_1d(scol0 + s * (cap + 4), a.colidx + c0, (c1 - c0) * 4, &bar[s]);
-    if (v1 > v0) tma_load_1d(sval0 + s * (cap + 2), a.val + v0, (v1 - v0) * 8, &bar[s]);
-  };
-
-  long long t = blockIdx.x;
-  int s = 0, phase0 = 0, phase1 = 0;
-  if (t < ntiles) {
-    stage_rp(t, 0);
-    __syncthreads();
-    if (threadIdx.x == 0) bulk(t, 0);
-  }
-  for (; t < ntiles; t += gridDim.x, s ^= 1) {
-    const long long tn = t + gridDim.x;
-    // prefetch the next tile into the other stage (its previous use finished at the
-    // __syncthreads that ended the last iteration)
-    if (tn < ntiles) {
-      stage_rp(tn, s ^ 1);
-      __syncthreads();
-      if (threadIdx.x == 0) bulk(tn, s ^ 1);
-    }
-    mbar_wait(&bar[s], s == 0 ? phase0 : phase1);
-    if (s == 0) phase0 ^= 1;
-    else phase1 ^= 1;
-    const TileStage& S = st[s];
-    const int* cs = scol0 + s * (cap + 4);
-    const double* vs = sval0 + s * (cap + 2);
-    const long long r0 = t * kTileRows;
-    const int nr = (int)min((long long)kTileRows, a.n - r0);
-    for (int lr = warp * G + g; lr < nr; lr += NW * G) {
-      const int beg = S.rp[lr], end = S.rp[lr + 1];
-      double acc[NV][VEC];
-#pragma unroll
-      for (int q = 0; q < NV; ++q)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
-      for (int j0 = beg; j0 < end; j0 += U) {
-        int col[U];
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int j = j0 + u;
-          const bool ok = j < end;
-          col[u] = ok ? (j < S.cend ? cs[j - S.c0] : __ldg(a.colidx + j)) : 0;
-          v[u] = ok ? (j < S.vend ? vs[j - S.v0] : __ldg(a.val + j)) : 0.0;
-        }
-        double xv[U][NV][VEC];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const double* xr = a.X + (long long)col[u] * a.ldx;
-#pragma unroll
-          for (int q = 0; q < NV; ++q) {
-            const int c = (q * LPR + sub) * VEC;
-            if (c < k && j0 + u < end) VecT<VEC>::load(xr + c, xv[u][q]);
-            else
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) xv[u][q][e] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int q = 0; q < NV; ++q)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
-      }
-      const long long r = r0 + lr;
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const int c = (q * LPR + sub) * VEC;
-        if (c < k) {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            double y = a.alpha * acc[q][e];
-            if (a.gamma != 0.0) y = fma(a.gamma, a.Z[r * a.ldz + c + e], y);
-            if (a.beta != 0.0) y = fma(a.beta, a.Yin[r * a.ldyin + c + e], y);
-            a.Y[r * a.ldy + c + e] = y;
-            if (a.dot_mode == 1) dacc[q][e] = fma(y, a.W[r * a.ldw + c + e], dacc[q][e]);
-            else if (a.dot_mode == 2) dacc[q][e] = fma(y, y, dacc[q][e]);
-          }
-        }
-      }
-    }
-    __syncthreads();  // stage s is free for the prefetch two tiles ahead
-  }
-
-  if (a.dot_mode == 0) return;
-#pragma unroll
-  for (int q = 0; q < NV; ++q)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      double v = dacc[q][e];
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      dacc[q][e] = v;
-    }
-  if (g == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) sdot[warp][(q * LPR + sub) * VEC + e] = dacc[q][e];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < k && c < COLS; c += kSpmmThreads) {
-    double sum = 0.0;
-    for (int w = 0; w < NW; ++w) sum += sdot[w][c];
-    a.partials[(long long)blockIdx.x * k + c] = sum;
-  }
-}
-
-template <int LPR, int VEC>
-static int launch_tiled_nv(Ctx* c, SpmmArgs a, int nv, int grid, size_t sm) {
-  switch (nv) {
-#define TCASE(NVV)                                                                         \
-  case NVV: {                                                                              \
-    auto kern = spmm_tiled_kernel<LPR, VEC, NVV>;                                          \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
-    kern<<<grid, kSpmmThreads, sm, c->stream>>>(a);                                        \
-    break;                                                                                 \
-  }
-    TCASE(1)
-    TCASE(2)
-    TCASE(3)
-    default:
-      TCASE(4)
-#undef TCASE
-  }
-  ++g_launches;
-  GCG_CHECK_LAUNCH();
-  return GCG_OK;
-}
-
-template <int VEC>
-static int launch_tiled(Ctx* c, SpmmArgs a, int lpr, int nv, int grid, size_t sm) {
-  switch (lpr) {
-    case 4: return launch_tiled_nv<4, VEC>(c, a, nv, grid, sm);
-    case 8: return launch_tiled_nv<8, VEC>(c, a, nv, grid, sm);
-    case 16: return launch_tiled_nv<16, VEC>(c, a, nv, grid, sm);
-    default: return launch_tiled_nv<32, VEC>(c, a, nv, grid, sm);
-  }
 }
 
 template <int LPR, int VEC>
@@ -480,7 +275,8 @@ static int launch_lpr(Ctx* c, SpmmArgs a, int lpr, int nv, int grid) {
 
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-int spmm_grid(Ctx* c, long long n) { return grid_for(n, 64, 8, c->num_sms); }
+// exactly one wave of kSpmmMinBlocks CTAs per SM (grid-stride over rows)
+int spmm_grid(Ctx* c, long long n) { return grid_for(n, 64, kSpmmMinBlocks, c->num_sms); }
 
 // One SpMM over all k columns, split into passes of at most 256 columns.  With
 // dot_mode != 0 and `partials` given, per-CTA partials ([grid][k], k <= 256)
@@ -493,21 +289,7 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
                      const int* skip) {
   if (n <= 0 || k <= 0) return GCG_OK;
   constexpr int kMaxPass = 256;
-  // tiled (TMA-staged) path: needs 16-byte aligned index/value arrays
-  static const bool legacy_env = getenv("GCG_SPMM_LEGACY") != nullptr;
-  const bool tiled = !legacy_env && nnz > 0 && ((uintptr_t)colidx & 15u) == 0 &&
-                     ((uintptr_t)val & 15u) == 0;
-  const double avg = (double)nnz / (double)n;
-  int tcap = (int)(1.25 * kTileRows * avg) + 16;
-  if (tcap > 8192) tcap = 8192;
-  tcap = (tcap + 3) & ~3;
-  const size_t tsm = (size_t)2 * (tcap + 2) * sizeof(double) + (size_t)2 * (tcap + 4) * sizeof(int);
-  int per_sm = (int)((200 * 1024) / (tsm + 16 * 1024));
-  if (per_sm > 4) per_sm = 4;
-  if (per_sm < 1) per_sm = 1;
-  const long long ntiles = (n + kTileRows - 1) / kTileRows;
-  const int tgrid = (int)(ntiles < (long long)c->num_sms * per_sm ? ntiles : c->num_sms * per_sm);
-  const int grid = tiled ? tgrid : spmm_grid(c, n);
+  const int grid = spmm_grid(c, n);
   if (grid_out) *grid_out = grid;
   if (partials_ext && k > kMaxPass) return GCG_ERR_ARG;
   double* partials = partials_ext;
@@ -517,16 +299,14 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
   }
   for (int c0 = 0; c0 < k; c0 += kMaxPass) {
     const int kc = (k - c0) < kMaxPass ? (k - c0) : kMaxPass;
-    bool vec2 = (kc % 2 == 0) && (ldx % 2 == 0) && aligned16(X + c0);
+    const bool vec2 = (kc % 2 == 0) && (ldx % 2 == 0) && aligned16(X + c0);
     const int vec = vec2 ? 2 : 1;
     const int lanes_needed = (kc + vec - 1) / vec;
+    // small lane groups keep more rows (independent gather chains) per warp:
+    // about two column chunks per lane, at most four
     int lpr = 4;
-    while (lpr < 32 && lpr * 2 < lanes_needed) lpr <<= 1;
-    int nv = (lanes_needed + lpr - 1) / lpr;
-    while (nv > 4 && lpr < 32) {
-      lpr <<= 1;
-      nv = (lanes_needed + lpr - 1) / lpr;
-    }
+    while (lpr < 32 && 2 * lpr < lanes_needed) lpr <<= 1;
+    const int nv = (lanes_needed + lpr - 1) / lpr;
     SpmmArgs a;
     a.n = n;
     a.rowptr = rowptr;
@@ -554,18 +334,9 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     if (gamma != 0.0 && Z != X) bytes += 8.0 * n * kc;
     if (beta != 0.0) bytes += 8.0 * n * kc;
     if (dot_mode == 1 && W != X && W != Z) bytes += 8.0 * n * kc;
-    a.nnz = nnz;
     const int ps = prof_start(c, PROF_SPMM, bytes);
     a.prof_skipped = prof_skip_slot(c, ps);
-    int s;
-    if (tiled) {
-      a.cap = tcap;
-      s = vec2 ? launch_tiled<2>(c, a, lpr, nv, tgrid, tsm)
-               : launch_tiled<1>(c, a, lpr, nv, tgrid, tsm);
-    } else {
-      a.cap = 0;
-      s = vec2 ? launch_lpr<2>(c, a, lpr, nv, grid) : launch_lpr<1>(c, a, lpr, nv, grid);
-    }
+    const int s = vec2 ? launch_lpr<2>(c, a, lpr, nv, grid) : launch_lpr<1>(c, a, lpr, nv, grid);
     prof_stop(c, ps);
     if (s != GCG_OK) return s;
     if (dot_mode && !partials_ext) {
@@ -582,8 +353,8 @@ int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, con
                       const double* Yin, long long ldyin, double* Y, long long ldy, int dot_mode,
                       const double* W, long long ldw, double* partials, int* grid_out,
                       const int* skip) {
-  return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta, Yin,
-                          ldyin, Y, ldy, dot_mode, W, ldw, nullptr, partials, grid_out, skip);
+  return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta,
+                          Yin, ldyin, Y, ldy, dot_mode, W, ldw, nullptr, partials, grid_out, skip);
 }
 
 }  // namespace gcg

@@ -1,23 +1,25 @@
-// Tall-skinny fp64 GEMMs on B200: Gram (MultiVecInnerProd) and LinComb
-// (MultiVecLinearComb).
+// Tall-skinny fp64 GEMMs on B200 with FP64 tensor cores (DMMA): Gram
+// (MultiVecInnerProd) and LinComb (MultiVecLinearComb).
 //
 //  gram     G = alpha X'Y + beta G   multivec.py:84-112, _cy.pyx:26-50, orth.py:139-140,164,242,288
 //  lincomb  Y = alpha X C + beta Y   solver.py:300,333,376; orth.py:144,175,184,264,291
 //
-// Both stream an n-long, k-wide row-major panel once from HBM.  Shapes on the
-// hot path are k ~ 16..600, so they are HBM-bound (Gram with k1*k2/(k1+k2)
-// small, LinComb with small d) up to FP64-bound (RR update m x d = 200 x 160).
-// B200 has no FP64 tcgen05 kind, so the FP64 work runs on the FFMA64 pipe;
-// the design goal is to keep enough bytes in flight: every CTA streams its
-// panel through a 3-stage cp.async (LDGSTS) shared-memory ring (16-byte copies
-// when the row runs are 16-byte aligned), and each thread keeps a 4x4 register
-// micro-tile so shared-memory reads stay at 1 LDS.64 per 2 FMAs.
+// B200 has no FP64 kind in tcgen05; its FP64 tensor path is the warp-level
+// DMMA (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4), at the same ~40 TF as the FFMA64
+// pipe but with 256 FMAs per instruction and operands from registers.  With
+// SIMT micro-tiles these kernels were shared-memory-issue bound (one LDS per
+// two FMAs); with DMMA a warp tile of FMxFN 8x8 blocks needs FM+FN fragment
+// loads per FM*FN*256 FMAs.
 //
-// Gram splits the n-long contraction into row slabs (grid = tiles x slabs, a
-// few CTAs per SM); each CTA reduces its row groups in shared memory and writes
-// one partial tile; a second kernel sums the slab partials with one warp per
-// output in a fixed order.  The result is bit-identical run to run (the
-// reference's `deterministic` contract, test_kernels.py:74-85).
+// Both kernels stream the n-long panel once from HBM through a 3-stage
+// cp.async (LDGSTS) shared-memory ring (16-byte copies when row runs are
+// 16-byte aligned).  Shared-memory row strides are 4 (mod 16) doubles so the
+// four rows a half-warp touches for a fragment land in disjoint bank groups.
+//
+// Gram splits the n-long contraction over (a) row groups of warps inside a CTA
+// and (b) row slabs across CTAs; CTA partials are combined in shared memory
+// and the slab partials by a second kernel with one warp per output, always
+// in a fixed order — bit-identical run to run (test_kernels.py:74-85).
 
 #include "common.cuh"
 
@@ -40,12 +42,17 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Copy `cols` doubles of row `row` (global, starting at src) into smem dst,
-// element stride 1; zero-fill beyond `valid`.  VEC16: 16-byte copies (src and
-// dst 16-byte aligned, cols even).
+// d = a*b + d for one 8x8x4 fp64 block (A row fragment, B col fragment)
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Copy element `idx` (pair index when VEC16) of a row run of `valid` doubles.
 template <bool VEC16>
-__device__ __forceinline__ void stage_row_elems(double* dst, const double* src, int idx,
-                                                int valid, const double* safe) {
+__device__ __forceinline__ void stage_elems(double* dst, const double* src, int idx, int valid,
+                                            const double* safe) {
   if (VEC16) {
     const int e = idx * 2;
     const int nb = valid - e >= 2 ? 16 : (valid - e == 1 ? 8 : 0);
@@ -55,29 +62,38 @@ __device__ __forceinline__ void stage_row_elems(double* dst, const double* src, 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Gram
-
 constexpr int kStages = 3;
 
-template <int BM, int BN, int R, bool VEC16>
-__global__ void __launch_bounds__(256) gram2_kernel(long long n, int k1, int k2,
-                                                    const double* __restrict__ X, long long ldx,
-                                                    const double* __restrict__ Y, long long ldy,
-                                                    long long rows_per_slab, double* part) {
-  constexpr int TM = 4, TN = 4;
-  constexpr int TX = BN / TN, TY = BM / TM, TT = TX * TY, G = 256 / TT;
-  constexpr int W = BM + BN + 2;  // padded smem row (doubles)
+// smem stride (doubles) >= w, even, and 4 (mod 16)
+__host__ __device__ constexpr int frag_stride(int w) { return ((w + 11) / 16) * 16 + 4; }
+
+// ---------------------------------------------------------------------------
+// Gram: CTA tile BM x BN; warps tile it WM x WN; the remaining warps split rows.
+
+template <int BM, int BN, int WM, int WN, int R, bool VEC16>
+__global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int k2,
+                                                        const double* __restrict__ X,
+                                                        long long ldx,
+                                                        const double* __restrict__ Y,
+                                                        long long ldy, long long rows_per_slab,
+                                                        double* part) {
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int WT = (BM / WM) * (BN / WN);  // warps per output tile
+  constexpr int RG = 8 / WT;                 // row groups
+  static_assert(WT * RG == 8, "8 warps");
+  constexpr int W = frag_stride(BM + BN);
   constexpr int V = VEC16 ? 2 : 1;
   extern __shared__ __align__(16) double smg[];
   const int tm0 = blockIdx.x * BM, tn0 = blockIdx.y * BN;
   const long long r0 = (long long)blockIdx.z * rows_per_slab;
   long long r1 = r0 + rows_per_slab;
   if (r1 > n) r1 = n;
-  const int tid = threadIdx.x;
-  const int grp = tid / TT, t = tid % TT, tx = t % TX, ty = t / TX;
-  const int vx = min(BM, k1 - tm0), vy = min(BN, k2 - tn0);  // valid columns of the tiles
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wt = warp % WT, rg = warp / WT;
+  const int wm0 = (wt / (BN / WN)) * WM, wn0 = (wt % (BN / WN)) * WN;
+  const int vx = min(BM, k1 - tm0), vy = min(BN, k2 - tn0);
   const int nch = (int)((r1 - r0 + R - 1) / R);
+  const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column (m or n)
 
   auto load = [&](int ch, int st) {
     const long long rb = r0 + (long long)ch * R;
@@ -88,17 +104,17 @@ __global__ void __launch_bounds__(256) gram2_kernel(long long n, int k1, int k2,
       double* dst = smg + (st * R + rr) * W;
       const bool ok = row < r1;
       if (cc < PX)
-        stage_row_elems<VEC16>(dst, X + (ok ? row : r0) * ldx + tm0, cc, ok ? vx : 0, X);
+        stage_elems<VEC16>(dst, X + (ok ? row : r0) * ldx + tm0, cc, ok ? vx : 0, X);
       else
-        stage_row_elems<VEC16>(dst + BM, Y + (ok ? row : r0) * ldy + tn0, cc - PX, ok ? vy : 0, Y);
+        stage_elems<VEC16>(dst + BM, Y + (ok ? row : r0) * ldy + tn0, cc - PX, ok ? vy : 0, Y);
     }
   };
 
-  double acc[TM][TN];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
@@ -112,34 +128,37 @@ __global__ void __launch_bounds__(256) gram2_kernel(long long n, int k1, int k2,
     cp_commit();
     const double* base = smg + (ch % kStages) * R * W;
 #pragma unroll 2
-    for (int rr = grp; rr < R; rr += G) {
-      const double* rowp = base + rr * W;
-      double xv[TM], yv[TN];
+    for (int ks = rg; ks < R / 4; ks += RG) {
+      const double* rowp = base + (ks * 4 + fr) * W;
+      double a[FM], b[FN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) xv[i] = rowp[ty + i * TY];
+      for (int i = 0; i < FM; ++i) a[i] = rowp[wm0 + i * 8 + fc];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) yv[j] = rowp[BM + tx + j * TX];
+      for (int j = 0; j < FN; ++j) b[j] = rowp[BM + wn0 + j * 8 + fc];
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fma(xv[i], yv[j], acc[i][j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_wait<0>();
   __syncthreads();
-  // combine the G row groups in a fixed order
-  double* red = smg;  // G * BM * BN doubles (<= 4096)
+  // combine the RG row groups in a fixed order
+  double* red = smg;  // RG * BM * BN doubles
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) red[(grp * BM + ty + i * TY) * BN + tx + j * TX] = acc[i][j];
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        red[(rg * BM + wm0 + i * 8 + fc) * BN + wn0 + j * 8 + fr * 2 + h] = acc[i][j][h];
   __syncthreads();
   double* out = part + (long long)blockIdx.z * k1 * k2;
   for (int e = tid; e < BM * BN; e += 256) {
     const int rr = e / BN, cc = e % BN;
     double s = 0.0;
 #pragma unroll
-    for (int g = 0; g < G; ++g) s += red[g * BM * BN + e];
+    for (int g = 0; g < RG; ++g) s += red[g * BM * BN + e];
     if (tm0 + rr < k1 && tn0 + cc < k2) out[(long long)(tm0 + rr) * k2 + tn0 + cc] = s;
   }
 }
@@ -164,59 +183,94 @@ __global__ void gram_finish2_kernel(int k1, int k2, int nslab, const double* __r
 
 static inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-template <int BM, int BN>
-static int gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
-                   const double* Y, long long ldy, double* part, long long rps, int nslab,
-                   bool vec) {
-  constexpr int R = 32;
-  const size_t sm = sizeof(double) * (size_t)kStages * R * (BM + BN + 2);
-  const size_t need = sm > 4096 * sizeof(double) ? sm : 4096 * sizeof(double);
+template <int BM, int BN, int WM, int WN>
+static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                    const double* Y, long long ldy, double* part, long long rps, int nslab,
+                    bool vec) {
+  constexpr int W = frag_stride(BM + BN);
+  // rows per stage: as many as fit three stages in ~110 KB (>= 16)
+  constexpr int R = (3 * 64 * W * 8 <= 112 * 1024) ? 64 : ((3 * 32 * W * 8 <= 160 * 1024) ? 32 : 16);
+  constexpr int RG = 8 / ((BM / WM) * (BN / WN));
+  const size_t sm_stage = sizeof(double) * (size_t)kStages * R * W;
+  const size_t sm_red = sizeof(double) * (size_t)RG * BM * BN;
+  const size_t sm = sm_stage > sm_red ? sm_stage : sm_red;
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, nslab);
   if (vec) {
-    auto kern = gram2_kernel<BM, BN, R, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
-    kern<<<grid, 256, need, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+    auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
   } else {
-    auto kern = gram2_kernel<BM, BN, R, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
-    kern<<<grid, 256, need, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+    auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
   }
-  return GCG_OK;
+}
+
+// Tile shapes: the whole k1 x k2 output in one CTA tile when it is skinny
+// (k2 <= 32, k1 <= 256: 8 warps stacked along k1), so X and Y are each read
+// once; 64 x 64 tiles (2 x 2 warps, 2 row groups) otherwise.
+static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                         const double* Y, long long ldy, double* part, long long rps, int nslab,
+                         bool vec, int* bm_out, int* bn_out) {
+  const int f1 = (k1 + 63) / 64, f2 = (k2 + 7) / 8;
+#define GO(bm, bn, wm, wn)                                                              \
+  do {                                                                                \
+    *bm_out = bm;                                                                     \
+    *bn_out = bn;                                                                     \
+    if (part) gram_go<bm, bn, wm, wn>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec); \
+    return GCG_OK;                                                                    \
+  } while (0)
+  if (k1 <= 16 && k2 <= 16) GO(16, 16, 16, 16);
+  if (k1 <= 32 && k2 <= 32) GO(32, 32, 32, 32);
+  if (k2 <= 32 && k1 <= 256) {
+    switch (f1 * 8 + f2) {
+      case 1 * 8 + 1: GO(64, 8, 8, 8);
+      case 1 * 8 + 2: GO(64, 16, 8, 16);
+      case 1 * 8 + 3: GO(64, 24, 8, 24);
+      case 1 * 8 + 4: GO(64, 32, 8, 32);
+      case 2 * 8 + 1: GO(128, 8, 16, 8);
+      case 2 * 8 + 2: GO(128, 16, 16, 16);
+      case 2 * 8 + 3: GO(128, 24, 16, 24);
+      case 2 * 8 + 4: GO(128, 32, 16, 32);
+      case 3 * 8 + 1: GO(192, 8, 24, 8);
+      case 3 * 8 + 2: GO(192, 16, 24, 16);
+      case 3 * 8 + 3: GO(192, 24, 24, 24);
+      case 3 * 8 + 4: GO(192, 32, 24, 32);
+      case 4 * 8 + 1: GO(256, 8, 32, 8);
+      case 4 * 8 + 2: GO(256, 16, 32, 16);
+      case 4 * 8 + 3: GO(256, 24, 32, 24);
+      default: GO(256, 32, 32, 32);
+    }
+  }
+  GO(64, 64, 32, 32);
+#undef GO
 }
 
 int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                 const double* Y, long long ldy, double alpha, double beta, double* G,
                 long long grs, long long gcs) {
   if (k1 <= 0 || k2 <= 0) return GCG_OK;
-  const int BM = k1 <= 16 ? 16 : (k1 <= 32 ? 32 : 64);
-  const int BN = k2 <= 16 ? 16 : (k2 <= 32 ? 32 : 64);
+  // skinny on the left: compute G' = Y'X with roles swapped (write through swapped strides)
+  if (k1 <= 32 && k2 > 32 && k2 <= 256)
+    return gram_launch(c, n, k2, k1, Y, ldy, X, ldx, alpha, beta, G, gcs, grs);
+  int BM = 0, BN = 0;
+  gram_dispatch(c, n, k1, k2, X, ldx, Y, ldy, nullptr, 0, 0, false, &BM, &BN);
   const long long tiles = (long long)((k1 + BM - 1) / BM) * ((k2 + BN - 1) / BN);
-  // ~3 CTAs per SM in total, slabs a multiple of the 32-row stage
-  long long nslab = (3LL * c->num_sms + tiles - 1) / tiles;
-  const long long max_slab = (n + 127) / 128;
+  // ~2 CTAs per SM in total, slabs a multiple of 64 rows
+  long long nslab = (2LL * c->num_sms + tiles - 1) / tiles;
+  const long long max_slab = (n + 255) / 256;
   if (nslab > max_slab) nslab = max_slab;
   if (nslab < 1) nslab = 1;
   if (nslab > 65535) nslab = 65535;
   long long rps = (n + nslab - 1) / nslab;
-  rps = (rps + 31) / 32 * 32;
+  rps = (rps + 63) / 64 * 64;
   nslab = (n + rps - 1) / rps;
   if (nslab < 1) nslab = 1;
   GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)nslab * k1 * k2));
   double* part = (double*)c->partials.ptr;
-  const bool vec = (ldx % 2 == 0) && (ldy % 2 == 0) && al16(X) && al16(Y) && (BM % 2 == 0);
+  const bool vec = (ldx % 2 == 0) && (ldy % 2 == 0) && al16(X) && al16(Y);
   const int ps = prof_start(c, PROF_GRAM, 8.0 * n * (X == Y ? k1 : k1 + k2));
-#define GRAM_CASE(bm, bn) \
-  if (BM == bm && BN == bn) gram_go<bm, bn>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, (int)nslab, vec)
-  GRAM_CASE(16, 16);
-  else GRAM_CASE(16, 32);
-  else GRAM_CASE(16, 64);
-  else GRAM_CASE(32, 16);
-  else GRAM_CASE(32, 32);
-  else GRAM_CASE(32, 64);
-  else GRAM_CASE(64, 16);
-  else GRAM_CASE(64, 32);
-  else GRAM_CASE(64, 64);
-#undef GRAM_CASE
+  gram_dispatch(c, n, k1, k2, X, ldx, Y, ldy, part, rps, (int)nslab, vec, &BM, &BN);
   prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
@@ -229,30 +283,34 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
 }
 
 // ---------------------------------------------------------------------------
-// LinComb  Y = alpha X C + beta Y
+// LinComb  Y = alpha X C + beta Y: CTA tile BM rows x BN columns, warp tile
+// WM x WN, K (= m) in BK = 16 chunks through the cp.async ring.
 
-template <int BM, int BN, bool VEC16>
-__global__ void __launch_bounds__(256) lincomb2_kernel(long long n, int m, int d, double alpha,
-                                                       const double* __restrict__ X,
-                                                       long long ldx,
-                                                       const double* __restrict__ C,
-                                                       long long ldc, double beta, double* Y,
-                                                       long long ldy) {
+template <int BM, int BN, int WM, int WN, bool VEC16>
+__global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, int d,
+                                                           double alpha,
+                                                           const double* __restrict__ X,
+                                                           long long ldx,
+                                                           const double* __restrict__ C,
+                                                           long long ldc, double beta, double* Y,
+                                                           long long ldy) {
   constexpr int BK = 16;
-  constexpr int TM = 4, TN = 4, TX = BN / TN, TY = BM / TM;
-  static_assert(TX * TY == 256, "256 threads");
-  constexpr int XW = BK + 2;  // padded X row in smem
-  constexpr int CW = BN + 2;
-  constexpr int XS = BM * XW, CS = BK * CW;  // doubles per stage
+  constexpr int FM = WM / 8, FN = WN / 8;
+  static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
+  constexpr int XW = frag_stride(BK);  // 20
+  constexpr int CW = frag_stride(BN);
+  constexpr int XS = BM * XW, CS = BK * CW;
   constexpr int V = VEC16 ? 2 : 1;
   extern __shared__ __align__(16) double sml[];
   double* xs = sml;
   double* cs = sml + kStages * XS;
   const long long r0 = (long long)blockIdx.x * BM;
   const int c0 = blockIdx.y * BN;
-  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp / (BN / WN)) * WM, wn0 = (warp % (BN / WN)) * WN;
   const int nk = (m + BK - 1) / BK;
   const int vc = min(BN, d - c0);
+  const int fr = lane & 3, fc = lane >> 2;
 
   auto load = [&](int kb, int st) {
     const int k0 = kb * BK;
@@ -262,8 +320,8 @@ __global__ void __launch_bounds__(256) lincomb2_kernel(long long n, int m, int d
       const int rr = e / PX, cc = e % PX;
       const long long row = r0 + rr;
       const bool ok = row < n;
-      stage_row_elems<VEC16>(xs + st * XS + rr * XW, X + (ok ? row : 0) * ldx + k0, cc,
-                             ok ? vk : 0, X);
+      stage_elems<VEC16>(xs + st * XS + rr * XW, X + (ok ? row : 0) * ldx + k0, cc, ok ? vk : 0,
+                         X);
     }
     for (int e = tid; e < BK * BN; e += 256) {
       const int kk = e / BN, cc = e % BN;
@@ -273,11 +331,11 @@ __global__ void __launch_bounds__(256) lincomb2_kernel(long long n, int m, int d
     }
   };
 
-  double acc[TM][TN];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < nk) load(s, s);
@@ -291,45 +349,49 @@ __global__ void __launch_bounds__(256) lincomb2_kernel(long long n, int m, int d
     const double* xb = xs + (kb % kStages) * XS;
     const double* cb = cs + (kb % kStages) * CS;
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double xv[TM], cv[TN];
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double a[FM], b[FN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) xv[i] = xb[(ty + i * TY) * XW + kk];
+      for (int i = 0; i < FM; ++i) a[i] = xb[(wm0 + i * 8 + fc) * XW + ks * 4 + fr];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) cv[j] = cb[kk * CW + tx + j * TX];
+      for (int j = 0; j < FN; ++j) b[j] = cb[(ks * 4 + fr) * CW + wn0 + j * 8 + fc];
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fma(xv[i], cv[j], acc[i][j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_wait<0>();
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const long long row = r0 + ty + i * TY;
+  for (int i = 0; i < FM; ++i) {
+    const long long row = r0 + wm0 + i * 8 + fc;
     if (row >= n) continue;
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int col = c0 + tx + j * TX;
-      if (col >= d) continue;
-      double* y = Y + row * ldy + col;
-      *y = (beta == 0.0) ? alpha * acc[i][j] : fma(alpha, acc[i][j], beta * *y);
+    for (int j = 0; j < FN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = c0 + wn0 + j * 8 + fr * 2 + h;
+        if (col >= d) continue;
+        double* y = Y + row * ldy + col;
+        *y = (beta == 0.0) ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *y);
+      }
     }
   }
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int WM, int WN>
 static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const double* X,
                        long long ldx, const double* C, long long ldc, double beta, double* Y,
                        long long ldy, bool vec) {
-  const size_t sm = sizeof(double) * (size_t)kStages * (BM * (16 + 2) + 16 * (BN + 2));
+  const size_t sm =
+      sizeof(double) * (size_t)kStages * (BM * frag_stride(16) + 16 * frag_stride(BN));
   dim3 grid((unsigned)((n + BM - 1) / BM), (d + BN - 1) / BN);
   if (vec) {
-    auto kern = lincomb2_kernel<BM, BN, true>;
+    auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
   } else {
-    auto kern = lincomb2_kernel<BM, BN, false>;
+    auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
   }
@@ -341,14 +403,23 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   if (n <= 0 || d <= 0) return GCG_OK;
   const int ps =
       prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
-  // 16-byte staging needs every X row run 16-byte aligned (XW = 18 keeps smem aligned)
   const bool vec = (ldx % 2 == 0) && al16(X);
-  if (d <= 16)
-    lincomb_go<256, 16>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec);
-  else if (d <= 32)
-    lincomb_go<128, 32>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec);
-  else
-    lincomb_go<64, 64>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec);
+  // One column tile covers all d <= 256 columns, so X is streamed exactly once:
+  // d <= 64: 8 warps stacked along rows (BM = 256, warp tile 32 x BN);
+  // d  > 64: 2 x 4 warps (BM = 64, warp tile 32 x BN/4).
+#define LC(bm, bn, wm, wn) lincomb_go<bm, bn, wm, wn>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec)
+  if (d <= 8) LC(256, 8, 32, 8);
+  else if (d <= 16) LC(256, 16, 32, 16);
+  else if (d <= 24) LC(256, 24, 32, 24);
+  else if (d <= 32) LC(256, 32, 32, 32);
+  else if (d <= 48) LC(256, 48, 32, 48);
+  else if (d <= 64) LC(256, 64, 32, 64);
+  else if (d <= 96) LC(64, 96, 32, 24);
+  else if (d <= 128) LC(64, 128, 32, 32);
+  else if (d <= 160) LC(64, 160, 32, 40);
+  else if (d <= 192) LC(64, 192, 32, 48);
+  else LC(64, 256, 32, 64);
+#undef LC
   prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();

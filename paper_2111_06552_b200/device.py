@@ -221,10 +221,10 @@ def symmetrize(ctx, A):
     return A
 
 
-def svqb_prepare(ctx, G, dep_tol, Q, status):
+def svqb_prepare(ctx, G, dep_tol, Q, status, skip_tol=-1.0):
     w = G.shape[0]
-    _lib.call("gcg_svqb_prepare", ctx.h, w, _p(G), _ld(G), float(dep_tol), _p(Q), _ld(Q),
-              _p(status))
+    _lib.call("gcg_svqb_prepare", ctx.h, w, _p(G), _ld(G), float(dep_tol), float(skip_tol), _p(Q),
+              _ld(Q), _p(status))
 
 
 def deflate_status(ctx, R, dnew, dgks, status):

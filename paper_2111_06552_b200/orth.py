@@ -146,7 +146,7 @@ def _leaf_svqb(st, lo, hi):
         st.reductions += 1
         passes += 1
         q = dev.empty(w, w)
-        D.svqb_prepare(dev, g, cfg.dependence_tol, q, st.status)
+        D.svqb_prepare(dev, g, cfg.dependence_tol, q, st.status, skip_tol=cfg.reorth_tol)
         defect, nbad, _ = st.status[:3].tolist()
         if defect <= cfg.reorth_tol:
             return

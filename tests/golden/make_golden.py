@@ -4,7 +4,8 @@ Run in the build container, where the reference is available — either built
 into oracle/_ref (oracle/build_ref.sh) or importable from /root/reference:
 
     python tests/golden/make_golden.py            # small cases -> golden.npz
-    python tests/golden/make_golden.py --cfg2     # BASELINE config 2 (~8 min)
+    python tests/golden/make_golden.py --cfg 2    # BASELINE config 2 (~8 min)
+    python tests/golden/make_golden.py --cfg 3    # BASELINE config 3 (~1-2 h)
 
 The outputs are committed; the GPU box (which has no /root/reference) only
 reads them.  Parity cases follow SURVEY.md §8(c): the reference's own KAT
@@ -180,12 +181,13 @@ def small(out):
     return meta
 
 
-def cfg2():
-    pr = P.baseline_problem(2)
+def cfg_run(cfg):
+    pr = P.baseline_problem(cfg)
     K.use_backend("numpy")
     t0 = time.perf_counter()
     with patched():
-        rep = gcg_solve(pr.a, None, SolverConfig(num_eigen=pr.num_eigen, tol=pr.tol, seed=0))
+        rep = gcg_solve(pr.a, pr.b, SolverConfig(num_eigen=pr.num_eigen, block_size=pr.block_size,
+                                                 tol=pr.tol, moving=pr.moving, seed=0))
     dt = time.perf_counter() - t0
     return dict(
         name=pr.name, status=rep.status, iterations=rep.iterations, seconds=dt,
@@ -201,13 +203,13 @@ def cfg2():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--cfg", type=int, default=0, help="full BASELINE config run (2 or 3)")
     args = ap.parse_args()
-    if args.cfg2:
-        res = cfg2()
-        with open(os.path.join(HERE, "golden_cfg2.json"), "w") as f:
+    if args.cfg:
+        res = cfg_run(args.cfg)
+        with open(os.path.join(HERE, f"golden_cfg{args.cfg}.json"), "w") as f:
             json.dump(res, f, indent=1)
-        print("cfg2", res["status"], res["iterations"], f"{res['seconds']:.1f}s")
+        print(f"cfg{args.cfg}", res["status"], res["iterations"], f"{res['seconds']:.1f}s")
         return
     out = {}
     meta = small(out)
