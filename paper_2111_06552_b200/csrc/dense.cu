@@ -29,14 +29,45 @@ constexpr int kJacMax = 64;
 
 // Parallel cyclic Jacobi on a[mp][kJacMax+1] (symmetric), accumulating v.
 // mp is even; rows/cols >= m are zero padding.  All threads of the CTA call it.
+//
+// Per round (mp/2 disjoint rotations, round-robin pairing): (1) one thread
+// per pair computes (c, s) with reciprocal/sqrt only, plus the exact new
+// diagonal (Rutishauser: a_pq becomes exactly 0); (2) every 2x2 block (P, R)
+// of pair rows x pair columns is transformed in one step, B' = J_P^T B J_R,
+// reading and writing each element once, together with V <- V J.  Two
+// barriers per round; each thread's block / row assignments are fixed for the
+// whole solve and kept in registers (no integer division in the loop).
+constexpr int kJacThreads = 256;
+constexpr int kJacMaxBlk = (kJacMax / 2) * (kJacMax / 2) / kJacThreads;  // 4
+constexpr int kJacMaxVrow = kJacMax * (kJacMax / 2) / kJacThreads;       // 8
+
 __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJacMax + 1],
                               double* cs, double* sn, int* pp, int* qq, double* red) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
   const int half = mp / 2;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    // convergence: off-diagonal mass vs diagonal mass
+  // fixed work lists: blocks (P <= R) and V items (row i, pair R)
+  // thread tid owns blocks e = tid + b*kJacThreads (kept only when P <= R) and V
+  // items e = tid + b*kJacThreads; -1 marks an empty slot
+  int blkP[kJacMaxBlk], blkR[kJacMaxBlk];
+#pragma unroll
+  for (int b = 0; b < kJacMaxBlk; ++b) {
+    const int e = tid + b * kJacThreads;
+    const int P = e / half, R = e % half;
+    const bool ok = e < half * half && P <= R;
+    blkP[b] = ok ? P : -1;
+    blkR[b] = R;
+  }
+  int vI[kJacMaxVrow], vR[kJacMaxVrow];
+#pragma unroll
+  for (int b = 0; b < kJacMaxVrow; ++b) {
+    const int e = tid + b * kJacThreads;
+    vI[b] = e < mp * half ? e / half : -1;
+    vR[b] = e % half;
+  }
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    // convergence: off-diagonal vs diagonal mass (accumulated separately)
     double off = 0.0, dia = 0.0;
-    for (int e = tid; e < mp * mp; e += nt) {
+    for (int e = tid; e < mp * mp; e += kJacThreads) {
       const int i = e / mp, j = e % mp;
       const double x = a[i][j];
       if (i == j) dia += x * x;
@@ -50,13 +81,12 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
     }
     __syncthreads();
     double toff = 0.0, tdia = 0.0;
-    for (int w = 0; w < nt / 32; ++w) {
+    for (int w = 0; w < kJacThreads / 32; ++w) {
       toff += red[2 * w];
       tdia += red[2 * w + 1];
     }
     __syncthreads();
     // relative off-diagonal norm <= 1e-14: eigenvalues/vectors at rounding level
-    // (a tighter test can stall on the rounding floor of the parallel rotations)
     if (toff <= 1e-28 * tdia || toff == 0.0) break;
     for (int round = 0; round < mp - 1; ++round) {
       if (tid < half) {
@@ -65,65 +95,75 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
           p = round;
           q = mp - 1;
         } else {
-          p = (round + tid) % (mp - 1);
-          q = (round - tid + mp - 1) % (mp - 1);
+          p = round + tid;
+          if (p >= mp - 1) p -= mp - 1;
+          q = round - tid;
+          if (q < 0) q += mp - 1;
         }
         if (p > q) {
-          int t = p;
+          const int t = p;
           p = q;
           q = t;
         }
-        const double apq = a[p][q];
-        double c = 1.0, s = 0.0;
-        const double app = a[p][p], aqq = a[q][q];
-        // skip rotations whose off-diagonal entry is negligible against the diagonal
+        const double apq = a[p][q], app = a[p][p], aqq = a[q][q];
+        double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq)) && apq != 0.0) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          c = 1.0 / sqrt(1.0 + t * t);
+          const double theta = (aqq - app) * (0.5 / apq);
+          t = 1.0 / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+          if (theta < 0.0) t = -t;
+          c = rsqrt(fma(t, t, 1.0));
           s = t * c;
         }
         cs[tid] = c;
         sn[tid] = s;
         pp[tid] = p;
         qq[tid] = q;
-        // exact post-rotation diagonal (Rutishauser); a_pq itself becomes exactly 0
-        const double tt = (c != 1.0 || s != 0.0) ? s / c : 0.0;
-        red[64 + 2 * tid] = app - tt * apq;
-        red[64 + 2 * tid + 1] = aqq + tt * apq;
+        red[64 + 2 * tid] = app - t * apq;
+        red[64 + 2 * tid + 1] = aqq + t * apq;
       }
       __syncthreads();
-      // rows: A <- J^T A
-      for (int e = tid; e < half * mp; e += nt) {
-        const int pr = e / mp, j = e % mp;
-        const int p = pp[pr], q = qq[pr];
-        const double c = cs[pr], s = sn[pr];
-        const double ap = a[p][j], aq = a[q][j];
-        a[p][j] = c * ap - s * aq;
-        a[q][j] = s * ap + c * aq;
-      }
-      __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int e = tid; e < half * mp; e += nt) {
-        const int pr = e / mp, i = e % mp;
-        const int p = pp[pr], q = qq[pr];
-        const double c = cs[pr], s = sn[pr];
-        const double ap = a[i][p], aq = a[i][q];
-        if (s == 0.0 && c == 1.0) {
-          // no rotation for this pair: entries unchanged
-        } else if (i == p) {
-          a[p][p] = red[64 + 2 * pr];
-          a[p][q] = 0.0;
-        } else if (i == q) {
-          a[q][p] = 0.0;
-          a[q][q] = red[64 + 2 * pr + 1];
-        } else {
-          a[i][p] = c * ap - s * aq;
-          a[i][q] = s * ap + c * aq;
+#pragma unroll
+      for (int b = 0; b < kJacMaxBlk; ++b) {
+        const int P = blkP[b], R = blkR[b];
+        if (P < 0) continue;
+        const double cP = cs[P], sP = sn[P];
+        const int p = pp[P], q = qq[P];
+        if (P == R) {
+          if (sP != 0.0) {
+            a[p][p] = red[64 + 2 * P];
+            a[q][q] = red[64 + 2 * P + 1];
+            a[p][q] = 0.0;
+            a[q][p] = 0.0;
+          }
+          continue;
         }
-        const double vp = v[i][p], vq = v[i][q];
-        v[i][p] = c * vp - s * vq;
-        v[i][q] = s * vp + c * vq;
+        const double cR = cs[R], sR = sn[R];
+        if (sP == 0.0 && sR == 0.0) continue;
+        const int r = pp[R], u = qq[R];
+        const double b00 = a[p][r], b01 = a[p][u], b10 = a[q][r], b11 = a[q][u];
+        const double u0 = cP * b00 - sP * b10, u1 = cP * b01 - sP * b11;
+        const double w0 = sP * b00 + cP * b10, w1 = sP * b01 + cP * b11;
+        const double n00 = cR * u0 - sR * u1, n01 = sR * u0 + cR * u1;
+        const double n10 = cR * w0 - sR * w1, n11 = sR * w0 + cR * w1;
+        a[p][r] = n00;
+        a[p][u] = n01;
+        a[q][r] = n10;
+        a[q][u] = n11;
+        a[r][p] = n00;
+        a[u][p] = n01;
+        a[r][q] = n10;
+        a[u][q] = n11;
+      }
+#pragma unroll
+      for (int b = 0; b < kJacMaxVrow; ++b) {
+        const int i = vI[b], R = vR[b];
+        if (i < 0) continue;
+        const double cR = cs[R], sR = sn[R];
+        if (sR == 0.0) continue;
+        const int r = pp[R], u = qq[R];
+        const double vr = v[i][r], vu = v[i][u];
+        v[i][r] = cR * vr - sR * vu;
+        v[i][u] = sR * vr + cR * vu;
       }
       __syncthreads();
     }
