@@ -127,6 +127,45 @@ int gcg_block_cg(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr, const
                  int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
                  int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres);
 
+/* Row-partitioned (multi-GPU) block CG.  Rows [0, n) are owned; rows [n, n + nghost)
+ * of x (and of the internal direction block) are ghost copies of neighbours' rows
+ * that the local CSR references (column indices >= n).  The host exchanges them:
+ *   callback(0, k, user): halo — send_buf (nsend x k, packed) -> recv_buf (nghost x k),
+ *                          the library gathers rows send_idx[] before and scatters
+ *                          recv_buf into the ghost rows after;
+ *   callback(1, k, user): allreduce — red_buf[0:k] holds this rank's column sums on
+ *                          entry and must hold the global sums on return.
+ * Both are called from the enqueuing thread, stream-ordered on the context stream. */
+typedef struct gcg_cg_dist {
+  int64_t nghost;
+  int64_t nsend;
+  const int32_t* send_idx; /* device [nsend], local row indices */
+  double* send_buf;        /* device [nsend * k] */
+  double* recv_buf;        /* device [nghost * k] */
+  double* red_buf;         /* device [k] */
+  int (*callback)(int op, int k, void* user);
+  void* user;
+} gcg_cg_dist;
+
+int gcg_block_cg_dist(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, const double* val, double diag_shift, int64_t k,
+                      const double* rhs, int64_t ldr, double* x, int64_t ldx, int32_t max_iters,
+                      double rel_tol, int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen,
+                      double* d_relres, const gcg_cg_dist* dist);
+
+/* out[i, :] = X[idx[i], :]  (row gather, k columns; halo send packing) */
+int gcg_gather_rows(void* ctx, int64_t nidx, const int32_t* idx, int64_t k, const double* X,
+                    int64_t ldx, double* out, int64_t ldo);
+
+/* Ritz-residual column sums (row-partitioned form of gcg_ritz_residuals):
+ * sums[q*k + j], q = 0..3: ||AX - lam (X or BX)||^2, X.X, X.BX, BX.BX; then
+ * gcg_ritz_finish turns (globally reduced) sums into the residuals. */
+int gcg_ritz_sums(void* ctx, int64_t n, int64_t k, const double* AX, int64_t ldax,
+                  const double* X, int64_t ldx, const double* BX, int64_t ldbx,
+                  const double* lam, int mode, double* sums);
+int gcg_ritz_finish(void* ctx, int64_t k, const double* sums, const double* lam, int mode,
+                    double* out);
+
 /* ---- small dense (device, row-major) -------------------------------------- */
 /* full symmetric eigendecomposition: w ascending, V[:, j] its eigenvector with the
  * largest-|entry| made positive (dense.py:63-82).  A is read only. */

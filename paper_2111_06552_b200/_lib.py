@@ -42,6 +42,11 @@ _SIGS = {
     "gcg_fill": [_ptr, _i64, _i64, _dbl, _ptr, _i64],
     "gcg_block_cg": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64, _i32,
                      _dbl, _ptr, _ptr, _ptr, _ptr],
+    "gcg_block_cg_dist": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64,
+                          _i32, _dbl, _ptr, _ptr, _ptr, _ptr, _ptr],
+    "gcg_gather_rows": [_ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64],
+    "gcg_ritz_sums": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
+    "gcg_ritz_finish": [_ptr, _i64, _ptr, _ptr, _int, _ptr],
     "gcg_syev": [_ptr, _i64, _ptr, _i64, _ptr, _ptr, _i64],
     "gcg_dgemm": [_ptr, _int, _int, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr,
                   _i64],
@@ -57,6 +62,24 @@ _SIGS = {
 _RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64}
 
 EXPORTED = tuple(_SIGS)
+
+# int (*callback)(int op, int k, void* user) of gcg_cg_dist
+CG_DIST_CALLBACK = C.CFUNCTYPE(C.c_int, C.c_int, C.c_int, C.c_void_p)
+
+
+class CgDist(C.Structure):
+    """gcg_cg_dist (include/gcgb200.h)."""
+
+    _fields_ = [
+        ("nghost", C.c_int64),
+        ("nsend", C.c_int64),
+        ("send_idx", C.c_void_p),
+        ("send_buf", C.c_void_p),
+        ("recv_buf", C.c_void_p),
+        ("red_buf", C.c_void_p),
+        ("callback", CG_DIST_CALLBACK),
+        ("user", C.c_void_p),
+    ]
 
 _lib = None
 

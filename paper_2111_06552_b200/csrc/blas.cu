@@ -108,7 +108,29 @@ __global__ void __launch_bounds__(256) col_dots_kernel(long long n, int k,
   }
 }
 
+// out[i*ldo + c] = X[idx[i]*ldx + c]  (halo send packing)
+__global__ void gather_rows_kernel(int nidx, const int* __restrict__ idx, int k,
+                                   const double* __restrict__ X, long long ldx, double* out,
+                                   long long ldo) {
+  const long long tot = (long long)nidx * k;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / k), c = (int)(e % k);
+    out[(long long)i * ldo + c] = X[(long long)idx[i] * ldx + c];
+  }
+}
+
 static int elem_grid(Ctx* c, long long tot) { return grid_for(tot, 256 * 4, 8, c->num_sms); }
+
+int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X, long long ldx,
+                       double* out, long long ldo) {
+  if (nidx <= 0 || k <= 0) return GCG_OK;
+  gather_rows_kernel<<<elem_grid(c, (long long)nidx * k), 256, 0, c->stream>>>(nidx, idx, k, X,
+                                                                              ldx, out, ldo);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
 
 int axpby_launch(Ctx* c, long long n, int k, double alpha, const double* X, long long ldx,
                  double beta, double* Y, long long ldy) {

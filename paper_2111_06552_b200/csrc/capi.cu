@@ -42,10 +42,17 @@ int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, cons
                  long long lda, const double* B, long long ldb, double beta, double* C,
                  long long ldc);
 int symmetrize_launch(Ctx* c, int m, double* A, long long lda);
-int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx, const double* val,
-                    double shift, int k, const double* rhs, long long ldr, double* x,
-                    long long ldx, int max_iters, double rel_tol, int* d_sweeps, int8_t* d_conv,
-                    int8_t* d_frozen, double* d_relres);
+int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
+                    const double* val, double shift, int k, const double* rhs, long long ldr,
+                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
+                    int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist);
+int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X, long long ldx,
+                       double* out, long long ldo);
+int ritz_sums_launch(Ctx* c, long long n, int k, const double* AX, long long ldax,
+                     const double* X, long long ldx, const double* BX, long long ldbx,
+                     const double* lam, int mode, double* sums);
+int ritz_finish_launch(Ctx* c, int k, const double* sums, const double* lam, int mode,
+                       double* out);
 int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
                         double skip_tol, double* Q,
                         long long ldq, double* status);
@@ -365,7 +372,43 @@ int gcg_block_cg(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const i
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
   return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
-                         max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres);
+                         max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres, nullptr);
+}
+
+int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, const double* val, double diag_shift, int64_t k,
+                      const double* rhs, int64_t ldr, double* x, int64_t ldx, int32_t max_iters,
+                      double rel_tol, int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen,
+                      double* d_relres, const gcg_cg_dist* dist) {
+  Ctx* c = CTX(p);
+  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0 || !dist ||
+      !dist->callback || !dist->red_buf)
+    return GCG_ERR_ARG;
+  if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
+  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
+                         max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres, dist);
+}
+
+int gcg_gather_rows(void* p, int64_t nidx, const int32_t* idx, int64_t k, const double* X,
+                    int64_t ldx, double* out, int64_t ldo) {
+  Ctx* c = CTX(p);
+  if (!c || nidx < 0 || k < 0 || ldx < k || ldo < k) return GCG_ERR_ARG;
+  return gather_rows_launch(c, (int)nidx, idx, (int)k, X, ldx, out, ldo);
+}
+
+int gcg_ritz_sums(void* p, int64_t n, int64_t k, const double* AX, int64_t ldax,
+                  const double* X, int64_t ldx, const double* BX, int64_t ldbx,
+                  const double* lam, int mode, double* sums) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || k > 256 || mode < 0 || mode > 2) return GCG_ERR_ARG;
+  return ritz_sums_launch(c, n, (int)k, AX, ldax, X, ldx, BX, ldbx, lam, mode, sums);
+}
+
+int gcg_ritz_finish(void* p, int64_t k, const double* sums, const double* lam, int mode,
+                    double* out) {
+  Ctx* c = CTX(p);
+  if (!c || k < 0 || mode < 0 || mode > 2) return GCG_ERR_ARG;
+  return ritz_finish_launch(c, (int)k, sums, lam, mode, out);
 }
 
 int gcg_syev(void* p, int64_t m, const double* A, int64_t lda, double* w, double* V,

@@ -247,7 +247,7 @@ __global__ void cg_final(int k, CgState s, int* d_sweeps, int8_t* conv, int8_t* 
 int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                    const double* val, double shift, int k, const double* rhs, long long ldr,
                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                   int8_t* d_conv, int8_t* d_frozen, double* d_relres);
+                   int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist);
 
 // The k CG recurrences are independent, so they can run in column chunks (each
 // chunk's sweep count is the same as in the joint run).  GCG_CG_CHUNK=w forces
@@ -258,39 +258,63 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
 int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                     const double* val, double shift, int k, const double* rhs, long long ldr,
                     double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                    int8_t* d_conv, int8_t* d_frozen, double* d_relres) {
+                    int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist) {
   if (k <= 0 || k > 256 || n <= 0) return GCG_ERR_ARG;
   GCG_TRY(cuda_status(cudaMemsetAsync(d_sweeps, 0, sizeof(int), c->stream)));
   static const char* env = getenv("GCG_CG_CHUNK");
   int kc = env ? atoi(env) : k;
-  if (kc < 1 || kc > k) kc = k;
+  if (kc < 1 || kc > k || dist) kc = k;
   for (int c0 = 0; c0 < k; c0 += kc) {
     const int w = (k - c0) < kc ? (k - c0) : kc;
     GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr, x + c0, ldx,
                            max_iters, rel_tol, d_sweeps, d_conv + c0, d_frozen + c0,
-                           d_relres + c0));
+                           d_relres + c0, dist));
   }
+  return GCG_OK;
+}
+
+int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X, long long ldx,
+                       double* out, long long ldo);
+
+// Row-partitioned runs: refresh the ghost rows [n, n + nghost) of a block
+// (ld) from the neighbours — gather the owned rows they need into send_buf,
+// let the host exchange send_buf -> recv_buf, scatter into the ghost rows.
+static int dist_halo(Ctx* c, const gcg_cg_dist* d, long long n, int k, double* X, long long ld) {
+  if (d->nsend > 0) GCG_TRY(gather_rows_launch(c, d->nsend, d->send_idx, k, X, ld, d->send_buf, k));
+  if (d->callback(0, k, d->user) != 0) return GCG_ERR_ARG;
+  if (d->nghost > 0) GCG_TRY(copy_launch(c, d->nghost, k, d->recv_buf, k, X + n * ld, ld));
+  return GCG_OK;
+}
+
+// Combine per-CTA partials into k local column sums, then the global sums
+// (host allreduce into red_buf); the finish kernels read them as 1 partial.
+static int dist_reduce(Ctx* c, const gcg_cg_dist* d, const double* part, int nparts, int k) {
+  GCG_TRY(reduce_partials(c, part, nparts, k, d->red_buf, 1, 0));
+  ++g_launches;
+  if (d->callback(1, k, d->user) != 0) return GCG_ERR_ARG;
   return GCG_OK;
 }
 
 int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                    const double* val, double shift, int k, const double* rhs, long long ldr,
                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                   int8_t* d_conv, int8_t* d_frozen, double* d_relres) {
+                   int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist) {
   const int sgrid = spmm_grid(c, n);
   int ugrid = grid_for(n, 512, 4, c->num_sms);
   long long rpc = (n + ugrid - 1) / ugrid;
   ugrid = (int)((n + rpc - 1) / rpc);
   const int nparts_max = sgrid > ugrid ? sgrid : ugrid;
-  // workspace: R, P, Q (n x k) + partials + state
+  const long long nghost = dist ? dist->nghost : 0;
+  // workspace: R, Q (n x k), P ((n + ghosts) x k) + partials + state
   const size_t vec = (size_t)n * k;
-  const size_t bytes = sizeof(double) * (3 * vec + (size_t)nparts_max * k + 6 * (size_t)k) +
+  const size_t pvec = (size_t)(n + nghost) * k;
+  const size_t bytes = sizeof(double) * (2 * vec + pvec + (size_t)nparts_max * k + 6 * (size_t)k) +
                        sizeof(int) * (4 * (size_t)k + 4) + 256;
   GCG_TRY(ensure(c->cg, bytes));
   double* R = (double*)c->cg.ptr;
-  double* P = R + vec;
-  double* Q = P + vec;
-  double* part = Q + vec;
+  double* Q = R + vec;
+  double* P = Q + vec;
+  double* part = P + pvec;
   double* sd = part + (size_t)nparts_max * k;
   CgState s;
   s.rz = sd;
@@ -313,22 +337,45 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
 
   // r = rhs - op(x) = -(A x) - shift*x + rhs ; ||r0||^2 partials
   int g = 0;
-  GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0, rhs,
-                            ldr, R, k, 2, nullptr, 0, part, &g, nullptr));
-  cg_init_fin<<<k, 128, 0, c->stream>>>(k, part, g, rel_tol, s);
+  if (dist) GCG_TRY(dist_halo(c, dist, n, k, x, ldx));
+  GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0,
+                            rhs, ldr, R, k, 2, nullptr, 0, part, &g, nullptr));
+  const double* red = part;
+  int nred = g;
+  if (dist) {
+    GCG_TRY(dist_reduce(c, dist, part, g, k));
+    red = dist->red_buf;
+    nred = 1;
+  }
+  cg_init_fin<<<k, 128, 0, c->stream>>>(k, red, nred, rel_tol, s);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   GCG_TRY(copy_launch(c, n, k, R, k, P, k));
   const int pgrid = grid_for(n * k, 1024, 8, c->num_sms);
   for (int it = 0; it < max_iters; ++it) {
-    GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0, nullptr,
-                              0, Q, k, 1, P, k, part, &g, s.skip));
-    cg_fin1<<<k, 128, 0, c->stream>>>(k, part, g, s);
+    if (dist) GCG_TRY(dist_halo(c, dist, n, k, P, k));
+    GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0,
+                              nullptr, 0, Q, k, 1, P, k, part, &g, s.skip));
+    red = part;
+    nred = g;
+    if (dist) {
+      GCG_TRY(dist_reduce(c, dist, part, g, k));
+      red = dist->red_buf;
+      nred = 1;
+    }
+    cg_fin1<<<k, 128, 0, c->stream>>>(k, red, nred, s);
     int ps = prof_start(c, PROF_CG_UPDATE, 48.0 * n * k);
     cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, Q, rpc, part, s,
                                                    prof_skip_slot(c, ps));
     prof_stop(c, ps);
-    cg_fin2<<<k, 128, 0, c->stream>>>(k, part, ugrid, s);
+    red = part;
+    nred = ugrid;
+    if (dist) {
+      GCG_TRY(dist_reduce(c, dist, part, ugrid, k));
+      red = dist->red_buf;
+      nred = 1;
+    }
+    cg_fin2<<<k, 128, 0, c->stream>>>(k, red, nred, s);
     ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
     cg_pupdate_kernel<<<pgrid, 256, 0, c->stream>>>(n, k, R, P, s, prof_skip_slot(c, ps));
     prof_stop(c, ps);

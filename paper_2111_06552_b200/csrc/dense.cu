@@ -698,4 +698,38 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
   return GCG_OK;
 }
 
+// split form for row-partitioned runs: local column sums [4][k] ...
+int ritz_sums_launch(Ctx* c, long long n, int k, const double* AX, long long ldax,
+                     const double* X, long long ldx, const double* BX, long long ldbx,
+                     const double* lam, int mode, double* sums) {
+  if (k <= 0) return GCG_OK;
+  if (k > 256) return GCG_ERR_ARG;
+  if (n <= 0) {
+    cudaMemsetAsync(sums, 0, sizeof(double) * 4 * k, c->stream);
+    return GCG_OK;
+  }
+  int grid = grid_for(n, 1024, 4, c->num_sms);
+  long long rpc = (n + grid - 1) / grid;
+  grid = (int)((n + rpc - 1) / rpc);
+  GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * 4 * k));
+  double* part = (double*)c->partials.ptr;
+  ritz_partials_kernel<<<grid, 256, 0, c->stream>>>(n, k, AX, ldax, X, ldx, BX, ldbx, lam, mode,
+                                                     rpc, part);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(reduce_partials(c, part, grid, 4 * k, sums, 1, 0));
+  ++g_launches;
+  return GCG_OK;
+}
+
+// ... and the residuals from (globally reduced) sums
+int ritz_finish_launch(Ctx* c, int k, const double* sums, const double* lam, int mode,
+                       double* out) {
+  if (k <= 0) return GCG_OK;
+  ritz_finish_kernel<<<1, 256, 0, c->stream>>>(k, 1, sums, lam, mode, out);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
 }  // namespace gcg

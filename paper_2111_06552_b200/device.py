@@ -265,6 +265,33 @@ def ritz_residuals(ctx, AX, X, BX, lam, mode, out):
     return out
 
 
+def gather_rows(ctx, idx, X, out):
+    """out[i, :] = X[idx[i], :] (idx int32 on device)."""
+    k = X.shape[1]
+    _lib.call("gcg_gather_rows", ctx.h, idx.shape[0], _p(idx), k, _p(X), _ld(X), _p(out), _ld(out))
+    return out
+
+
+def ritz_sums(ctx, AX, X, BX, lam, mode, sums):
+    n, k = X.shape
+    _lib.call("gcg_ritz_sums", ctx.h, n, k, _p(AX), _ld(AX), _p(X), _ld(X), _p(BX), _ld(BX),
+              _p(lam), int(mode), _p(sums))
+    return sums
+
+
+def ritz_finish(ctx, sums, lam, mode, out):
+    _lib.call("gcg_ritz_finish", ctx.h, out.shape[0], _p(sums), _p(lam), int(mode), _p(out))
+    return out
+
+
+def block_cg_dist(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres,
+                  dist):
+    n, k = rhs.shape
+    _lib.call("gcg_block_cg_dist", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(vals),
+              float(shift), k, _p(rhs), _ld(rhs), _p(x), _ld(x), int(max_iters), float(rel_tol),
+              _p(sweeps), _p(conv), _p(frozen), _p(relres), C.byref(dist))
+
+
 def block_cg(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
     n, k = x.shape
     _lib.call("gcg_block_cg", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(vals), float(shift), k,

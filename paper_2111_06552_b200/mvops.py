@@ -1,0 +1,88 @@
+"""Multivector operations of one solve: single-GPU pass-through or row-partitioned.
+
+The solver, the B-orthogonalisation and block CG call these instead of the raw
+C-ABI wrappers, so the same control flow runs on one GPU or on a row-partitioned
+multi-GPU problem:
+
+* SpMM inputs are local row blocks whose storage continues with `nghost` ghost
+  rows; `spmm` first refreshes the ghost rows from the neighbours (halo
+  exchange), then runs the local CSR (ghost columns index rows >= nloc);
+* Gram blocks and column dots are local partial sums followed by an ordered
+  all-gather sum (bit-identical on every rank, deterministic run to run — the
+  paper's MPI_Allreduce of SUBMAT);
+* the small dense algebra (RR, SVQB, momentum) is replicated; the RR
+  eigenvectors are broadcast from rank 0 so every replica takes the same
+  decisions;
+* block CG runs its sweeps in the library and calls back for the halo and the
+  two column-sum reductions per sweep (gcg_block_cg_dist).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import device as D
+from .cg import CgReport
+
+__all__ = ["LocalOps"]
+
+
+class LocalOps:
+    """One GPU, whole problem: thin pass-through to the C ABI."""
+
+    distributed = False
+    rank = 0
+    size = 1
+
+    def __init__(self, dev, prob):
+        self.dev = dev
+        self.prob = prob
+        self.nloc = prob.n          # owned rows
+        self.nghost = 0
+        self.n_global = prob.n
+        self.row0 = 0
+
+    # -- allocation -----------------------------------------------------------
+    def vec(self, k, zero=False):
+        """n_local x k block whose storage has room for the ghost rows (SpMM input)."""
+        buf = self.dev.zeros(self.nloc + self.nghost, k) if zero else \
+            self.dev.empty(self.nloc + self.nghost, k)
+        return buf[: self.nloc]
+
+    # -- long-vector ops --------------------------------------------------------
+    def spmm(self, op, X, Y, **kw):
+        return D.spmm(self.dev, op, X, Y, **kw)
+
+    def apply(self, op, X):
+        out = self.dev.empty(X.shape[0], X.shape[1])
+        return self.spmm(op, X, out)
+
+    def gram(self, X, Y, G, **kw):
+        return D.gram(self.dev, X, Y, G, **kw)
+
+    def col_dots(self, X, Y, out):
+        return D.col_dots(self.dev, X, Y, out)
+
+    def residuals(self, AX, X, BX, lam, mode, out):
+        return D.ritz_residuals(self.dev, AX, X, BX, lam, mode, out)
+
+    def block_cg(self, vals, shift, rhs, x, max_iters, rel_tol):
+        k = rhs.shape[1]
+        sweeps = self.dev.zeros(1, dtype=torch.int32)
+        conv = self.dev.zeros(k, dtype=torch.int8)
+        frozen = self.dev.zeros(k, dtype=torch.int8)
+        relres = self.dev.zeros(k)
+        self._cg(vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres)
+        return CgReport(sweeps, conv, frozen, relres)
+
+    def _cg(self, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
+        D.block_cg(self.dev, self.prob.A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv,
+                   frozen, relres)
+
+    # -- replicated small data ------------------------------------------------
+    def broadcast(self, t):
+        return t
+
+    def host_rows(self, X):
+        """Local rows of a device block as a host array (F-order)."""
+        return X.t().contiguous().cpu().numpy().T

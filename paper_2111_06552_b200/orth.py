@@ -19,6 +19,10 @@ When the target columns sit right after the basis in the same arena (always
 the case inside the recursion and for W against [X | P]), the squared norms
 ride along in the Gram as the diagonal of its bottom block, so one pass over
 the data yields both — the fused reduction the reference counts as one.
+
+The first argument is an ops object (mvops.LocalOps / distributed.DistOps) or
+a plain device Context; in a row-partitioned run every "reduction" is one
+ordered all-gather sum, exactly the unit the reference counts.
 """
 
 from __future__ import annotations
@@ -27,6 +31,7 @@ from dataclasses import dataclass, field
 
 from . import device as D
 from .errors import AllDependent, InvalidRange, InvalidShape
+from .mvops import LocalOps
 
 __all__ = ["OrthConfig", "OrthOutcome", "recursive_orth_svd", "orth_against"]
 
@@ -51,6 +56,17 @@ class OrthOutcome:
     reduction_count: int = 0
 
 
+class _NoProblem:
+    B = None
+    n = None
+
+
+def _as_ops(obj):
+    if isinstance(obj, LocalOps):
+        return obj
+    return LocalOps(obj, _NoProblem())  # a bare Context: single-GPU ops, no operator needed
+
+
 def _adjacent(left, right):
     """True when `right` starts exactly where `left` ends in the same row-major storage."""
     if left.shape[1] == 0 or right.shape[1] == 0:
@@ -69,8 +85,9 @@ def _span(left, width):
 class _State:
     """Per-call bookkeeping (orth.py:72-108)."""
 
-    def __init__(self, dev, x, b, cfg, start, end):
-        self.dev = dev
+    def __init__(self, ops, x, b, cfg, start, end):
+        self.ops = ops
+        self.dev = ops.dev
         self.x = x
         self.b = b
         self.cfg = cfg
@@ -79,13 +96,14 @@ class _State:
         self.reductions = 0
         self.replaced = []
         self.leaf_width = 16
-        self.status = dev.empty(4)
+        self.status = self.dev.empty(4)
 
     def bdot(self, y):
-        if self.b is None:
-            return y
-        out = self.dev.empty(y.shape[0], y.shape[1])
-        return D.spmm(self.dev, self.b, y, out)
+        return y if self.b is None else self.ops.apply(self.b, y)
+
+    def read_status(self, count):
+        """Host copy of the decision record (identical on every rank)."""
+        return self.ops.broadcast(self.status)[:count].tolist()
 
     def pull_rear(self, slot):
         self.replaced.append(slot)
@@ -100,7 +118,7 @@ class _State:
 
 def _deflate_against(st, basis, lo, hi):
     """Repeat-until deflation of x[:, lo:hi] against a B-orthonormal basis (orth.py:124-152)."""
-    cfg, dev = st.cfg, st.dev
+    cfg, dev, ops = st.cfg, st.dev, st.ops
     passes = 0
     while passes < cfg.max_reorth_passes:
         hi = min(hi, st.active_end)
@@ -112,18 +130,18 @@ def _deflate_against(st, basis, lo, hi):
         bt = st.bdot(target)
         if _adjacent(basis, target):
             g = dev.empty(K + w, w)
-            D.gram(dev, _span(basis, K + w), bt, g)
+            ops.gram(_span(basis, K + w), bt, g)
             coef, dnew = g[:K], g[K:].diagonal()
         else:
             coef = dev.empty(K, w)
-            D.gram(dev, basis, bt, coef)
+            ops.gram(basis, bt, coef)
             dnew = dev.empty(w)
-            D.col_dots(dev, target, bt, dnew)
+            ops.col_dots(target, bt, dnew)
         st.reductions += 1
         passes += 1
         D.lincomb(dev, basis, coef, target, alpha=-1.0, beta=1.0)
         D.deflate_status(dev, coef, dnew, _DGKS_RATIO, st.status)
-        rmax, risky = st.status[:2].tolist()
+        rmax, risky = st.read_status(2)
         if rmax <= cfg.reorth_tol:
             return passes
         if not risky:
@@ -133,7 +151,7 @@ def _deflate_against(st, basis, lo, hi):
 
 def _leaf_svqb(st, lo, hi):
     """Orthonormalise x[:, lo:hi] by repeated scaled Gram factorisations (orth.py:155-188)."""
-    cfg, dev = st.cfg, st.dev
+    cfg, dev, ops = st.cfg, st.dev, st.ops
     passes = 0
     while True:
         hi = min(hi, st.active_end)
@@ -142,14 +160,15 @@ def _leaf_svqb(st, lo, hi):
         w = hi - lo
         block = st.x[:, lo:hi]
         g = dev.empty(w, w)
-        D.gram(dev, block, st.bdot(block), g)
+        ops.gram(block, st.bdot(block), g)
         st.reductions += 1
         passes += 1
         q = dev.empty(w, w)
         D.svqb_prepare(dev, g, cfg.dependence_tol, q, st.status, skip_tol=cfg.reorth_tol)
-        defect, nbad, _ = st.status[:3].tolist()
+        defect, nbad, _ = st.read_status(3)
         if defect <= cfg.reorth_tol:
             return
+        ops.broadcast(q)
         bad = int(nbad)
         kept = w - bad
         if kept > 0:
@@ -183,8 +202,9 @@ def _recurse_svd(st, lo, hi):
     _recurse_svd(st, mid, hi)
 
 
-def recursive_orth_svd(dev, x, s=None, e=None, b=None, cfg=None):
+def recursive_orth_svd(ops, x, s=None, e=None, b=None, cfg=None):
     """B-orthonormalise columns s..e (1-based, inclusive) of device block ``x`` in place."""
+    ops = _as_ops(ops)
     cfg = cfg if cfg is not None else OrthConfig()
     ncols = x.shape[1]
     s = 1 if s is None else s
@@ -192,7 +212,7 @@ def recursive_orth_svd(dev, x, s=None, e=None, b=None, cfg=None):
     if not (1 <= s <= e <= ncols):
         raise InvalidRange(f"column range {s}..{e} invalid for width {ncols}")
     lo, hi = s - 1, e
-    st = _State(dev, x, b, cfg, lo, hi)
+    st = _State(ops, x, b, cfg, lo, hi)
     st.leaf_width = cfg.svd_leaf if cfg.svd_leaf is not None else min(hi - lo, 16)
     if st.leaf_width < 1:
         raise InvalidShape(f"svd_leaf must be >= 1, got {st.leaf_width}")
@@ -203,23 +223,24 @@ def recursive_orth_svd(dev, x, s=None, e=None, b=None, cfg=None):
     return OrthOutcome(kept, st.replaced, st.reductions)
 
 
-def orth_against(dev, x, basis, b=None, cfg=None):
+def orth_against(ops, x, basis, b=None, cfg=None):
     """Deflate ``x`` against ``basis``, Alg. 3, then deflate + SVQB the kept block (orth.py:339-372)."""
+    ops = _as_ops(ops)
     cfg = cfg if cfg is not None else OrthConfig()
     if x.shape[1] == 0:
         return OrthOutcome(0, [], 0)
-    st = _State(dev, x, b, cfg, 0, x.shape[1])
+    st = _State(ops, x, b, cfg, 0, x.shape[1])
     have_basis = basis is not None and basis.shape[1] > 0
     if have_basis:
         if basis.shape[0] != x.shape[0]:
             raise InvalidShape(f"basis dim {basis.shape[0]} != block dim {x.shape[0]}")
         _deflate_against(st, basis, 0, x.shape[1])
-    inner = recursive_orth_svd(dev, x, 1, x.shape[1], b=b, cfg=cfg)
+    inner = recursive_orth_svd(ops, x, 1, x.shape[1], b=b, cfg=cfg)
     kept = inner.num_kept
     replaced = list(inner.replaced_indices)
     extra = 0
     if have_basis and kept > 0:
-        post = _State(dev, x, b, cfg, 0, kept)
+        post = _State(ops, x, b, cfg, 0, kept)
         _deflate_against(post, basis, 0, kept)
         _leaf_svqb(post, 0, kept)
         kept = post.active_end

@@ -7,6 +7,11 @@ same report.  The multivector arena V = [X | P | W] (n x (sx + 2 bs)) lives in
 HBM, row-major; the host only ever sees m x m-sized decisions (eigenvalues,
 residual norms, dependence counts) read back as a handful of doubles.
 
+The same driver runs row-partitioned over several GPUs (``gcg_solve_distributed``):
+the multivector operations go through an ops object (mvops.LocalOps on one GPU,
+distributed.DistOps across ranks) that adds halo exchanges and ordered
+reductions; every host-side decision is taken on bit-identical replicated data.
+
 Two parity switches that the reference does not have:
 ``init`` ("uniform" = reference mv_set_random, "normal" = BASELINE N(0,1)) and
 ``residual`` ("reference" = solver._rel_residual, "relative" = north-star
@@ -23,9 +28,9 @@ import numpy as np
 import torch
 
 from . import device as D
-from .cg import block_cg
 from .dense import sym_eig_full
 from .errors import AllDependent, InvalidShape
+from .mvops import LocalOps
 from .operators import DeviceProblem, as_device_problem
 from .orth import OrthConfig, orth_against, recursive_orth_svd
 
@@ -34,6 +39,7 @@ __all__ = [
     "IterationRecord",
     "SolverReport",
     "gcg_solve",
+    "gcg_solve_ops",
     "select_shift",
     "moving_memory_budget",
 ]
@@ -41,6 +47,7 @@ __all__ = [
 BACKEND_NAME = "sm100"
 _TIMING_KEYS = ("t_step2", "t_step3", "t_step4", "t_step5", "t_step6")
 _RESIDUAL_MODES = {"reference": None, "relative": 2}
+_RNG_CHUNK_ROWS = 1 << 16
 
 
 @dataclass
@@ -97,6 +104,7 @@ class SolverReport:
     max_projection_dim: int
     total_reductions: int
     backend: str
+    row_range: tuple = (0, 0)      # rows of `eigenvectors` (all of them on one GPU)
 
 
 def moving_memory_budget(size_x, block_size):
@@ -147,39 +155,44 @@ class _Timer:
 class _Solve:
     """State of one device solve (the body of solver.py:226-486)."""
 
-    def __init__(self, dev, prob, cfg):
-        self.dev = dev
-        self.prob = prob
+    def __init__(self, ops, cfg):
+        self.ops = ops
+        self.dev = ops.dev
+        self.prob = ops.prob
         self.cfg = cfg
-        self.n = prob.n
-        self.generalized = prob.B is not None
+        self.generalized = self.prob.B is not None
         mode = _RESIDUAL_MODES.get(cfg.residual, "bad")
         if mode == "bad":
             raise InvalidShape(f"unknown residual kind {cfg.residual!r}")
         self.res_mode = mode if mode is not None else (1 if self.generalized else 0)
-        self.scalar = dev.empty(8)
+        self.scalar = self.dev.empty(8)
 
     # -- small helpers -------------------------------------------------------
     def set_random(self, block, seed):
-        """multivec.mv_set_random (multivec.py:46-50) drawn on host, uploaded (parity)."""
+        """multivec.mv_set_random (multivec.py:46-50) on host, uploaded (parity).
+
+        The global n x k block is drawn in row order (row chunks consume the
+        PCG64 stream exactly like one call); each rank keeps its own rows.
+        """
+        ops = self.ops
         rng = np.random.Generator(np.random.PCG64(seed))
-        shape = tuple(block.shape)
-        if self.cfg.init == "normal":
-            host = rng.standard_normal(shape)
-        else:
-            host = rng.uniform(-1.0, 1.0, size=shape)
-        src = torch.from_numpy(host).to(self.dev.device)
-        D.copy(self.dev, src, block)
+        k = block.shape[1]
+        r0, r1 = ops.row0, ops.row0 + ops.nloc
+        for c0 in range(0, min(r1, ops.n_global), _RNG_CHUNK_ROWS):
+            c1 = min(c0 + _RNG_CHUNK_ROWS, ops.n_global)
+            shape = (c1 - c0, k)
+            host = rng.standard_normal(shape) if self.cfg.init == "normal" else \
+                rng.uniform(-1.0, 1.0, size=shape)
+            lo, hi = max(c0, r0), min(c1, r1)
+            if lo < hi:
+                src = torch.from_numpy(host[lo - c0:hi - c0]).to(self.dev.device)
+                D.copy(self.dev, src, block[lo - r0:hi - r0])
 
     def apply_a(self, x):
-        out = self.dev.empty(x.shape[0], x.shape[1])
-        return D.spmm(self.dev, self.prob.A, x, out)
+        return self.ops.apply(self.prob.A, x)
 
     def apply_b(self, x):
-        if self.prob.B is None:
-            return x
-        out = self.dev.empty(x.shape[0], x.shape[1])
-        return D.spmm(self.dev, self.prob.B, x, out)
+        return x if self.prob.B is None else self.ops.apply(self.prob.B, x)
 
     def residuals(self, x, lam_dev):
         """Per-column relative residuals of Ritz pairs (solver.py:129-141), device -> host."""
@@ -191,11 +204,11 @@ class _Solve:
             ax = self.apply_a(xc)
             bx = self.apply_b(xc)
             r = self.dev.empty(e - s)
-            D.ritz_residuals(self.dev, ax, xc, bx, lam_dev[s:e], self.res_mode, r)
-            out[s:e] = r.cpu().numpy()
+            self.ops.residuals(ax, xc, bx, lam_dev[s:e], self.res_mode, r)
+            out[s:e] = self.ops.broadcast(r).cpu().numpy()
         return out
 
-    def count_converged(self, x_new, lam_new_dev, lam_new, limit, chunk, tol):
+    def count_converged(self, x_new, lam_new_dev, limit, chunk, tol):
         """solver._count_converged (solver.py:144-164): prefix of Ritz pairs below tol."""
         count = 0
         for start in range(0, limit, chunk):
@@ -239,6 +252,8 @@ class _Solve:
         D.dgemm(dev, pt, pt, g, ta=True)
         D.symmetrize(dev, g)
         dec = sym_eig_full(dev, g)
+        self.ops.broadcast(dec.values)
+        self.ops.broadcast(dec.vectors)
         D.count_le(dev, dec.values, rel, self.scalar)
         bad = int(self.scalar[0].item())
         if bad >= gw:
@@ -249,6 +264,17 @@ class _Solve:
         q = dev.empty(pt.shape[0], kept)
         D.dgemm(dev, pt, scaled, q)
         return q, kept
+
+    def hstack(self, parts):
+        """Contiguous copy of column blocks (the reference's np.hstack, solver.py:337,356,401,450)."""
+        parts = [p for p in parts if p.shape[1] > 0]
+        width = sum(p.shape[1] for p in parts)
+        out = self.ops.vec(width)
+        c = 0
+        for p in parts:
+            D.copy(self.dev, p, out[:, c:c + p.shape[1]])
+            c += p.shape[1]
+        return out
 
 
 def gcg_solve(a, b=None, config=None, *, x0=None):
@@ -265,8 +291,15 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         prob = a
     else:
         prob = as_device_problem(dev, a, b, validate=cfg.validate)
-    S = _Solve(dev, prob, cfg)
-    n = prob.n
+    return gcg_solve_ops(LocalOps(dev, prob), cfg, x0=x0)
+
+
+def gcg_solve_ops(ops, cfg, x0=None):
+    """The GCG iteration (solver.py:226-486) over an ops object (one GPU or one rank)."""
+    S = _Solve(ops, cfg)
+    dev, prob = ops.dev, ops.prob
+    n = ops.n_global
+    nloc = ops.nloc
     ne = int(cfg.num_eigen)
     if not (1 <= ne <= n):
         raise InvalidShape(f"num_eigen must be in 1..{n}, got {ne}")
@@ -283,22 +316,22 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
     det = cfg.deterministic
     Bop = prob.B
 
-    v = dev.zeros(n, sx + 2 * bs)
+    v = ops.vec(sx + 2 * bs, zero=True)
     lam = np.zeros(sx + 2 * bs)
     if x0 is None:
         S.set_random(v[:, :sx], cfg.seed)
     else:
-        if tuple(x0.shape) != (n, sx):
-            raise InvalidShape(f"x0 shape {tuple(x0.shape)} != ({n}, {sx})")
+        if tuple(x0.shape) != (nloc, sx):
+            raise InvalidShape(f"x0 shape {tuple(x0.shape)} != ({nloc}, {sx})")
         src = x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(np.asarray(x0))
         if src.device != dev.device:
             src = src.to(dev.device, non_blocking=True)
         D.copy(dev, src.contiguous(), v[:, :sx])
-    out = recursive_orth_svd(dev, v, 1, sx, b=Bop, cfg=ocfg)
+    out = recursive_orth_svd(ops, v, 1, sx, b=Bop, cfg=ocfg)
     total_red = out.reduction_count
     if out.num_kept < sx:
         S.set_random(v[:, out.num_kept:sx], cfg.seed + 9973)
-        out = recursive_orth_svd(dev, v, 1, sx, b=Bop, cfg=ocfg)
+        out = recursive_orth_svd(ops, v, 1, sx, b=Bop, cfg=ocfg)
         total_red += out.reduction_count
         if out.num_kept < sx:
             raise AllDependent("could not build a full-rank starting block")
@@ -326,36 +359,38 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         abar = dev.empty(m, m)
         if abar_prev is None:
             ab = S.apply_a(basis)
-            D.gram(dev, basis, ab, abar)
+            ops.gram(basis, ab, abar)
             D.symmetrize(dev, abar)
         else:
             cross = None
             if nw:
                 aw = S.apply_a(v[:, sx + np_:sx + np_ + nw])
                 cross = dev.empty(m, nw)
-                D.gram(dev, basis, aw, cross)
+                ops.gram(basis, aw, cross)
             lam_x = torch.from_numpy(lam[locked:sx].copy()).to(dev.device)
             D.abar_assemble(dev, d, lam_x, p_coupling if np_ else None, cross, abar)
         abar_defect = None
         if cfg.cross_check_abar and abar_prev is not None:
             naive = dev.empty(m, m)
-            D.gram(dev, basis, S.apply_a(basis), naive)
+            ops.gram(basis, S.apply_a(basis), naive)
             D.symmetrize(dev, naive)
             D.max_abs_diff(dev, abar, naive, S.scalar)
             abar_defect = float(S.scalar[0].item())
         timer.lap("t_step3")
 
         full = sym_eig_full(dev, abar)
+        ops.broadcast(full.values)      # every replica continues from rank 0's RR solution
+        ops.broadcast(full.vectors)
         lam_new_dev = full.values[:d]
         coeffs = full.vectors[:, :d]
-        x_new = dev.empty(n, d)
+        x_new = ops.vec(d)
         D.lincomb(dev, basis, coeffs, x_new)
         lam_new = lam_new_dev.cpu().numpy()
         timer.lap("t_step3")
 
         stored = sum(len(vv) for vv in store_vals)
         limit = max(0, min(sx - locked, ne - stored - locked))
-        newly, first_res = S.count_converged(x_new, lam_new_dev, lam_new, limit, bs, cfg.tol)
+        newly, first_res = S.count_converged(x_new, lam_new_dev, limit, bs, cfg.tol)
         c = locked + newly
         total_locked = stored + c
         timer.lap("t_step4")
@@ -376,9 +411,9 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         if cfg.moving and c > 0 and (c >= 2 * bs or c >= sx):
             # window slide (solver.py:325-363)
             lam_all = full.values.cpu().numpy()
-            x_all = dev.empty(n, m)
+            x_all = dev.empty(nloc, m)
             D.lincomb(dev, basis, full.vectors, x_all)
-            blk = dev.empty(n, locked + newly)
+            blk = dev.empty(nloc, locked + newly)
             if locked:
                 D.copy(dev, v[:, :locked], blk[:, :locked])
             if newly:
@@ -399,8 +434,8 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
                 add = min(3 * bs, n - stored) - sx
                 if add > 0:
                     S.set_random(v[:, sx:sx + add], cfg.seed + 104729 * it)
-                    defl = _hstack(dev, store_x + [v[:, :sx]])
-                    ro = orth_against(dev, v[:, sx:sx + add], defl, b=Bop, cfg=ocfg)
+                    defl = S.hstack(store_x + [v[:, :sx]])
+                    ro = orth_against(ops, v[:, sx:sx + add], defl, b=Bop, cfg=ocfg)
                     iter_red += ro.reduction_count
                     sx += ro.num_kept
                 refilled = True
@@ -420,7 +455,7 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
                 if phat is None:
                     p_coupling = None
                 else:
-                    p_new = dev.empty(n, phat.shape[1])
+                    p_new = dev.empty(nloc, phat.shape[1])
                     D.lincomb(dev, basis, phat, p_new)
                     ap = dev.empty(m, phat.shape[1])
                     D.dgemm(dev, abar, phat, ap)
@@ -438,24 +473,24 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
             x_act = v[:, locked:locked + bs_eff]
             w_region = v[:, sx + np_:sx + np_ + bs_eff]
             scale = torch.from_numpy(lam[locked:locked + bs_eff] - theta).to(dev.device)
-            rhs = dev.empty(n, bs_eff)
+            rhs = dev.empty(nloc, bs_eff)
             if Bop is not None:
-                D.spmm(dev, Bop, x_act, rhs)
+                ops.spmm(Bop, x_act, rhs)
             else:
                 D.copy(dev, x_act, rhs)
             D.col_scale(dev, scale, rhs)
             D.copy(dev, x_act, w_region)
-            _, cg_rep = block_cg(dev, prob, theta, rhs, w_region,
-                                 max_iters=cfg.cg_max_iters, rel_tol=cfg.cg_rel_tol)
+            vals, shift = prob.shifted(theta)
+            cg_rep = ops.block_cg(vals, shift, rhs, w_region, cfg.cg_max_iters, cfg.cg_rel_tol)
             timer.lap("t_step6")
 
             # STEP 2: W against [store, X, P] (solver.py:398-420)
             if store_x:
-                defl = _hstack(dev, store_x + [v[:, :sx + np_]])
+                defl = S.hstack(store_x + [v[:, :sx + np_]])
             else:
                 defl = v[:, :sx + np_]
             try:
-                w_out = orth_against(dev, w_region, defl, b=Bop, cfg=ocfg)
+                w_out = orth_against(ops, w_region, defl, b=Bop, cfg=ocfg)
                 nw = w_out.num_kept
                 iter_red += w_out.reduction_count
             except AllDependent:
@@ -463,7 +498,7 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
             if nw == 0:
                 S.set_random(w_region, cfg.seed + 7919 * it)
                 try:
-                    w_out = orth_against(dev, w_region, defl, b=Bop, cfg=ocfg)
+                    w_out = orth_against(ops, w_region, defl, b=Bop, cfg=ocfg)
                     nw = w_out.num_kept
                     iter_red += w_out.reduction_count
                 except AllDependent:
@@ -476,7 +511,7 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         if cfg.instrument_orth:
             fb = v[:, :sx + np_ + nw]
             g = dev.empty(fb.shape[1], fb.shape[1])
-            D.gram(dev, fb, S.apply_b(fb), g)
+            ops.gram(fb, S.apply_b(fb), g)
             D.max_abs_diff(dev, g, None, S.scalar)
             basis_defect = float(S.scalar[0].item())
 
@@ -502,7 +537,7 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
             all_vals = np.concatenate([all_vals, lam[locked:locked + extra]])
         take = min(ne, all_vals.shape[0])
         values = all_vals[:take].copy()
-        vectors = _hstack(dev, parts)[:, :take]
+        vectors = S.hstack(parts)[:, :take]
     else:
         n_conv = locked
         values = lam[:ne].copy()
@@ -513,11 +548,8 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         vd = torch.from_numpy(values).to(dev.device)
         residuals = S.residuals(vectors, vd)
 
-    if cfg.return_device:
-        evecs = vectors
-    else:
-        # one on-device layout transpose, then a single D2H of an F-order block
-        evecs = vectors.t().contiguous().cpu().numpy().T
+    # one on-device layout transpose, then a single D2H of an F-order block
+    evecs = vectors if cfg.return_device else ops.host_rows(vectors)
 
     return SolverReport(
         status=status,
@@ -531,17 +563,5 @@ def gcg_solve(a, b=None, config=None, *, x0=None):
         max_projection_dim=max_m,
         total_reductions=total_red,
         backend=BACKEND_NAME,
+        row_range=(ops.row0, ops.row0 + nloc),
     )
-
-
-def _hstack(dev, parts):
-    """Contiguous copy of column blocks (the reference's np.hstack, solver.py:337,356,401,450)."""
-    parts = [p for p in parts if p.shape[1] > 0]
-    n = parts[0].shape[0] if parts else 0
-    width = sum(p.shape[1] for p in parts)
-    out = dev.empty(n, width)
-    c = 0
-    for p in parts:
-        D.copy(dev, p, out[:, c:c + p.shape[1]])
-        c += p.shape[1]
-    return out
