@@ -201,7 +201,7 @@ def run_reference_arm(args, pr, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE generator, seeded N(0,1) initial block)",
         "config": {"workload": pr.name, "n": pr.a.shape[0], "nnz": int(pr.a.nnz),
                    "nev": pr.num_eigen, "tol": pr.tol},
@@ -231,23 +231,45 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # one GPU per rank; GCG_BENCH_BACKEND=gloo lets several ranks share a GPU (testing only)
+    backend = os.environ.get("GCG_BENCH_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     from paper_2111_06552_b200 import SolverConfig, _lib, gcg_solve
     from paper_2111_06552_b200 import device as D
     from paper_2111_06552_b200.operators import as_device_problem
+    from paper_2111_06552_b200.solver import gcg_solve_ops
 
     ctx = D.default_context()
     kw = solver_kwargs(pr)
     x0_host = initial_block(pr)
-    prob = as_device_problem(ctx, pr.a, pr.b, validate=False)
-    x0_dev = torch.from_numpy(x0_host).to(ctx.device)
     cfg = SolverConfig(**kw, init="normal", residual="relative", validate=False, return_device=True,
                        collect_history=True)
+    plane = int(np.prod(pr.grid[1:])) if len(pr.grid) > 1 else 1
+    if world > 1:
+        # row-partitioned solve: z-slab row blocks, halo exchange + NCCL reductions
+        from paper_2111_06552_b200.distributed import (Comm, DistOps, DistProblem, local_part,
+                                                       row_bounds)
+
+        comm = Comm()
+        bounds = row_bounds(pr.a.shape[0], world, plane)
+        part = local_part(pr.a, pr.b, bounds, rank)
+        ops = DistOps(ctx, DistProblem(ctx, part, comm, pr.a.shape[0]))
+        x0_local = x0_host[part.r0:part.r0 + part.nloc]
+    else:
+        from paper_2111_06552_b200.mvops import LocalOps
+
+        ops = LocalOps(ctx, as_device_problem(ctx, pr.a, pr.b, validate=False))
+        x0_local = x0_host
+    x0_dev = torch.from_numpy(np.ascontiguousarray(x0_local)).to(ctx.device)
 
     def step():
-        return gcg_solve(prob, None, cfg, x0=x0_dev)
+        return gcg_solve_ops(ops, cfg, x0=x0_dev)
 
     for _ in range(args.warmup):
         rep = step()
@@ -257,7 +279,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
     iters = []
-    with ClockSampler(local) as clk, D.KernelProfile(ctx) as prof:
+    with ClockSampler(dev_index) as clk, D.KernelProfile(ctx) as prof:
         ev0.record(ctx.stream)
         for _ in range(args.steps):
             rep = step()
@@ -280,17 +302,26 @@ def main():
         import scipy.sparse
 
         a_pinned = scipy.sparse.csr_matrix(pr.a)
-        x0_pin = torch.from_numpy(x0_host).pin_memory()
+        x0_pin = torch.from_numpy(np.ascontiguousarray(x0_local)).pin_memory()
         cfg_h = SolverConfig(**kw, init="normal", residual="relative", validate=False)
-        h2d = (a_pinned.data.nbytes + a_pinned.indices.astype(np.int32).nbytes
-               + a_pinned.indptr.astype(np.int32).nbytes + x0_pin.numel() * 8)
+        rows = slice(ops.row0, ops.row0 + ops.nloc)
+        nnz_local = int(a_pinned.indptr[rows.stop] - a_pinned.indptr[rows.start])
+        h2d = 12 * nnz_local + 4 * (ops.nloc + 1) + x0_pin.numel() * 8
+        if pr.b is not None:
+            h2d += 8 * nnz_local
         torch.cuda.synchronize()
         barrier()
         te = []
         for _ in range(max(1, args.steps)):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rh = gcg_solve(a_pinned, pr.b, cfg_h, x0=x0_pin)
+            if world > 1:
+                from paper_2111_06552_b200.distributed import gcg_solve_distributed
+
+                rh = gcg_solve_distributed(a_pinned, pr.b, cfg_h, comm=comm, plane=plane,
+                                           x0=x0_pin)
+            else:
+                rh = gcg_solve(a_pinned, pr.b, cfg_h, x0=x0_pin)
             torch.cuda.synchronize()
             te.append(time.perf_counter() - t0)
         d2h = rh.eigenvectors.nbytes + rh.eigenvalues.nbytes + rh.residuals.nbytes
@@ -336,11 +367,12 @@ def main():
         line = {
             "metric": METRIC, "value": t_solve, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE generator, seeded N(0,1) initial block)",
             "config": {"workload": pr.name, "n": pr.a.shape[0], "nnz": int(pr.a.nnz),
                        "nev": pr.num_eigen, "tol": pr.tol, "criterion": "north-star relative",
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": f"row-partition x{world} (z-slabs, halo + reductions)"
+                       if world > 1 else "single",
                        "l2": "working set > 126 MB L2 (V arena 0.42 GB + CG blocks), no flush"},
             "iterations": iters[-1], "gcg_iters_per_s": iters[-1] / t_solve,
             "max_residual": float(rep.residuals.max()),
