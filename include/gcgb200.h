@@ -153,6 +153,10 @@ int gcg_block_cg_dist(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
                       double rel_tol, int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen,
                       double* d_relres, const gcg_cg_dist* dist);
 
+/* FP64 peak probe (roofline denominator): mode 1 = DMMA.8x8x4 chains, 0 = DFMA chains;
+ * *flops_per_launch receives the flop count of the launch (time it with events). */
+int gcg_fp64_peak(void* ctx, int mode, int32_t iters, double* flops_per_launch, double* sink);
+
 /* out[i, :] = X[idx[i], :]  (row gather, k columns; halo send packing) */
 int gcg_gather_rows(void* ctx, int64_t nidx, const int32_t* idx, int64_t k, const double* X,
                     int64_t ldx, double* out, int64_t ldo);

@@ -45,6 +45,7 @@ _SIGS = {
     "gcg_block_cg_dist": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64,
                           _i32, _dbl, _ptr, _ptr, _ptr, _ptr, _ptr],
     "gcg_gather_rows": [_ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64],
+    "gcg_fp64_peak": [_ptr, _int, _i32, C.POINTER(C.c_double), _ptr],
     "gcg_ritz_sums": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
     "gcg_ritz_finish": [_ptr, _i64, _ptr, _ptr, _int, _ptr],
     "gcg_syev": [_ptr, _i64, _ptr, _i64, _ptr, _ptr, _i64],

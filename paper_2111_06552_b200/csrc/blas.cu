@@ -232,6 +232,49 @@ int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, cons
   return GCG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// FP64 peak probes (roofline denominators; MEASURED_PEAKS.json has no FP64 entry):
+// every thread runs `iters` x 8 independent chains of DMMA.8x8x4 (mode 1, 512 flop
+// per warp-instruction per chain) or DFMA (mode 0, 2 flop per lane).
+__global__ void fp64_peak_kernel(int mode, int iters, double* sink) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  if (mode == 1) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c[i][0]), "+d"(c[i][1])
+            : "d"(a), "d"(b));
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c[i][0] = fma(a, c[i][0], b);
+        c[i][1] = fma(b, c[i][1], a);
+      }
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) sink[0] = s;  // keep the chains live
+}
+
+int fp64_peak_launch(Ctx* c, int mode, int iters, double* sink, int* grid_out, int* block_out) {
+  const int block = 256, grid = c->num_sms * 4;
+  fp64_peak_kernel<<<grid, block, 0, c->stream>>>(mode, iters, sink);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  *grid_out = grid;
+  *block_out = block;
+  return GCG_OK;
+}
+
 __global__ void symmetrize_kernel(int m, double* A, long long lda) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)m * m) return;

@@ -48,6 +48,7 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
                     int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist);
 int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X, long long ldx,
                        double* out, long long ldo);
+int fp64_peak_launch(Ctx* c, int mode, int iters, double* sink, int* grid_out, int* block_out);
 int ritz_sums_launch(Ctx* c, long long n, int k, const double* AX, long long ldax,
                      const double* X, long long ldx, const double* BX, long long ldbx,
                      const double* lam, int mode, double* sums);
@@ -387,6 +388,18 @@ int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
   return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
                          max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres, dist);
+}
+
+int gcg_fp64_peak(void* p, int mode, int32_t iters, double* flops_per_launch, double* sink) {
+  Ctx* c = CTX(p);
+  if (!c || (mode != 0 && mode != 1) || iters <= 0 || !flops_per_launch || !sink)
+    return GCG_ERR_ARG;
+  int grid = 0, block = 0;
+  GCG_TRY(fp64_peak_launch(c, mode, iters, sink, &grid, &block));
+  const double warps = (double)grid * block / 32.0;
+  *flops_per_launch = mode == 1 ? warps * iters * 8.0 * 512.0          // 8x8x4 x 2 flop
+                                : (double)grid * block * iters * 8.0 * 4.0;  // 2 fma x 2 flop
+  return GCG_OK;
 }
 
 int gcg_gather_rows(void* p, int64_t nidx, const int32_t* idx, int64_t k, const double* X,

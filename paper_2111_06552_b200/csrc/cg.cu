@@ -12,8 +12,8 @@
 // and the scalar recurrences run in 1-CTA "finish" kernels.  No host sync
 // happens inside the solve: once every column has stopped, a device flag turns
 // the remaining launches into no-ops and the sweep count is read back lazily
-// by the caller.  Per sweep HBM traffic ~ SpMM + 48nk (x,r,p,q update) + 24nk
-// (p = r + beta p).
+// by the caller.  Per sweep HBM traffic ~ SpMM + 24nk (r -= alpha q) + 40nk
+// (x += alpha p, p = r + beta p).
 
 #include <stdlib.h>
 
@@ -47,6 +47,7 @@ struct CgState {
   int* sweeps;
   int* nact;
   int* ticket;
+  int* live;
 };
 
 // Fixed-order reduction of one column's per-CTA partials by a 128-thread block:
@@ -110,7 +111,13 @@ __global__ void cg_init_fin(int k, const double* part, int nparts, double rel_to
 
 // den = p'q per active column; freeze on den <= 0, else alpha = rz / den.
 __global__ void cg_fin1(int k, const double* part, int nparts, CgState s) {
-  if (*s.skip) return;
+  // `live` tells cg_pupdate_kernel whether this sweep ran (its deferred x update
+  // must still happen in the sweep that raises `skip`)
+  if (*s.skip) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *s.live = 0;
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *s.live = 1;
   __shared__ double sm[128];
   const int c = blockIdx.x;
   const double den = block_sum_parts(part, nparts, k, c, sm);
@@ -156,10 +163,10 @@ __global__ void cg_fin2(int k, const double* part, int nparts, CgState s) {
   publish_active(s, k, active, false);
 }
 
-// x += alpha p ; r -= alpha q ; partial ||r||^2 (updated columns only)
-__global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, double* x,
-                                                        long long ldx, double* r,
-                                                        const double* __restrict__ p,
+// r -= alpha q ; partial ||r||^2 (updated columns only).  The matching
+// x += alpha p is deferred to cg_pupdate_kernel, which reads the old p anyway:
+// per sweep 24nk + 40nk bytes instead of 48nk + 24nk.
+__global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, double* r,
                                                         const double* __restrict__ q,
                                                         long long rows_per_cta, double* part,
                                                         CgState s, int* prof_skipped) {
@@ -176,37 +183,28 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
   double acc = 0.0;
-  if (rl < lanes) {
-    const int u = s.upd[c];
+  if (rl < lanes && s.upd[c]) {
     const double al = s.alpha[c];
-    if (u) {
-      constexpr int U = 4;  // rows in flight per thread
-      long long i = r0 + rl;
-      for (; i + (U - 1) * lanes < r1; i += U * lanes) {
-        double xv[U], pv[U], qv[U], rv[U];
+    constexpr int U = 8;  // rows in flight per thread
+    long long i = r0 + rl;
+    for (; i + (U - 1) * lanes < r1; i += U * lanes) {
+      double qv[U], rv[U];
 #pragma unroll
-        for (int q4 = 0; q4 < U; ++q4) {
-          const long long ii = i + q4 * lanes;
-          xv[q4] = x[ii * ldx + c];
-          pv[q4] = p[ii * k + c];
-          qv[q4] = q[ii * k + c];
-          rv[q4] = r[ii * k + c];
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < U; ++q4) {
-          const long long ii = i + q4 * lanes;
-          x[ii * ldx + c] = fma(al, pv[q4], xv[q4]);
-          const double nr = fma(-al, qv[q4], rv[q4]);
-          r[ii * k + c] = nr;
-          acc = fma(nr, nr, acc);
-        }
+      for (int u = 0; u < U; ++u) {
+        qv[u] = q[(i + u * lanes) * k + c];
+        rv[u] = r[(i + u * lanes) * k + c];
       }
-      for (; i < r1; i += lanes) {
-        x[i * ldx + c] = fma(al, p[i * k + c], x[i * ldx + c]);
-        const double nr = fma(-al, q[i * k + c], r[i * k + c]);
-        r[i * k + c] = nr;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double nr = fma(-al, qv[u], rv[u]);
+        r[(i + u * lanes) * k + c] = nr;
         acc = fma(nr, nr, acc);
       }
+    }
+    for (; i < r1; i += lanes) {
+      const double nr = fma(-al, q[i * k + c], r[i * k + c]);
+      r[i * k + c] = nr;
+      acc = fma(nr, nr, acc);
     }
   }
   sm[threadIdx.x] = acc;
@@ -218,18 +216,50 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   }
 }
 
-// p = r + beta p for columns still iterating
-__global__ void cg_pupdate_kernel(long long n, int k, const double* __restrict__ r, double* p,
-                                  CgState s, int* prof_skipped) {
-  if (*s.skip) {
+// x += alpha p (columns updated this sweep) then p = r + beta p (columns still iterating)
+__global__ void __launch_bounds__(256) cg_pupdate_kernel(long long n, int k, double* x,
+                                                         long long ldx,
+                                                         const double* __restrict__ r, double* p,
+                                                         long long rows_per_cta, CgState s,
+                                                         int* prof_skipped) {
+  if (!*s.live) {
     if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
     return;
   }
-  const long long tot = n * k;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(e % k);
-    if (s.pup[c]) p[e] = fma(s.beta[c], p[e], r[e]);
+  // same (row lane, column) mapping as cg_update_kernel: flags and scalars are
+  // per-thread constants, U rows in flight per thread
+  const int lanes = 256 / k;
+  const int c = threadIdx.x % k;
+  const int rl = threadIdx.x / k;
+  if (rl >= lanes) return;
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  long long r1 = r0 + rows_per_cta;
+  if (r1 > n) r1 = n;
+  const bool ux = s.upd[c], up = s.pup[c];
+  if (!ux && !up) return;
+  const double al = s.alpha[c], be = s.beta[c];
+  constexpr int U = 8;
+  long long i = r0 + rl;
+  for (; i + (U - 1) * lanes < r1; i += U * lanes) {
+    double pv[U], xv[U], rv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long ii = i + u * lanes;
+      pv[u] = p[ii * k + c];
+      if (ux) xv[u] = x[ii * ldx + c];
+      if (up) rv[u] = r[ii * k + c];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long ii = i + u * lanes;
+      if (ux) x[ii * ldx + c] = fma(al, pv[u], xv[u]);
+      if (up) p[ii * k + c] = fma(be, pv[u], rv[u]);
+    }
+  }
+  for (; i < r1; i += lanes) {
+    const double pv = p[i * k + c];
+    if (ux) x[i * ldx + c] = fma(al, pv, x[i * ldx + c]);
+    if (up) p[i * k + c] = fma(be, pv, r[i * k + c]);
   }
 }
 
@@ -305,16 +335,25 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   ugrid = (int)((n + rpc - 1) / rpc);
   const int nparts_max = sgrid > ugrid ? sgrid : ugrid;
   const long long nghost = dist ? dist->nghost : 0;
-  // workspace: R, Q (n x k), P ((n + ghosts) x k) + partials + state
+  // workspace: R, Q (n x k), P and X ((n + ghosts) x k) + partials + state.  The
+  // iterate lives in the dense X (ld = k) during the sweeps — a strided arena view
+  // streams noticeably slower — and is copied back into x at the end.
   const size_t vec = (size_t)n * k;
   const size_t pvec = (size_t)(n + nghost) * k;
-  const size_t bytes = sizeof(double) * (2 * vec + pvec + (size_t)nparts_max * k + 6 * (size_t)k) +
-                       sizeof(int) * (4 * (size_t)k + 4) + 256;
+  const size_t bytes =
+      sizeof(double) * (2 * vec + 2 * pvec + (size_t)nparts_max * k + 6 * (size_t)k) +
+      sizeof(int) * (4 * (size_t)k + 5) + 256;
   GCG_TRY(ensure(c->cg, bytes));
   double* R = (double*)c->cg.ptr;
   double* Q = R + vec;
   double* P = Q + vec;
-  double* part = P + pvec;
+  double* Xc = P + pvec;
+  double* part = Xc + pvec;
+  double* const x_user = x;
+  const long long ldx_user = ldx;
+  GCG_TRY(copy_launch(c, n, k, x_user, ldx_user, Xc, k));
+  x = Xc;
+  ldx = k;
   double* sd = part + (size_t)nparts_max * k;
   CgState s;
   s.rz = sd;
@@ -332,7 +371,8 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   s.sweeps = si + 4 * k + 1;
   s.nact = si + 4 * k + 2;
   s.ticket = si + 4 * k + 3;
-  GCG_TRY(cuda_status(cudaMemsetAsync(s.skip, 0, 4 * sizeof(int), c->stream)));
+  s.live = si + 4 * k + 4;
+  GCG_TRY(cuda_status(cudaMemsetAsync(s.skip, 0, 5 * sizeof(int), c->stream)));
   const int fin_threads = k < 32 ? 32 : (k + 31) / 32 * 32;
 
   // r = rhs - op(x) = -(A x) - shift*x + rhs ; ||r0||^2 partials
@@ -351,7 +391,6 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   ++g_launches;
   GCG_CHECK_LAUNCH();
   GCG_TRY(copy_launch(c, n, k, R, k, P, k));
-  const int pgrid = grid_for(n * k, 1024, 8, c->num_sms);
   for (int it = 0; it < max_iters; ++it) {
     if (dist) GCG_TRY(dist_halo(c, dist, n, k, P, k));
     GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0,
@@ -364,9 +403,8 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       nred = 1;
     }
     cg_fin1<<<k, 128, 0, c->stream>>>(k, red, nred, s);
-    int ps = prof_start(c, PROF_CG_UPDATE, 48.0 * n * k);
-    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, Q, rpc, part, s,
-                                                   prof_skip_slot(c, ps));
+    int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
+    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, R, Q, rpc, part, s, prof_skip_slot(c, ps));
     prof_stop(c, ps);
     red = part;
     nred = ugrid;
@@ -376,12 +414,14 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       nred = 1;
     }
     cg_fin2<<<k, 128, 0, c->stream>>>(k, red, nred, s);
-    ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
-    cg_pupdate_kernel<<<pgrid, 256, 0, c->stream>>>(n, k, R, P, s, prof_skip_slot(c, ps));
+    ps = prof_start(c, PROF_CG_PUPDATE, 40.0 * n * k);
+    cg_pupdate_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, rpc, s,
+                                                    prof_skip_slot(c, ps));
     prof_stop(c, ps);
     g_launches += 4;
     GCG_CHECK_LAUNCH();
   }
+  GCG_TRY(copy_launch(c, n, k, Xc, k, x_user, ldx_user));
   cg_final<<<1, fin_threads, 0, c->stream>>>(k, s, d_sweeps, d_conv, d_frozen, d_relres);
   ++g_launches;
   GCG_CHECK_LAUNCH();

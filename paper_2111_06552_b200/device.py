@@ -265,6 +265,23 @@ def ritz_residuals(ctx, AX, X, BX, lam, mode, out):
     return out
 
 
+def fp64_peak(ctx, mode="dmma", iters=4096, reps=5):
+    """Measured FP64 throughput (TFLOP/s) of DMMA.8x8x4 ('dmma') or DFMA ('dfma') chains."""
+    sink = ctx.empty(1)
+    flops = C.c_double()
+    m = 1 if mode == "dmma" else 0
+    _lib.call("gcg_fp64_peak", ctx.h, m, int(iters), C.byref(flops), _p(sink))  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(reps):
+        e0.record(ctx.stream)
+        _lib.call("gcg_fp64_peak", ctx.h, m, int(iters), C.byref(flops), _p(sink))
+        e1.record(ctx.stream)
+        e1.synchronize()
+        best = max(best, flops.value / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    return best
+
+
 def gather_rows(ctx, idx, X, out):
     """out[i, :] = X[idx[i], :] (idx int32 on device)."""
     k = X.shape[1]

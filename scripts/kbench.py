@@ -39,6 +39,8 @@ def report(name, sec, nbytes, flops=0.0):
 
 def main(cfgs):
     rng = np.random.default_rng(1)
+    print(f"FP64 peak: DMMA {D.fp64_peak(dev, 'dmma'):.1f} TF/s, DFMA {D.fp64_peak(dev, 'dfma'):.1f} TF/s",
+          flush=True)
     for cfg in cfgs:
         pr = P.baseline_problem(cfg)
         a = pr.a
