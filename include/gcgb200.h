@@ -100,7 +100,9 @@ int gcg_gram(void* ctx, int64_t n, int64_t k1, int64_t k2, const double* X, int6
              int64_t g_cs, const double* T, int64_t ldt, double* dots);
 
 /* Y = alpha * X C + beta * Y;  X: n x m, C: m x d (row-major, ldc), Y: n x d.
- * Y must not overlap X. */
+ * Y may share rows with X (same row stride): column ranges disjoint, or in
+ * place (Y row i inside X row i) when d <= 256 — one CTA owns all output
+ * columns of its rows; any other overlap is GCG_ERR_ARG. */
 int gcg_lincomb(void* ctx, int64_t n, int64_t m, int64_t d, double alpha, const double* X,
                 int64_t ldx, const double* C, int64_t ldc, double beta, double* Y, int64_t ldy);
 

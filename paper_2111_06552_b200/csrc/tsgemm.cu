@@ -289,7 +289,7 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
 template <int BM, int BN, int WM, int WN, bool VEC16>
 __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, int d,
                                                            double alpha,
-                                                           const double* __restrict__ X,
+                                                           const double* X,
                                                            long long ldx,
                                                            const double* __restrict__ C,
                                                            long long ldc, double beta, double* Y,
@@ -401,6 +401,22 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
                    long long ldx, const double* C, long long ldc, double beta, double* Y,
                    long long ldy) {
   if (n <= 0 || d <= 0) return GCG_OK;
+  {
+    // In-place use (Y inside the rows of X: [X|P] <- basis [coeffs|phat]) is safe
+    // only when one CTA owns all d output columns of its rows (grid.y == 1): every
+    // X row tile is fully staged (cp.async + barrier) before that CTA stores it.
+    const double* xe = X + (n - 1) * ldx + m;
+    const double* ye = Y + (n - 1) * ldy + d;
+    if ((Y < xe) && (X < ye)) {  // address hulls meet: compare on the row lattice
+      if (ldx != ldy) return GCG_ERR_ARG;
+      const long long off = Y - X;
+      const long long r = off >= 0 ? off / ldx : -((-off + ldx - 1) / ldx);
+      const long long co = off - r * ldx;  // Y row i starts at column co of X row i + r
+      const bool same = co < m;            // hits X row i + r
+      const bool next = co + d > ldx;      // wraps into X row i + r + 1
+      if (next || (same && (r != 0 || d > 256))) return GCG_ERR_ARG;
+    }
+  }
   const int ps =
       prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
   const bool vec = (ldx % 2 == 0) && al16(X);

@@ -157,7 +157,8 @@ def gram(ctx, X, Y, G, alpha=1.0, beta=0.0, T=None, dots=None, transpose_out=Fal
 
 
 def lincomb(ctx, X, Cm, Y, alpha=1.0, beta=0.0):
-    """Y = alpha X C + beta Y  (gcg_lincomb); Y must not overlap X."""
+    """Y = alpha X C + beta Y  (gcg_lincomb); Y may alias X only row-for-row
+    (in place, d <= 256 — see gcgb200.h)."""
     n, m = X.shape
     d = Cm.shape[1]
     if Cm.shape[0] != m or Y.shape != (n, d):

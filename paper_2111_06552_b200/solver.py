@@ -208,12 +208,20 @@ class _Solve:
             out[s:e] = self.ops.broadcast(r).cpu().numpy()
         return out
 
-    def count_converged(self, x_new, lam_new_dev, limit, chunk, tol):
-        """solver._count_converged (solver.py:144-164): prefix of Ritz pairs below tol."""
+    def count_converged(self, basis, coeffs, lam_new_dev, limit, chunk, tol):
+        """solver._count_converged (solver.py:144-164): prefix of Ritz pairs below tol.
+
+        The Ritz vectors are formed chunk by chunk (basis @ coeffs[:, chunk]) only
+        as far as the prefix test reads them; the full X update happens in place
+        afterwards (:meth:`update_in_place`)."""
         count = 0
+        xc = None
         for start in range(0, limit, chunk):
             stop = min(start + chunk, limit)
-            rel = self.residuals(x_new[:, start:stop], lam_new_dev[start:stop])
+            if xc is None or xc.shape[1] != stop - start:
+                xc = self.ops.vec(stop - start)
+            D.lincomb(self.dev, basis, coeffs[:, start:stop], xc)
+            rel = self.residuals(xc, lam_new_dev[start:stop])
             for j in range(stop - start):
                 if rel[j] < tol:
                     count += 1
@@ -264,6 +272,17 @@ class _Solve:
         q = dev.empty(pt.shape[0], kept)
         D.dgemm(dev, pt, scaled, q)
         return q, kept
+
+    def update_in_place(self, basis, cm, dst):
+        """dst <- basis @ cm where dst = the leading columns of basis (the reference's
+        v[:, locked:sx] = x_new; v[:, sx:sx+np] = p_new, solver.py:378-384).  One
+        in-place lincomb when all columns fit one tile (<= 256), else via a temporary."""
+        if cm.shape[1] <= 256:
+            D.lincomb(self.dev, basis, cm, dst)
+        else:
+            tmp = self.ops.vec(cm.shape[1])
+            D.lincomb(self.dev, basis, cm, tmp)
+            D.copy(self.dev, tmp, dst)
 
     def hstack(self, parts):
         """Contiguous copy of column blocks (the reference's np.hstack, solver.py:337,356,401,450)."""
@@ -383,20 +402,18 @@ def gcg_solve_ops(ops, cfg, x0=None):
         ops.broadcast(full.vectors)
         lam_new_dev = full.values[:d]
         coeffs = full.vectors[:, :d]
-        x_new = ops.vec(d)
-        D.lincomb(dev, basis, coeffs, x_new)
         lam_new = lam_new_dev.cpu().numpy()
         timer.lap("t_step3")
 
         stored = sum(len(vv) for vv in store_vals)
         limit = max(0, min(sx - locked, ne - stored - locked))
-        newly, first_res = S.count_converged(x_new, lam_new_dev, limit, bs, cfg.tol)
+        newly, first_res = S.count_converged(basis, coeffs, lam_new_dev, limit, bs, cfg.tol)
         c = locked + newly
         total_locked = stored + c
         timer.lap("t_step4")
 
         if total_locked >= ne:
-            D.copy(dev, x_new, v[:, locked:sx])
+            S.update_in_place(basis, coeffs, v[:, locked:sx])
             lam[locked:sx] = lam_new
             locked = c
             status = "converged"
@@ -451,22 +468,22 @@ def gcg_solve_ops(ops, cfg, x0=None):
             else:
                 bs_eff = max(1, min(bs, ne - stored - c, sx - c))
                 phat = S.build_p(coeffs, d, c - locked, bs_eff, ocfg.dependence_tol)
-                p_new = None
                 if phat is None:
                     p_coupling = None
+                    cm = coeffs
                 else:
-                    p_new = dev.empty(nloc, phat.shape[1])
-                    D.lincomb(dev, basis, phat, p_new)
                     ap = dev.empty(m, phat.shape[1])
                     D.dgemm(dev, abar, phat, ap)
                     p_coupling = dev.empty(phat.shape[1], phat.shape[1])
                     D.dgemm(dev, phat, ap, p_coupling, ta=True)
-                D.copy(dev, x_new, v[:, locked:sx])
+                    cm = dev.empty(m, d + phat.shape[1])
+                    D.copy(dev, coeffs, cm[:, :d])
+                    D.copy(dev, phat, cm[:, d:])
+                # [X_new | P_new] = basis [coeffs | phat], written over the basis' head
+                S.update_in_place(basis, cm, v[:, locked:locked + cm.shape[1]])
                 lam[locked:sx] = lam_new
                 locked = c
-                np_ = 0 if p_new is None else p_new.shape[1]
-                if np_:
-                    D.copy(dev, p_new, v[:, sx:sx + np_])
+                np_ = 0 if phat is None else phat.shape[1]
             timer.lap("t_step5")
 
             # STEP 6: damped inverse power via block CG (solver.py:386-396)

@@ -135,6 +135,30 @@ def test_lincomb_vs_numpy(dev, n, m, d):
     assert rel_err(host(y), want) <= 1e-13
 
 
+@pytest.mark.parametrize("n,m,d,off", [(5000, 200, 180, 0), (3001, 40, 24, 0),
+                                        (3001, 40, 20, 7), (777, 64, 64, 0)])
+def test_lincomb_in_place(dev, n, m, d, off):
+    """[X|P] <- basis [coeffs|phat] written over the basis' own columns (solver step 5)."""
+    rng = np.random.default_rng(n + d)
+    x = rng.standard_normal((n, m + 3))
+    c = rng.standard_normal((m, d))
+    v = rm(dev, x)
+    D.lincomb(dev, v[:, :m], rm(dev, c), v[:, off:off + d])
+    got = host(v)
+    assert rel_err(got[:, off:off + d], x[:, :m] @ c) <= 1e-13
+    assert np.array_equal(got[:, :off], x[:, :off])
+    assert np.array_equal(got[:, off + d:], x[:, off + d:])
+
+
+def test_lincomb_rejects_cross_row_overlap(dev):
+    v = dev.zeros(100, 300)
+    cm = dev.zeros(20, 8)
+    with pytest.raises(Exception):
+        D.lincomb(dev, v[1:, :20], cm, v[:-1, :8])     # Y row i aliases X row i - 1
+    with pytest.raises(Exception):
+        D.lincomb(dev, v, dev.zeros(300, 260), v[:, :260])  # in place beyond one column tile
+
+
 def test_axpby_copy_scale_dots(dev):
     rng = np.random.default_rng(5)
     x, y = rng.standard_normal((999, 7)), rng.standard_normal((999, 7))
