@@ -338,8 +338,9 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   // workspace: R, Q (n x k), P and X ((n + ghosts) x k) + partials + state.  The
   // iterate lives in the dense X (ld = k) during the sweeps — a strided arena view
   // streams noticeably slower — and is copied back into x at the end.
-  const size_t vec = (size_t)n * k;
-  const size_t pvec = (size_t)(n + nghost) * k;
+  // block starts kept 32-byte aligned so the SpMM can gather rows with 256-bit loads
+  const size_t vec = ((size_t)n * k + 3) & ~(size_t)3;
+  const size_t pvec = ((size_t)(n + nghost) * k + 3) & ~(size_t)3;
   const size_t bytes =
       sizeof(double) * (2 * vec + 2 * pvec + (size_t)nparts_max * k + 6 * (size_t)k) +
       sizeof(int) * (4 * (size_t)k + 5) + 256;

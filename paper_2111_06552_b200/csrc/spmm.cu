@@ -6,22 +6,27 @@
 //
 // B200 design.  X is row-major, so the k values a nonzero (i, j) needs are one
 // contiguous run X[j*ldx : j*ldx+k].  A group of LPR lanes owns one row and
-// reads those runs with 16-byte vector loads (NV column chunks per lane); a
-// warp holds 32/LPR rows.  The row's (column index, value) stream is loaded
-// once, cooperatively (one nonzero per lane, 12 B/nnz from HBM), and broadcast
-// inside the group with shuffles.
+// reads that run with the widest aligned vector loads (32-byte LDG.256 when
+// rows are 4-double aligned, else 16 or 8 bytes), NV column chunks per lane;
+// LPR is any 1..32 chosen so the groups tile the row and the warp with the
+// least idle lanes (k = 20: five lanes x 32 B per row, six rows per warp), so
+// one row gather is one instruction touching the two 128-byte lines it spans.
+// The row's (column index, value) stream is loaded once, cooperatively (two
+// nonzeros per lane, 12 B/nnz from HBM), and broadcast inside the group with
+// shuffles.
 //
 // At the BASELINE shapes the kernel is latency-bound (a row is a 3-deep chain:
 // row pointer -> index/value -> X gathers), so it is software-pipelined: while
 // a warp gathers X for its current rows it already holds the row pointers and
 // the index/value chunk of its NEXT rows in registers, leaving only the X
-// gathers on the critical path; all gathers of a row batch (up to 8 nonzeros)
-// are issued before the first FMA.
+// gathers on the critical path.
 //
 // The epilogue fuses the shifted-operator term (gamma*Z, Z = X for A - theta*I),
 // an axpby with a second input (beta*Yin, used for r = rhs - op x) and an
 // optional per-column dot product reduced deterministically (p'q and ||r||^2
-// for block CG), so CG never makes a separate pass for them.
+// for block CG), so CG never makes a separate pass for them.  When Z (and W)
+// is X itself the row's own values come from the diagonal gather already in
+// registers instead of a second read; the epilogue streams are vectorised.
 //
 // Roofline: HBM.  Algorithmic bytes per launch = 12*nnz + 4*(n+1) + 16*n*k
 // (+8*n*k per extra epilogue stream); flops = 2*nnz*k.
@@ -50,9 +55,13 @@ struct SpmmArgs {
   double* Y;
   long long ldy;
   int dot_mode;
+  int lpr, gpw;    // lanes per row, rows per warp step
+  int vepi;        // epilogue streams VEC-aligned
+  long long rpc;   // > 0: rows per CTA (contiguous ranges); 0: grid-stride
   const double* __restrict__ W;
   long long ldw;
-  double* partials;   // [gridDim.x][k]
+  double* partials;   // [gridDim.x][pld] (+ this pass' column offset)
+  int pld;
   const int* skip;    // device flag: nonzero -> kernel is a no-op (CG early exit)
   int* prof_skipped;  // profiling: set when the launch was a no-op
 };
@@ -62,6 +71,8 @@ struct VecT;
 template <>
 struct VecT<1> {
   static __device__ __forceinline__ void load(const double* p, double* o) { o[0] = __ldg(p); }
+  static __device__ __forceinline__ void ld(const double* p, double* o) { o[0] = *p; }
+  static __device__ __forceinline__ void st(double* p, const double* o) { *p = o[0]; }
 };
 template <>
 struct VecT<2> {
@@ -70,97 +81,153 @@ struct VecT<2> {
     o[0] = v.x;
     o[1] = v.y;
   }
+  static __device__ __forceinline__ void ld(const double* p, double* o) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    o[0] = v.x;
+    o[1] = v.y;
+  }
+  static __device__ __forceinline__ void st(double* p, const double* o) {
+    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+  }
+};
+// 32-byte accesses (LDG.E.ENL2.256 on sm_100): a 20-column row is 5 lanes
+template <>
+struct VecT<4> {
+  static __device__ __forceinline__ void load(const double* p, double* o) {
+    const double4 v = *reinterpret_cast<const double4*>(p);
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  }
+  static __device__ __forceinline__ void ld(const double* p, double* o) { load(p, o); }
+  static __device__ __forceinline__ void st(double* p, const double* o) {
+    *reinterpret_cast<double4*>(p) = make_double4(o[0], o[1], o[2], o[3]);
+  }
 };
 
 constexpr int kSpmmThreads = 256;
-constexpr int kSpmmMinBlocks = 4;  // <= 64 registers: 32 resident warps per SM
+constexpr int kSpmmMaxPass = 256;
+constexpr int kSpmmMaxSlots = 8;  // NV * VEC
+// resident CTAs per SM by per-lane accumulator width (<= 64 registers at 4)
+__host__ __device__ constexpr int spmm_min_blocks(int doubles) {
+  return doubles > 0 ? 4 : 4;  // every shape: 64 registers, one grid size
+}
 
-template <int LPR, int VEC, int NV>
-__global__ void __launch_bounds__(kSpmmThreads, kSpmmMinBlocks) spmm_csr_kernel(SpmmArgs a) {
+template <int VEC, int NV>
+__global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
+    spmm_csr_kernel(SpmmArgs a) {
   if (a.skip != nullptr && *a.skip) {
     if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
     return;
   }
-  constexpr int G = 32 / LPR;  // rows per warp step
-  constexpr int COLS = LPR * VEC * NV;
-  // gathers in flight per batch: <= 16 doubles of X per lane, a power of 2 dividing LPR
+  // gathers in flight per batch: <= 16 doubles of X per lane, at most 4 nonzeros
   constexpr int UB = 16 / (NV * VEC);
-  constexpr int U0 = UB >= 8 ? 8 : (UB >= 4 ? 4 : 2);
-  constexpr int U = U0 < LPR ? U0 : LPR;
+  constexpr int U = UB >= 4 ? 4 : (UB >= 2 ? 2 : 1);
   constexpr int NW = kSpmmThreads / 32;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int LPR = a.lpr, G = a.gpw;  // lanes per row (any 1..32), rows per warp step
+  const int CH = 2 * LPR;            // nonzeros per index/value chunk (2 per lane)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane / LPR, sub = lane % LPR;
-  const long long stride = (long long)gridDim.x * NW * G;
+  const int g0 = lane / LPR;
+  const bool active = g0 < G;  // lanes past G*LPR mirror the last group, never store
+  const int g = active ? g0 : G - 1;
+  const int sub = lane - g0 * LPR;
+  const int gbase = g * LPR;
+  // rows: contiguous per CTA (a.rpc > 0: stencil neighbours i +- 1, i +- nx are
+  // gathered by the same SM and hit L1) or interleaved grid-stride
+  long long rb, rend, stride;
+  if (a.rpc > 0) {
+    rb = (long long)blockIdx.x * a.rpc + (long long)warp * G;
+    rend = min(a.n, (long long)(blockIdx.x + 1) * a.rpc);
+    stride = (long long)NW * G;
+  } else {
+    rb = ((long long)blockIdx.x * NW + warp) * G;
+    rend = a.n;
+    stride = (long long)gridDim.x * NW * G;
+  }
   const int k = a.k;
 
-  __shared__ double sdot[NW][COLS];
-  double dacc[NV][VEC];
+  // per-lane dot accumulators live in shared memory ([warp][slot][lane]: each
+  // lane owns its column slots), keeping registers for gathers in flight
+  __shared__ double sacc[NW][kSpmmMaxSlots][32];
+  __shared__ double sdot[NW][kSpmmMaxPass];
+  if (a.dot_mode) {
 #pragma unroll
-  for (int q = 0; q < NV; ++q)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) dacc[q][e] = 0.0;
+    for (int q = 0; q < NV * VEC; ++q) sacc[warp][q][lane] = 0.0;
+  }
 
   // prefetched state of the row this lane group handles next
-  long long rb = ((long long)blockIdx.x * NW + warp) * G;
-  int nstart = 0, nlen = 0, ncol = 0;
-  double nval = 0.0;
+  int nstart = 0, nlen = 0, ncol0 = 0, ncol1 = 0;
+  double nval0 = 0.0, nval1 = 0.0;
   auto fetch_rowptr = [&](long long base, int& st, int& ln) {
     const long long r = base + g;
     st = 0;
     ln = 0;
-    if (r < a.n) {
+    if (r < rend) {
       st = __ldg(a.rowptr + r);
       ln = __ldg(a.rowptr + r + 1) - st;
     }
   };
-  auto fetch_chunk = [&](int st, int ln, int off, int& cidx, double& cval) {
-    cidx = 0;
-    cval = 0.0;
-    if (off + sub < ln) {
-      cidx = __ldg(a.colidx + st + off + sub);
-      cval = __ldg(a.val + st + off + sub);
+  auto fetch_chunk = [&](int st, int ln, int off, int& c0, double& v0, int& c1, double& v1) {
+    const int i0 = off + sub, i1 = off + LPR + sub;
+    c0 = 0;
+    v0 = 0.0;
+    c1 = 0;
+    v1 = 0.0;
+    if (i0 < ln) {
+      c0 = __ldg(a.colidx + st + i0);
+      v0 = __ldg(a.val + st + i0);
+    }
+    if (i1 < ln) {
+      c1 = __ldg(a.colidx + st + i1);
+      v1 = __ldg(a.val + st + i1);
     }
   };
-  if (rb < a.n) {
+  if (rb < rend) {
     fetch_rowptr(rb, nstart, nlen);
-    fetch_chunk(nstart, nlen, 0, ncol, nval);
+    fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
   }
 
-  for (; rb < a.n; rb += stride) {
+  for (; rb < rend; rb += stride) {
     const long long r = rb + g;
     const int start = nstart, len = nlen;
-    int mycol = ncol;
-    double myval = nval;
+    int col0 = ncol0, col1 = ncol1;
+    double val0 = nval0, val1 = nval1;
     const long long rbn = rb + stride;
-    if (rbn < a.n) fetch_rowptr(rbn, nstart, nlen);  // lands during the gathers below
-    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+    if (rbn < rend) fetch_rowptr(rbn, nstart, nlen);  // lands during the gathers below
+    const int maxlen = __reduce_max_sync(FULL, len);
     double acc[NV][VEC];
 #pragma unroll
     for (int q = 0; q < NV; ++q)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
 
-    for (int off = 0; off < maxlen; off += LPR) {
-      if (off > 0) fetch_chunk(start, len, off, mycol, myval);  // rows longer than LPR
-      const int tmax = min(LPR, maxlen - off);
+    for (int off = 0; off < maxlen; off += CH) {
+      if (off > 0) fetch_chunk(start, len, off, col0, val0, col1, val1);  // long rows
+      const int tmax = min(CH, maxlen - off);
       for (int t0 = 0; t0 < tmax; t0 += U) {
         int j[U];
         double v[U];
+        bool ok[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          j[u] = __shfl_sync(0xffffffffu, mycol, t0 + u, LPR);
-          v[u] = __shfl_sync(0xffffffffu, myval, t0 + u, LPR);
-          if (t0 + u >= tmax || off + t0 + u >= len) v[u] = 0.0;
+          const int t = t0 + u;  // warp-uniform
+          const bool lo = t < LPR;
+          const int src = (gbase + (lo ? t : t - LPR)) & 31;
+          j[u] = __shfl_sync(FULL, lo ? col0 : col1, src);
+          v[u] = __shfl_sync(FULL, lo ? val0 : val1, src);
+          ok[u] = (t < tmax) && (off + t < len);
+          if (!ok[u]) v[u] = 0.0;
         }
         double xv[U][NV][VEC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const bool ok = (t0 + u < tmax) && (off + t0 + u < len);
           const double* xr = a.X + (long long)j[u] * a.ldx;
 #pragma unroll
           for (int q = 0; q < NV; ++q) {
             const int c = (q * LPR + sub) * VEC;
-            if (ok && c < k) {
+            if (ok[u] && c < k) {
               VecT<VEC>::load(xr + c, xv[u][q]);
             } else {
 #pragma unroll
@@ -177,48 +244,79 @@ __global__ void __launch_bounds__(kSpmmThreads, kSpmmMinBlocks) spmm_csr_kernel(
       }
     }
     // first index/value chunk of the next rows (their row pointers have arrived)
-    if (rbn < a.n) fetch_chunk(nstart, nlen, 0, ncol, nval);
-    if (r < a.n) {
+    if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
+    if (active && r < rend) {
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         const int c = (q * LPR + sub) * VEC;
-        if (c < k) {
+        if (c >= k) continue;
+        double y[VEC], t[VEC];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            double y = a.alpha * acc[q][e];
-            if (a.gamma != 0.0) y = fma(a.gamma, a.Z[r * a.ldz + c + e], y);
-            if (a.beta != 0.0) y = fma(a.beta, a.Yin[r * a.ldyin + c + e], y);
-            a.Y[r * a.ldy + c + e] = y;
-            if (a.dot_mode == 1) dacc[q][e] = fma(y, a.W[r * a.ldw + c + e], dacc[q][e]);
-            else if (a.dot_mode == 2) dacc[q][e] = fma(y, y, dacc[q][e]);
+        for (int e = 0; e < VEC; ++e) y[e] = a.alpha * acc[q][e];
+        if (a.gamma != 0.0) {
+          if (a.vepi) {
+            VecT<VEC>::ld(a.Z + r * a.ldz + c, t);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) t[e] = a.Z[r * a.ldz + c + e];
           }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(a.gamma, t[e], y[e]);
+        }
+        if (a.beta != 0.0) {
+          if (a.vepi) {
+            VecT<VEC>::ld(a.Yin + r * a.ldyin + c, t);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) t[e] = a.Yin[r * a.ldyin + c + e];
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(a.beta, t[e], y[e]);
+        }
+        if (a.vepi) {
+          VecT<VEC>::st(a.Y + r * a.ldy + c, y);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) a.Y[r * a.ldy + c + e] = y[e];
+        }
+        if (a.dot_mode == 1) {
+          if (a.vepi) {
+            VecT<VEC>::ld(a.W + r * a.ldw + c, t);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) t[e] = a.W[r * a.ldw + c + e];
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sacc[warp][q * VEC + e][lane] = fma(y[e], t[e], sacc[warp][q * VEC + e][lane]);
+        } else if (a.dot_mode == 2) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sacc[warp][q * VEC + e][lane] = fma(y[e], y[e], sacc[warp][q * VEC + e][lane]);
         }
       }
     }
   }
 
   if (a.dot_mode == 0) return;
-  // reduce over the row groups of the warp (lanes with equal `sub`), then warps
-#pragma unroll
-  for (int q = 0; q < NV; ++q)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      double v = dacc[q][e];
-#pragma unroll
-      for (int o = LPR; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      dacc[q][e] = v;
-    }
-  if (g == 0) {
+  // reduce over the row groups of the warp (fixed order g = 0..G-1), then warps
+  __syncwarp();
+  if (g0 == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q)
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) sdot[warp][(q * LPR + sub) * VEC + e] = dacc[q][e];
+      for (int e = 0; e < VEC; ++e) {
+        const int c = (q * LPR + sub) * VEC + e;
+        double v = 0.0;
+        for (int gg = 0; gg < G; ++gg) v += sacc[warp][q * VEC + e][gg * LPR + sub];
+        if (c < k) sdot[warp][c] = v;
+      }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < k && c < COLS; c += kSpmmThreads) {
+  for (int c = threadIdx.x; c < k; c += kSpmmThreads) {
     double s = 0.0;
     for (int w = 0; w < NW; ++w) s += sdot[w][c];
-    a.partials[(long long)blockIdx.x * k + c] = s;
+    a.partials[(long long)blockIdx.x * a.pld + c] = s;
   }
 }
 
@@ -250,37 +348,67 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
   return GCG_OK;
 }
 
-template <int LPR, int VEC>
-static int launch_nv(Ctx* c, SpmmArgs a, int nv, int grid) {
-  switch (nv) {
-    case 1: spmm_csr_kernel<LPR, VEC, 1><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
-    case 2: spmm_csr_kernel<LPR, VEC, 2><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
-    case 3: spmm_csr_kernel<LPR, VEC, 3><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
-    default: spmm_csr_kernel<LPR, VEC, 4><<<grid, kSpmmThreads, 0, c->stream>>>(a); break;
-  }
-  ++g_launches;
-  GCG_CHECK_LAUNCH();
-  return GCG_OK;
+template <int VEC, int NV>
+static void launch_one(Ctx* c, const SpmmArgs& a, int grid) {
+  spmm_csr_kernel<VEC, NV><<<grid, kSpmmThreads, 0, c->stream>>>(a);
 }
 
 template <int VEC>
-static int launch_lpr(Ctx* c, SpmmArgs a, int lpr, int nv, int grid) {
-  switch (lpr) {
-    case 4: return launch_nv<4, VEC>(c, a, nv, grid);
-    case 8: return launch_nv<8, VEC>(c, a, nv, grid);
-    case 16: return launch_nv<16, VEC>(c, a, nv, grid);
-    default: return launch_nv<32, VEC>(c, a, nv, grid);
+static void launch_vec(Ctx* c, const SpmmArgs& a, int nv, int grid) {
+  if constexpr (VEC == 4) {
+    if (nv == 1) launch_one<4, 1>(c, a, grid);
+    else launch_one<4, 2>(c, a, grid);
+  } else if constexpr (VEC == 2) {
+    switch (nv) {
+      case 1: launch_one<2, 1>(c, a, grid); break;
+      case 2: launch_one<2, 2>(c, a, grid); break;
+      case 3: launch_one<2, 3>(c, a, grid); break;
+      default: launch_one<2, 4>(c, a, grid); break;
+    }
+  } else {
+    switch (nv) {
+      case 1: launch_one<1, 1>(c, a, grid); break;
+      case 2: launch_one<1, 2>(c, a, grid); break;
+      case 3: launch_one<1, 3>(c, a, grid); break;
+      default: launch_one<1, 4>(c, a, grid); break;
+    }
   }
 }
 
-static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static inline bool aligned_to(const void* p, int bytes) {
+  return ((uintptr_t)p % (uintptr_t)bytes) == 0;
+}
 
-// exactly one wave of kSpmmMinBlocks CTAs per SM (grid-stride over rows)
-int spmm_grid(Ctx* c, long long n) { return grid_for(n, 64, kSpmmMinBlocks, c->num_sms); }
+// grid for a variant: one wave of its resident CTAs (grid-stride over rows)
+static int spmm_grid_for(Ctx* c, long long n, int doubles) {
+  return grid_for(n, 64, spmm_min_blocks(doubles), c->num_sms);
+}
+// upper bound over all variants (partials sizing in block CG)
+int spmm_grid(Ctx* c, long long n) { return spmm_grid_for(c, n, 1); }
 
-// One SpMM over all k columns, split into passes of at most 256 columns.  With
-// dot_mode != 0 and `partials` given, per-CTA partials ([grid][k], k <= 256)
-// are left for the caller to reduce; otherwise they are reduced into `dots`.
+// Lane-group shape for `chunks` VEC-wide column chunks: NV chunks per lane,
+// LPR = ceil(chunks / NV) lanes per row (any 1..32), G = 32 / LPR rows per warp.
+// Maximises the useful fraction (G LPR / 32) (chunks / (LPR NV)); ties keep the
+// smaller NV (fewer registers, more resident warps).
+static double spmm_shape(int chunks, int vec, int* nv_out, int* lpr_out) {
+  double best = -1.0;
+  for (int nv = 1; nv <= 4 && nv * vec <= kSpmmMaxSlots; ++nv) {
+    const int lpr = (chunks + nv - 1) / nv;
+    if (lpr > 32) continue;
+    const int g = 32 / lpr;
+    const double eff = (double)(g * lpr) / 32.0 * (double)chunks / (double)(lpr * nv);
+    if (eff > best + 1e-9) {
+      best = eff;
+      *nv_out = nv;
+      *lpr_out = lpr;
+    }
+  }
+  return best;
+}
+
+// One SpMM over all k columns, in even passes of at most 256 columns.  With
+// dot_mode != 0 and `partials` given, per-CTA partials ([grid][k]) are left for
+// the caller to reduce; otherwise they are reduced into `dots` per pass.
 int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                      const double* val, int k, const double* X, long long ldx, double alpha,
                      double gamma, const double* Z, long long ldz, double beta, const double* Yin,
@@ -288,31 +416,59 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
                      long long ldw, double* dots, double* partials_ext, int* grid_out,
                      const int* skip) {
   if (n <= 0 || k <= 0) return GCG_OK;
-  constexpr int kMaxPass = 256;
-  const int grid = spmm_grid(c, n);
-  if (grid_out) *grid_out = grid;
-  if (partials_ext && k > kMaxPass) return GCG_ERR_ARG;
   double* partials = partials_ext;
   if (dot_mode && !partials) {
-    GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * (size_t)kMaxPass));
+    GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)spmm_grid(c, n) * kSpmmMaxPass));
     partials = (double*)c->partials.ptr;
   }
-  for (int c0 = 0; c0 < k; c0 += kMaxPass) {
-    const int kc = (k - c0) < kMaxPass ? (k - c0) : kMaxPass;
-    const bool vec2 = (kc % 2 == 0) && (ldx % 2 == 0) && aligned16(X + c0);
-    const int vec = vec2 ? 2 : 1;
-    const int lanes_needed = (kc + vec - 1) / vec;
-    // small lane groups keep more rows (independent gather chains) per warp:
-    // about two column chunks per lane, at most four
-    int lpr = 4;
-    while (lpr < 32 && 2 * lpr < lanes_needed) lpr <<= 1;
-    const int nv = (lanes_needed + lpr - 1) / lpr;
+  int c0 = 0;
+  while (c0 < k) {
+    const int rest = k - c0;
+    // widest access every row start of X allows (rows of X must stay VEC-aligned)
+    static const int vec_cap = getenv("GCG_SPMM_VEC") ? atoi(getenv("GCG_SPMM_VEC")) : 4;
+    static const int contig = getenv("GCG_SPMM_ORDER") ? atoi(getenv("GCG_SPMM_ORDER")) : 0;
+    int vec = 1;
+    if (vec_cap >= 4 && ldx % 4 == 0 && aligned_to(X + c0, 32) && rest >= 4) vec = 4;
+    else if (vec_cap >= 2 && ldx % 2 == 0 && aligned_to(X + c0, 16) && rest >= 2) vec = 2;
+    // even passes of at most 32 lanes x NV x VEC columns
+    auto max_cols = [](int v) { return 32 * v * (kSpmmMaxSlots / v < 4 ? kSpmmMaxSlots / v : 4); };
+    const int npass = (rest + max_cols(vec) - 1) / max_cols(vec);
+    int kc = (rest + npass - 1) / npass;
+    kc = (kc + vec - 1) / vec * vec;
+    if (kc > rest) kc = rest;
+    if (kc % vec) {
+      if (kc > vec) kc -= kc % vec;  // ragged tail goes to a narrower next pass
+      else vec = 1;
+    }
+    int nv = 1, lpr = 1;
+    double eff = spmm_shape((kc + vec - 1) / vec, vec, &nv, &lpr);
+    if (vec > 1) {  // half-width accesses can tile the row and warp better (k = 160)
+      int nv2 = 1, lpr2 = 1;
+      const double eff2 = spmm_shape((kc + vec / 2 - 1) / (vec / 2), vec / 2, &nv2, &lpr2);
+      if (eff2 > eff + 1e-9) {
+        vec /= 2;
+        nv = nv2;
+        lpr = lpr2;
+        eff = eff2;
+      }
+    }
+    int grid = spmm_grid_for(c, n, nv * vec);
+    long long rpc = 0;
+    if (contig) {
+      const long long step = 8LL * (32 / lpr);  // rows per CTA step (8 warps)
+      rpc = ((n + grid - 1) / grid + step - 1) / step * step;
+      grid = (int)((n + rpc - 1) / rpc);
+    }
+    if (grid_out) *grid_out = grid;
     SpmmArgs a;
     a.n = n;
     a.rowptr = rowptr;
     a.colidx = colidx;
     a.val = val;
     a.k = kc;
+    a.lpr = lpr;
+    a.gpw = 32 / lpr;
+    a.rpc = rpc;
     a.X = X + c0;
     a.ldx = ldx;
     a.alpha = alpha;
@@ -327,8 +483,14 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     a.dot_mode = dot_mode;
     a.W = W ? W + c0 : nullptr;
     a.ldw = ldw;
-    a.partials = partials;
+    a.partials = partials_ext ? partials + c0 : partials;
+    a.pld = partials_ext ? k : kc;
     a.skip = skip;
+    const int vb = 8 * vec;
+    a.vepi = aligned_to(a.Y, vb) && ldy % vec == 0 &&
+             (gamma == 0.0 || (aligned_to(a.Z, vb) && ldz % vec == 0)) &&
+             (beta == 0.0 || (aligned_to(a.Yin, vb) && ldyin % vec == 0)) &&
+             (dot_mode != 1 || (aligned_to(a.W, vb) && ldw % vec == 0));
     // algorithmic bytes: index/value stream + X once + Y once + each extra distinct stream
     double bytes = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * kc;
     if (gamma != 0.0 && Z != X) bytes += 8.0 * n * kc;
@@ -336,13 +498,19 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     if (dot_mode == 1 && W != X && W != Z) bytes += 8.0 * n * kc;
     const int ps = prof_start(c, PROF_SPMM, bytes);
     a.prof_skipped = prof_skip_slot(c, ps);
-    const int s = vec2 ? launch_lpr<2>(c, a, lpr, nv, grid) : launch_lpr<1>(c, a, lpr, nv, grid);
+    switch (vec) {
+      case 4: launch_vec<4>(c, a, nv, grid); break;
+      case 2: launch_vec<2>(c, a, nv, grid); break;
+      default: launch_vec<1>(c, a, nv, grid); break;
+    }
+    ++g_launches;
+    GCG_CHECK_LAUNCH();
     prof_stop(c, ps);
-    if (s != GCG_OK) return s;
     if (dot_mode && !partials_ext) {
       GCG_TRY(reduce_partials(c, partials, grid, kc, dots + c0, 1, 0));
       ++g_launches;
     }
+    c0 += kc;
   }
   return GCG_OK;
 }

@@ -90,6 +90,34 @@ def test_spmm_strided_views_and_epilogue(dev):
     assert rel_err(host(dots2), (w2 * w2).sum(0)) <= 1e-12
 
 
+@pytest.mark.parametrize("k", [4, 20, 22, 40, 64, 100, 160, 250])
+@pytest.mark.parametrize("diag", [True, False])
+def test_spmm_self_epilogue(dev, k, diag):
+    """The block-CG forms: Z = W = X (diagonal gather reused), 256-bit rows, ragged tails,
+    and a pattern without stored diagonal (fallback loads)."""
+    a = P.laplacian_3d(9).tocsr()
+    if not diag:
+        a = (a - scipy.sparse.diags(a.diagonal())).tocsr()
+        a.eliminate_zeros()
+    n = a.shape[0]
+    A = DeviceCsr.from_scipy(dev, a)
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((n, k))
+    yin = rng.standard_normal((n, k))
+    xd = rm(dev, x)
+    y = dev.empty(n, k)
+    dots = dev.empty(k)
+    D.spmm(dev, A, xd, y, alpha=1.0, gamma=-0.7, Z=xd, dot_mode=1, W=xd, dots=dots)
+    want = a @ x - 0.7 * x
+    assert rel_err(host(y), want) <= 1e-13
+    assert rel_err(host(dots), (want * x).sum(0)) <= 1e-12
+    D.spmm(dev, A, xd, y, alpha=-1.0, gamma=0.3, Z=xd, beta=1.0, Yin=rm(dev, yin), dot_mode=2,
+           dots=dots)
+    want = yin - (a @ x) + 0.3 * x
+    assert rel_err(host(y), want) <= 1e-13
+    assert rel_err(host(dots), (want * want).sum(0)) <= 1e-12
+
+
 @pytest.mark.parametrize("n,k1,k2", [(1, 1, 1), (23, 4, 3), (5000, 6, 4), (262144, 200, 20),
                                       (100003, 80, 80), (4097, 17, 33), (70000, 120, 7)])
 def test_gram_vs_numpy(dev, n, k1, k2):
