@@ -219,6 +219,7 @@ def block_cg(apply, rhs, x0, max_iters=30, rel_tol=0.01):
 class OrthParams:
     """orth.OrthConfig defaults (orth.py:48-62)."""
 
+    block_width: int | None = None
     svd_leaf: int | None = None
     reorth_tol: float = 1e-10
     dependence_tol: float = 1e-10
@@ -226,6 +227,7 @@ class OrthParams:
 
 
 DGKS = 0.5  # orth.py:43
+REPAIR = 1e-8  # orth.py:45
 
 
 class _State:
@@ -380,6 +382,106 @@ def orth_against(x, basis, b=None, prm=None):
         if kept <= 0:
             raise AllDependentError("all columns dependent")
     return OrthResult(kept, replaced, st.nred + inner.reduction_count + extra)
+
+
+def _seed_norms(st):
+    """orth.py:114-119: without B, every squared column norm joins the first round."""
+    if st.b is None:
+        sl = slice(st.lo0, st.end)
+        st.d[sl] = np.einsum("ij,ij->j", st.x[:, sl], st.x[:, sl])
+        st.bump_scale(st.d[sl])
+
+
+def mgs_block(st, j0, j1):
+    """Column-at-a-time orthonormalisation of x[:, j0:j1] (orth.py:229-269): one fused
+    round per column (its squared B-norm + projections onto the rest of the block)."""
+    prm = st.prm
+    j = j0
+    while j < min(j1, st.end):
+        j1 = min(j1, st.end)
+        c = st.x[:, j:j + 1]
+        bc = st.bmul(c)
+        nn = float(np.vdot(c, bc))
+        proj = st.x[:, j + 1:j1].T @ bc
+        st.nred += 1
+        if j == st.lo0 and st.nred == 1:
+            _seed_norms(st)
+        st.bump_scale([nn])
+        if nn <= prm.dependence_tol * st.scale:
+            if not st.rear_fill(j):
+                return
+            if j > st.lo0:
+                deflate(st, st.x[:, st.lo0:j], j, j + 1)
+            continue
+        tracked = st.d[j]
+        if np.isfinite(tracked) and nn <= REPAIR * max(tracked, st.scale):
+            deflate(st, st.x[:, st.lo0:j], j, j + 1)
+            st.d[j] = np.nan
+            continue
+        s = 1.0 / np.sqrt(nn)
+        c *= s
+        if proj.size:
+            st.x[:, j + 1:j1] -= c @ (proj.T * s)
+            gone = (proj[:, 0] * s) ** 2
+            st.d[j + 1:j1] = np.maximum(st.d[j + 1:j1] - gone, 0.0)
+        st.d[j] = 1.0
+        j += 1
+
+
+def block_deflate(st, j0, j1):
+    """Repeat-until sweep of the finished block x[:, j0:j1] out of all later columns
+    (orth.py:272-301); tracked norm estimates drive the repeat test."""
+    prm = st.prm
+    npass = 0
+    while npass < prm.max_reorth_passes:
+        j1 = min(j1, st.end)
+        later = st.x[:, j1:st.end]
+        if later.shape[1] == 0 or j1 <= j0:
+            return
+        bb = st.bmul(st.x[:, j0:j1])
+        r = later.T @ bb
+        st.nred += 1
+        npass += 1
+        later -= st.x[:, j0:j1] @ r.T
+        if float(np.abs(r).max(initial=0.0)) <= prm.reorth_tol:
+            return
+        gone = np.einsum("ij,ij->i", r, r)
+        tracked = st.d[j1:st.end]
+        with np.errstate(invalid="ignore"):
+            risky = gone > DGKS * np.maximum(tracked, 1e-300)
+        st.d[j1:st.end] = np.maximum(tracked - gone, 0.0)
+        if not bool(np.any(risky[np.isfinite(tracked)])):
+            return
+
+
+def modified_block_orth(x, x0=None, b=None, prm=None):
+    """Alg. 2 (orth.py:304-336): optional deflation against x0, then per block of width
+    bw an MGS pass and a sweep of the block out of the remaining columns."""
+    prm = prm or OrthParams()
+    m = x.shape[1]
+    if m == 0:
+        return OrthResult(0, [], 0)
+    if x0 is not None and x0.shape[1] == 0:
+        x0 = None
+    if x0 is not None and x0.shape[0] != x.shape[0]:
+        raise OracleError("basis row count differs")
+    bw = prm.block_width if prm.block_width is not None else min(max(m // 4, 1), 200)
+    if bw < 1:
+        raise OracleError(f"block width {bw}")
+    st = _State(x, b, prm, 0, m)
+    if x0 is not None:
+        deflate(st, x0, 0, m)
+    j0 = 0
+    while j0 < st.end:
+        j1 = min(j0 + bw, st.end)
+        mgs_block(st, j0, j1)
+        j1 = min(j1, st.end)
+        if j1 < st.end:
+            block_deflate(st, j0, j1)
+        j0 = j1
+    if st.end <= 0:
+        raise AllDependentError("all columns dependent")
+    return OrthResult(st.end, st.replaced, st.nred)
 
 
 # ---------------------------------------------------------------------------

@@ -15,7 +15,7 @@ from .errors import (
     NoConvergence,
     Unsupported,
 )
-from .orth import OrthConfig, OrthOutcome, orth_against, recursive_orth_svd
+from .orth import OrthConfig, OrthOutcome, modified_block_orth, orth_against, recursive_orth_svd
 from .solver import (
     IterationRecord,
     SolverConfig,
@@ -37,6 +37,7 @@ __all__ = [
     "OrthConfig",
     "OrthOutcome",
     "recursive_orth_svd",
+    "modified_block_orth",
     "orth_against",
     "GcgError",
     "InvalidMatrix",

@@ -1,9 +1,11 @@
-"""B-orthogonalisation on device: Alg. 3 (recursive SVD-based) and orth_against.
+"""B-orthogonalisation on device: Alg. 3 (recursive SVD-based), orth_against and
+Alg. 2 (block modified Gram-Schmidt).
 
 Reference: orth.py — `_deflate_against` (:124-152), `_leaf_svqb` (:155-188),
 `_recurse_svd` (:191-204), `recursive_orth_svd` (:207-226), `orth_against`
 (:339-372), `_Ctx.pull_rear` (:95-108), `OrthConfig` (:48-62),
-`OrthOutcome` (:65-69).
+`OrthOutcome` (:65-69); Alg. 2: `_seed_local_norms` (:114-119), `_mgs_block`
+(:229-269), `_block_deflate` (:272-301), `modified_block_orth` (:304-336).
 
 The control flow (recursion, repeat-until tests, dependent-column
 replacement, reduction counts) is the reference's, run on the host; every
@@ -29,13 +31,17 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import numpy as np
+import torch
+
 from . import device as D
 from .errors import AllDependent, InvalidRange, InvalidShape
 from .mvops import LocalOps
 
-__all__ = ["OrthConfig", "OrthOutcome", "recursive_orth_svd", "orth_against"]
+__all__ = ["OrthConfig", "OrthOutcome", "modified_block_orth", "recursive_orth_svd", "orth_against"]
 
 _DGKS_RATIO = 0.5  # orth.py:43
+_REPAIR_RATIO = 1e-8  # orth.py:45
 
 
 @dataclass
@@ -97,6 +103,16 @@ class _State:
         self.replaced = []
         self.leaf_width = 16
         self.status = self.dev.empty(4)
+        # Alg. 2 only: host copies of the tracked squared B-norms and the largest
+        # one seen (orth.py:87-88); Alg. 3 never reads them, so it skips the reads
+        self.track = False
+        self.scale = 0.0
+        self.d = np.full(x.shape[1], np.nan)
+
+    def note_scale(self, vals):
+        top = float(np.max(vals, initial=0.0))
+        if top > self.scale:
+            self.scale = top
 
     def bdot(self, y):
         return y if self.b is None else self.ops.apply(self.b, y)
@@ -111,6 +127,7 @@ class _State:
             self.active_end -= 1
             D.copy(self.dev, self.x[:, self.active_end:self.active_end + 1],
                    self.x[:, slot:slot + 1])
+            self.d[slot] = self.d[self.active_end]
             return True
         self.active_end = slot
         return False
@@ -141,7 +158,16 @@ def _deflate_against(st, basis, lo, hi):
         passes += 1
         D.lincomb(dev, basis, coef, target, alpha=-1.0, beta=1.0)
         D.deflate_status(dev, coef, dnew, _DGKS_RATIO, st.status)
-        rmax, risky = st.read_status(2)
+        if st.track:
+            lost = dev.empty(w)
+            D.col_dots(dev, coef, coef, lost)  # coef is replicated: a local reduction
+            rec = torch.cat([st.ops.broadcast(st.status)[:2], dnew, lost]).cpu().numpy()
+            rmax, risky = float(rec[0]), rec[1]
+            dn, ls = rec[2:2 + w], rec[2 + w:]
+            st.note_scale(dn)
+            st.d[lo:hi] = np.maximum(dn if rmax <= cfg.reorth_tol else dn - ls, 0.0)
+        else:
+            rmax, risky = st.read_status(2)
         if rmax <= cfg.reorth_tol:
             return passes
         if not risky:
@@ -221,6 +247,127 @@ def recursive_orth_svd(ops, x, s=None, e=None, b=None, cfg=None):
     if kept <= 0:
         raise AllDependent("every column in the block is linearly dependent")
     return OrthOutcome(kept, st.replaced, st.reductions)
+
+
+def _seed_local_norms(st):
+    """orth.py:114-119: without B the squared column norms join the first round."""
+    if st.b is None:
+        lo, hi = st.start, st.active_end
+        dd = st.dev.empty(hi - lo)
+        st.ops.col_dots(st.x[:, lo:hi], st.x[:, lo:hi], dd)
+        st.d[lo:hi] = dd.cpu().numpy()
+        st.note_scale(st.d[lo:hi])
+
+
+def _mgs_block(st, start, stop):
+    """Column-by-column orthonormalisation of x[:, start:stop] (orth.py:229-269).
+
+    One fused reduction per column: the Gram of x[:, j:stop] against B x_j gives
+    the squared norm (first entry) and the projections onto the rest of the
+    block; the normalisation and the rank-1 removal are device kernels."""
+    cfg, dev, ops = st.cfg, st.dev, st.ops
+    j = start
+    while j < min(stop, st.active_end):
+        stop = min(stop, st.active_end)
+        col = st.x[:, j:j + 1]
+        bcol = st.bdot(col)
+        w = stop - j
+        g = dev.empty(w, 1)
+        ops.gram(st.x[:, j:stop], bcol, g)
+        st.reductions += 1
+        if j == st.start and st.reductions == 1:
+            _seed_local_norms(st)
+        gh = g[:, 0].cpu().numpy()
+        nrm2, fwd = float(gh[0]), gh[1:]
+        st.note_scale([nrm2])
+        if nrm2 <= cfg.dependence_tol * st.scale:
+            if not st.pull_rear(j):
+                return
+            if j > st.start:
+                _deflate_against(st, st.x[:, st.start:j], j, j + 1)
+            continue
+        known = st.d[j]
+        if np.isfinite(known) and nrm2 <= _REPAIR_RATIO * max(known, st.scale):
+            _deflate_against(st, st.x[:, st.start:j], j, j + 1)
+            st.d[j] = np.nan
+            continue
+        inv = 1.0 / np.sqrt(nrm2)
+        D.col_scale(dev, torch.full((1,), inv, dtype=torch.float64, device=dev.device), col)
+        if fwd.size:
+            cf = fwd * inv
+            D.lincomb(dev, col, torch.from_numpy(cf[None, :].copy()).to(dev.device),
+                      st.x[:, j + 1:stop], alpha=-1.0, beta=1.0)
+            st.d[j + 1:stop] = np.maximum(st.d[j + 1:stop] - cf * cf, 0.0)
+        st.d[j] = 1.0
+        j += 1
+
+
+def _block_deflate(st, start, stop):
+    """Repeat-until removal of the finished block from every later column (orth.py:272-301).
+
+    R' = (rest' B block)' is written transposed by the Gram kernel, so the
+    update rest -= block R' is one LinComb; the repeat test uses the host-tracked
+    norm estimates as in the reference."""
+    cfg, dev, ops = st.cfg, st.dev, st.ops
+    passes = 0
+    while passes < cfg.max_reorth_passes:
+        stop = min(stop, st.active_end)
+        nrest = st.active_end - stop
+        if nrest <= 0 or stop <= start:
+            return
+        blk = st.x[:, start:stop]
+        rest = st.x[:, stop:st.active_end]
+        bblock = st.bdot(blk)
+        rt = dev.empty(stop - start, nrest)
+        ops.gram(rest, bblock, rt, transpose_out=True)
+        st.reductions += 1
+        passes += 1
+        D.lincomb(dev, blk, rt, rest, alpha=-1.0, beta=1.0)
+        lost = dev.empty(nrest)
+        D.col_dots(dev, rt, rt, lost)
+        D.deflate_status(dev, rt, lost, _DGKS_RATIO, st.status)  # status[0] = max |R|
+        rec = torch.cat([st.status[:1], lost]).cpu().numpy()
+        if float(rec[0]) <= cfg.reorth_tol:
+            return
+        lost_h = rec[1:]
+        known = st.d[stop:st.active_end]
+        with np.errstate(invalid="ignore"):
+            risky = lost_h > _DGKS_RATIO * np.maximum(known, 1e-300)
+        st.d[stop:st.active_end] = np.maximum(known - lost_h, 0.0)
+        if not bool(np.any(risky[np.isfinite(known)])):
+            return
+
+
+def modified_block_orth(ops, x, x0=None, b=None, cfg=None):
+    """Alg. 2: B-orthonormalise device block ``x`` in place, optionally against a fixed
+    B-orthonormal basis ``x0`` (orth.py:304-336).  Kept columns end in x[:, :num_kept]."""
+    ops = _as_ops(ops)
+    cfg = cfg if cfg is not None else OrthConfig()
+    m = x.shape[1]
+    if m == 0:
+        return OrthOutcome(0, [], 0)
+    if x0 is not None and x0.shape[1] == 0:
+        x0 = None
+    if x0 is not None and x0.shape[0] != x.shape[0]:
+        raise InvalidShape(f"basis dim {x0.shape[0]} != block dim {x.shape[0]}")
+    bw = cfg.block_width if cfg.block_width is not None else min(max(m // 4, 1), 200)
+    if bw < 1:
+        raise InvalidShape(f"block_width must be >= 1, got {bw}")
+    st = _State(ops, x, b, cfg, 0, m)
+    st.track = True
+    if x0 is not None:
+        _deflate_against(st, x0, 0, m)
+    start = 0
+    while start < st.active_end:
+        stop = min(start + bw, st.active_end)
+        _mgs_block(st, start, stop)
+        stop = min(stop, st.active_end)
+        if stop < st.active_end:
+            _block_deflate(st, start, stop)
+        start = stop
+    if st.active_end <= 0:
+        raise AllDependent("every column in the block is linearly dependent")
+    return OrthOutcome(st.active_end, st.replaced, st.reductions)
 
 
 def orth_against(ops, x, basis, b=None, cfg=None):

@@ -3,7 +3,8 @@
 Run in the build container, where the reference is available — either built
 into oracle/_ref (oracle/build_ref.sh) or importable from /root/reference:
 
-    python tests/golden/make_golden.py            # small cases -> golden.npz
+    python tests/golden/make_golden.py            # small cases -> golden.npz (+ Alg. 2)
+    python tests/golden/make_golden.py --alg2     # Alg. 2 cases only -> golden_alg2.npz
     python tests/golden/make_golden.py --cfg 2    # BASELINE config 2 (~8 min)
     python tests/golden/make_golden.py --cfg 3    # BASELINE config 3 (~1-2 h)
 
@@ -201,10 +202,58 @@ def cfg_run(cfg):
     )
 
 
+def alg2_cases():
+    """modified_block_orth (Alg. 2) inputs following test_orth.py:46-67, 145-178."""
+    def blk(n, m, seed):
+        return np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, (n, m)))
+    cases = [
+        ("m8_b2", blk(64, 8, 101), None, None, dict(block_width=2)),
+        ("m32_b2", blk(256, 32, 202), None, None, dict(block_width=2)),
+        ("m8_default", blk(64, 8, 103), None, None, {}),
+    ]
+    x = blk(40, 8, 21)
+    x[:, 3] = x[:, 1]
+    cases.append(("dup_col", x, None, None, dict(block_width=2)))
+    x = blk(30, 6, 23)
+    x[:, 4] = 0.0
+    cases.append(("zero_col", x, None, None, dict(block_width=3)))
+    cases.append(("with_b", blk(50, 8, 7), None, "tridiag50", {}))
+    basis = blk(120, 10, 61)
+    R.recursive_orth_svd(basis)
+    cases.append(("with_x0", blk(120, 24, 62), basis, None, dict(block_width=5)))
+    cases.append(("m96_b16", blk(600, 96, 63), None, None, dict(block_width=16)))
+    return cases
+
+
+def spd_tridiag(n):
+    return scipy.sparse.diags([np.ones(n - 1), 4.0 * np.ones(n), np.ones(n - 1)], [-1, 0, 1],
+                              format="csr")
+
+
+def alg2(out):
+    for tag, x, x0, bname, kw in alg2_cases():
+        b = CsrOperator(spd_tridiag(50)) if bname == "tridiag50" else None
+        out[f"{tag}_in"] = x.copy(order="F")
+        if x0 is not None:
+            out[f"{tag}_x0"] = x0
+        r = R.modified_block_orth(x, x0=x0, b=b, cfg=R.OrthConfig(**kw))
+        out[f"{tag}_out"] = x
+        out[f"{tag}_meta"] = np.array([r.num_kept, r.reduction_count])
+        out[f"{tag}_replaced"] = np.array(r.replaced_indices, dtype=np.int64)
+        print(f"alg2 {tag}: kept={r.num_kept} reductions={r.reduction_count}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=0, help="full BASELINE config run (2 or 3)")
+    ap.add_argument("--alg2", action="store_true", help="only the Alg. 2 vectors -> golden_alg2.npz")
     args = ap.parse_args()
+    if args.alg2 or not args.cfg:
+        o2 = {}
+        alg2(o2)
+        np.savez_compressed(os.path.join(HERE, "golden_alg2.npz"), **o2)
+        if args.alg2:
+            return
     if args.cfg:
         res = cfg_run(args.cfg)
         with open(os.path.join(HERE, f"golden_cfg{args.cfg}.json"), "w") as f:

@@ -104,3 +104,25 @@ def test_analytic_eigenvalues_match_dense():
     a = P.stencil27(8).toarray()
     w = np.linalg.eigvalsh(a)[:12]
     assert np.abs(w - P.analytic_eigenvalues(5, 12, scale=8)).max() < 1e-12
+
+
+@pytest.mark.parametrize("tag", ["m8_b2", "m32_b2", "m8_default", "dup_col", "zero_col", "with_b",
+                                 "with_x0", "m96_b16"])
+def test_modified_block_orth(golden_alg2, tag):
+    """Alg. 2 restatement vs the reference run (counts m + m/b - 1, test_orth.py:46-67)."""
+    from tests.conftest import ALG2_KW
+
+    g = golden_alg2
+    x = g[f"{tag}_in"].copy(order="F")
+    x0 = g[f"{tag}_x0"] if f"{tag}_x0" in g else None
+    b = None
+    if tag == "with_b":
+        n = x.shape[0]
+        import scipy.sparse
+
+        b = O.Csr(scipy.sparse.diags([np.ones(n - 1), 4.0 * np.ones(n), np.ones(n - 1)], [-1, 0, 1],
+                                     format="csr"))
+    r = O.modified_block_orth(x, x0=x0, b=b, prm=O.OrthParams(**ALG2_KW[tag]))
+    assert [r.num_kept, r.reduction_count] == list(g[f"{tag}_meta"])
+    assert r.replaced_indices == list(g[f"{tag}_replaced"])
+    assert np.array_equal(x, g[f"{tag}_out"])
