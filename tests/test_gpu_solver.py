@@ -123,6 +123,27 @@ def test_cfg2_baseline_against_reference_run():
     assert abs(rep.iterations - ref["iterations"]) <= 5
 
 
+@pytest.mark.slow
+def test_cfg3_baseline_against_reference_run():
+    """BASELINE cfg3 (P1 FEM, generalized, nev=200) vs the reference's full run (43 iters,
+    2915 s on 8 cores, tests/golden/golden_cfg3.json).  No closed form exists; the
+    reference eigenvalues and the north-star residual bound are the targets."""
+    path = os.path.join(HERE, "golden", "golden_cfg3.json")
+    if not os.path.exists(path):
+        pytest.skip("golden_cfg3.json not generated")
+    ref = json.load(open(path))
+    pr = P.baseline_problem(3)
+    rep = gcg_solve(pr.a, pr.b, SolverConfig(num_eigen=200, tol=1e-8, seed=0, init="normal",
+                                             residual="relative", validate=False))
+    want = np.array(ref["eigenvalues"])
+    assert rep.status == "converged"
+    assert np.abs(rep.eigenvalues - want).max() / np.abs(want).max() <= 1e-9
+    assert rep.residuals.max() <= 1e-8
+    assert abs(rep.iterations - ref["iterations"]) <= max(4, ref["iterations"] // 7)
+    # P1 eigenvalues are upper bounds of the continuum ones (3 pi^2 smallest, SURVEY §8(c))
+    assert rep.eigenvalues[0] >= 3 * np.pi ** 2 * (1 - 1e-12)
+
+
 # ---- reference solver test cases (test_solver.py) ---------------------------------
 
 
