@@ -45,7 +45,10 @@ enum {
   GCG_ERR_CUDA = 2,    /* CUDA runtime error                                    */
   GCG_ERR_SOLVER = 3,  /* dense eigensolver failure (maps to NoConvergence)     */
   GCG_ERR_ALLOC = 4,   /* device allocation failed                              */
-  GCG_ERR_NODEV = 5    /* no CUDA device                                        */
+  GCG_ERR_NODEV = 5,   /* no CUDA device                                        */
+  GCG_ERR_IO = 6,      /* file could not be read (maps to IoError)              */
+  GCG_ERR_PARSE = 7,   /* malformed input file (maps to ParseError + line)      */
+  GCG_ERR_UNSUPPORTED = 8 /* well-formed but unhandled input (Unsupported)      */
 };
 
 #define GCG_ABI_VERSION 1
@@ -219,6 +222,28 @@ int gcg_max_abs_diff(void* ctx, int64_t m, int64_t n, const double* A, int64_t l
 int gcg_ritz_residuals(void* ctx, int64_t n, int64_t k, const double* AX, int64_t ldax,
                        const double* X, int64_t ldx, const double* BX, int64_t ldbx,
                        const double* lam, int mode, double* out);
+
+/* ---- MatrixMarket ingestion (host; io.py:108-216 read_matrix_market) ------
+ * gcg_mm_open parses the whole file (coordinate entries tokenised by
+ * `nthreads` host threads, 0 = all cores) into a handle; on a malformed file it
+ * returns GCG_ERR_PARSE with info->err_line (1-based) and info->err_msg set,
+ * GCG_ERR_UNSUPPORTED / GCG_ERR_IO likewise, and no handle.  gcg_mm_fetch
+ * copies the parsed data into caller buffers: coordinate -> nentries (row,
+ * col, value) triples, 0-based, symmetric storage already mirrored (duplicates
+ * NOT yet summed); array -> the dense nrows x ncols matrix, column-major. */
+typedef struct gcg_mm_info {
+  int64_t nrows, ncols;
+  int64_t nentries;   /* coordinate: triples after mirroring; array: nrows * ncols */
+  int32_t format;     /* 0 coordinate, 1 array */
+  int32_t symmetric;
+  int32_t err_kind;   /* 0 none, 1 parse, 2 unsupported, 3 io */
+  int32_t pad_;
+  int64_t err_line;
+  char err_msg[240];
+} gcg_mm_info;
+int gcg_mm_open(const char* path, int nthreads, void** handle, gcg_mm_info* info);
+int gcg_mm_fetch(void* handle, int64_t* rows, int64_t* cols, double* vals);
+void gcg_mm_close(void* handle);
 
 #ifdef __cplusplus
 }

@@ -12,8 +12,19 @@ from .errors import (
     InvalidMatrix,
     InvalidRange,
     InvalidShape,
+    IoError,
     NoConvergence,
+    ParseError,
+    UnknownGenerator,
     Unsupported,
+)
+from .io import (
+    RunRecord,
+    generate_builtin,
+    history_rows,
+    read_matrix_market,
+    write_history,
+    write_matrix_market,
 )
 from .orth import OrthConfig, OrthOutcome, modified_block_orth, orth_against, recursive_orth_svd
 from .solver import (
@@ -46,4 +57,13 @@ __all__ = [
     "NoConvergence",
     "AllDependent",
     "Unsupported",
+    "ParseError",
+    "UnknownGenerator",
+    "IoError",
+    "read_matrix_market",
+    "write_matrix_market",
+    "generate_builtin",
+    "RunRecord",
+    "write_history",
+    "history_rows",
 ]

@@ -59,8 +59,27 @@ _SIGS = {
     "gcg_count_le": [_ptr, _i64, _ptr, _dbl, _ptr],
     "gcg_scale_rsqrt": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _ptr, _i64],
     "gcg_ritz_residuals": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
+    "gcg_mm_open": [C.c_char_p, _int, C.POINTER(_ptr), _ptr],
+    "gcg_mm_fetch": [_ptr, _ptr, _ptr, _ptr],
+    "gcg_mm_close": [_ptr],
 }
-_RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64}
+_RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64, "gcg_mm_close": None}
+
+
+class MMInfo(C.Structure):
+    """gcg_mm_info (include/gcgb200.h)."""
+
+    _fields_ = [
+        ("nrows", C.c_int64),
+        ("ncols", C.c_int64),
+        ("nentries", C.c_int64),
+        ("format", C.c_int32),
+        ("symmetric", C.c_int32),
+        ("err_kind", C.c_int32),
+        ("pad_", C.c_int32),
+        ("err_line", C.c_int64),
+        ("err_msg", C.c_char * 240),
+    ]
 
 EXPORTED = tuple(_SIGS)
 

@@ -178,6 +178,9 @@ const char* gcg_status_string(int status) {
     case GCG_ERR_SOLVER: return "dense eigensolver failure";
     case GCG_ERR_ALLOC: return "device allocation failed";
     case GCG_ERR_NODEV: return "no CUDA device";
+    case GCG_ERR_IO: return "file could not be read";
+    case GCG_ERR_PARSE: return "malformed input file";
+    case GCG_ERR_UNSUPPORTED: return "unsupported input";
     default: return "unknown status";
   }
 }

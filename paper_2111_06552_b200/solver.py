@@ -21,7 +21,6 @@ Two parity switches that the reference does not have:
 from __future__ import annotations
 
 import math
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -140,16 +139,35 @@ def _stagnation_flag(history, window):
 
 
 class _Timer:
-    def __init__(self, enabled):
-        self.enabled = enabled
+    """Per-step GPU time of one iteration (the reference's t_step* wall clocks,
+    solver.py:269-445): a CUDA event is recorded on the solver stream at every step
+    boundary and the intervals are resolved once after the loop, so the timings
+    measure device work and add no host synchronisation inside the iteration.
+    Disabled (all zero) in deterministic mode, as in the reference."""
+
+    def __init__(self, enabled, stream):
+        self.enabled = enabled and stream is not None
         self.marks = {k: 0.0 for k in _TIMING_KEYS}
-        self._last = time.perf_counter()
+        self._stream = stream
+        self._laps = []
+        self._last = self._event() if self.enabled else None
+
+    def _event(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self._stream)
+        return e
 
     def lap(self, key):
-        now = time.perf_counter()
         if self.enabled:
-            self.marks[key] += now - self._last
-        self._last = now
+            now = self._event()
+            self._laps.append((key, self._last, now))
+            self._last = now
+
+    def resolve(self):
+        for key, e0, e1 in self._laps:
+            e1.synchronize()
+            self.marks[key] += e0.elapsed_time(e1) / 1e3
+        self._laps = []
 
 
 class _Solve:
@@ -362,13 +380,15 @@ def gcg_solve_ops(ops, cfg, x0=None):
     store_x, store_vals = [], []
     history = []
     pending_cg = []
+    timers = []
     max_m = 0
     status = "max_iterations"
     iters_run = 0
 
     for it in range(1, cfg.max_gcg_iters + 1):
         iters_run = it
-        timer = _Timer(not det)
+        timer = _Timer(not det and cfg.collect_history, getattr(dev, "stream", None))
+        timers.append(timer)
         d = sx - locked
         m = d + np_ + nw
         max_m = max(max_m, m)
@@ -542,6 +562,8 @@ def gcg_solve_ops(ops, cfg, x0=None):
 
     for rec, rep in pending_cg:  # resolve CG sweep counts (one D2H each, after the loop)
         rec.cg_iterations = rep.iterations
+    for tm in timers:             # per-step GPU times (the records hold tm.marks)
+        tm.resolve()
 
     # result assembly (solver.py:447-472)
     if store_x:
