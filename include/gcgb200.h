@@ -180,6 +180,11 @@ int gcg_ritz_finish(void* ctx, int64_t k, const double* sums, const double* lam,
  * largest-|entry| made positive (dense.py:63-82).  A is read only. */
 int gcg_syev(void* ctx, int64_t m, const double* A, int64_t lda, double* w, double* V,
              int64_t ldv);
+/* eigenpairs il..iu (1-based inclusive, dense.py:86-117 sym_eig_range): w gets
+ * iu - il + 1 ascending values, V (m x (iu - il + 1), row-major) the sign-fixed
+ * vectors.  cuSOLVER syevdx with an index range (any m). */
+int gcg_syev_range(void* ctx, int64_t m, const double* A, int64_t lda, int64_t il, int64_t iu,
+                   double* w, double* V, int64_t ldv);
 /* C = alpha op(A) op(B) + beta C, op = transpose when t* != 0. */
 int gcg_dgemm(void* ctx, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
               const double* A, int64_t lda, const double* B, int64_t ldb, double beta,

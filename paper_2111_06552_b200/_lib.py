@@ -49,6 +49,7 @@ _SIGS = {
     "gcg_ritz_sums": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
     "gcg_ritz_finish": [_ptr, _i64, _ptr, _ptr, _int, _ptr],
     "gcg_syev": [_ptr, _i64, _ptr, _i64, _ptr, _ptr, _i64],
+    "gcg_syev_range": [_ptr, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _i64],
     "gcg_dgemm": [_ptr, _int, _int, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr,
                   _i64],
     "gcg_symmetrize": [_ptr, _i64, _ptr, _i64],

@@ -435,6 +435,14 @@ int gcg_syev(void* p, int64_t m, const double* A, int64_t lda, double* w, double
   return dense_syev_cusolver(c, (int)m, A, lda, w, V, ldv);
 }
 
+int gcg_syev_range(void* p, int64_t m, const double* A, int64_t lda, int64_t il, int64_t iu,
+                   double* w, double* V, int64_t ldv) {
+  Ctx* c = CTX(p);
+  const int64_t k = iu - il + 1;
+  if (!c || m <= 0 || lda < m || il < 1 || iu < il || iu > m || ldv < k) return GCG_ERR_ARG;
+  return dense_syev_range(c, (int)m, A, lda, (int)il, (int)iu, w, V, ldv);
+}
+
 int gcg_dgemm(void* p, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
               const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
               double* C, int64_t ldc) {

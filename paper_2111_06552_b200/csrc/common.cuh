@@ -114,5 +114,7 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
                       long long ldv);
 int dense_syev_cusolver(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
                         long long ldv);
+int dense_syev_range(Ctx* c, int m, const double* A, long long lda, int il, int iu, double* w,
+                     double* V, long long ldv);
 
 }  // namespace gcg

@@ -440,6 +440,43 @@ int dense_syev_cusolver(Ctx* c, int m, const double* A, long long lda, double* w
   return dense_syev_cusolver_sym(c, m, A, lda, 0, w, V, ldv);
 }
 
+// Eigenpairs il..iu (1-based inclusive) — sym_eig_range (dense.py:86-117) — by
+// cuSOLVER syevdx with an index range: the same tridiagonalisation, then only the
+// requested pairs (bisection + inverse iteration) and their back-transformation.
+// w receives iu - il + 1 values, V (m x (iu - il + 1), row-major) the sign-fixed vectors.
+int dense_syev_range(Ctx* c, int m, const double* A, long long lda, int il, int iu, double* w,
+                     double* V, long long ldv) {
+  if (m <= 0 || il < 1 || iu < il || iu > m) return GCG_ERR_ARG;
+  cusolverDnSetStream(c->solver, c->stream);
+  const size_t mat = (size_t)m * m;
+  GCG_TRY(ensure(c->dense, sizeof(double) * (mat + (size_t)m) + 64));
+  double* B = (double*)c->dense.ptr;
+  double* wall = B + mat;  // syevdx writes the selected values into the head of an m-array
+  int lwork = 0, meig = 0;
+  if (cusolverDnDsyevdx_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                   CUBLAS_FILL_MODE_LOWER, m, B, m, 0.0, 0.0, il, iu, &meig, wall,
+                                   &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return GCG_ERR_SOLVER;
+  GCG_TRY(ensure(c->eigwork, sizeof(double) * ((size_t)lwork + 8)));
+  double* work = (double*)c->eigwork.ptr;
+  int* info = (int*)(work + lwork);
+  sym_copy_kernel<<<(unsigned)((mat + 255) / 256), 256, 0, c->stream>>>(m, A, lda, B, 0, nullptr);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  if (cusolverDnDsyevdx(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                        CUBLAS_FILL_MODE_LOWER, m, B, m, 0.0, 0.0, il, iu, &meig, wall, work, lwork,
+                        info) != CUSOLVER_STATUS_SUCCESS)
+    return GCG_ERR_SOLVER;
+  const int k = iu - il + 1;
+  if (meig != k) return GCG_ERR_SOLVER;
+  GCG_TRY(cuda_status(cudaMemcpyAsync(w, wall, sizeof(double) * k, cudaMemcpyDeviceToDevice,
+                                      c->stream)));
+  vec_fix_kernel<<<k, 256, 0, c->stream>>>(m, B, V, ldv);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
 // count of vals[j] <= rel * max(max(vals), 0)  (vals ascending; searchsorted side=right)
 __global__ void count_le_kernel(int len, const double* vals, double rel, double* out) {
   __shared__ double red[32];

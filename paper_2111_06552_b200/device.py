@@ -206,6 +206,13 @@ def syev(ctx, A, w, V):
     return w, V
 
 
+def syev_range(ctx, A, il, iu, w, V):
+    """Eigenpairs il..iu (1-based inclusive) of symmetric A (gcg_syev_range)."""
+    m = A.shape[0]
+    _lib.call("gcg_syev_range", ctx.h, m, _p(A), _ld(A), int(il), int(iu), _p(w), _p(V), _ld(V))
+    return w, V
+
+
 def dgemm(ctx, A, B, Cm, ta=False, tb=False, alpha=1.0, beta=0.0):
     M = A.shape[1] if ta else A.shape[0]
     K = A.shape[0] if ta else A.shape[1]

@@ -272,6 +272,9 @@ class DistOps(LocalOps):
     def broadcast(self, t):
         return self.comm.broadcast(t, src=0)
 
+    def allgather_sum_small(self, t):
+        return self.comm.allgather_sum(self.dev, t)
+
     def _cg(self, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
         k = rhs.shape[1]
         prob, comm, dev = self.prob, self.comm, self.dev

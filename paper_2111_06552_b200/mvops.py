@@ -83,6 +83,10 @@ class LocalOps:
     def broadcast(self, t):
         return t
 
+    def allgather_sum_small(self, t):
+        """Ordered sum over ranks of a replicated-shape small tensor (identity on one GPU)."""
+        return t
+
     def host_rows(self, X):
         """Local rows of a device block as a host array (F-order)."""
         return X.t().contiguous().cpu().numpy().T

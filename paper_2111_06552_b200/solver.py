@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import device as D
-from .dense import sym_eig_full
+from .dense import sym_eig_full, sym_eig_range_split
 from .errors import AllDependent, InvalidShape
 from .mvops import LocalOps
 from .operators import DeviceProblem, as_device_problem
@@ -74,6 +74,7 @@ class SolverConfig:
     residual: str = "reference"    # "reference" | "relative" (north-star)
     validate: bool = True          # host symmetry/finiteness check of the input matrices
     return_device: bool = False    # keep eigenvectors as a device tensor (row-major n x nev)
+    rr_split: bool = False         # distributed: split the RR index range over ranks (§8(f) 4)
 
 
 @dataclass
@@ -417,11 +418,17 @@ def gcg_solve_ops(ops, cfg, x0=None):
             abar_defect = float(S.scalar[0].item())
         timer.lap("t_step3")
 
-        full = sym_eig_full(dev, abar)
-        ops.broadcast(full.values)      # every replica continues from rank 0's RR solution
-        ops.broadcast(full.vectors)
-        lam_new_dev = full.values[:d]
-        coeffs = full.vectors[:, :d]
+        if cfg.rr_split and ops.size > 1:
+            # split-range RR: rank r solves a slice of 1..d, all-gather
+            dec = sym_eig_range_split(ops, abar, 1, d)
+            full = None
+            lam_new_dev, coeffs = dec.values, dec.vectors
+        else:
+            full = sym_eig_full(dev, abar)
+            ops.broadcast(full.values)      # every replica continues from rank 0's RR solution
+            ops.broadcast(full.vectors)
+            lam_new_dev = full.values[:d]
+            coeffs = full.vectors[:, :d]
         lam_new = lam_new_dev.cpu().numpy()
         timer.lap("t_step3")
 
@@ -447,6 +454,10 @@ def gcg_solve_ops(ops, cfg, x0=None):
         iter_red = 0
         if cfg.moving and c > 0 and (c >= 2 * bs or c >= sx):
             # window slide (solver.py:325-363)
+            if full is None:  # compaction needs the whole spectrum (solver.py:332)
+                full = sym_eig_full(dev, abar)
+                ops.broadcast(full.values)
+                ops.broadcast(full.vectors)
             lam_all = full.values.cpu().numpy()
             x_all = dev.empty(nloc, m)
             D.lincomb(dev, basis, full.vectors, x_all)

@@ -56,10 +56,16 @@ CASES = [
     ("lap3d12_baseline", dict(num_eigen=24, seed=0, init="normal", residual="relative")),
     ("fem8_baseline", dict(num_eigen=10, seed=0, init="normal", residual="relative")),
     ("varcoef10_moving", dict(num_eigen=40, seed=0, moving=True, init="normal", residual="relative")),
+    # split-range RR: each rank solves a slice of the Ritz index range
+    ("lap3d12_baseline", dict(num_eigen=24, seed=0, init="normal", residual="relative",
+                              rr_split=True)),
+    ("varcoef10_moving", dict(num_eigen=40, seed=0, moving=True, init="normal", residual="relative",
+                              rr_split=True)),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("case", CASES,
+                         ids=[c[0] + ("_rrsplit" if c[1].get("rr_split") else "") for c in CASES])
 def test_two_rank_solve_matches_golden(golden, golden_meta, case):
     name, kw = case
     ctx = mp.get_context("spawn")

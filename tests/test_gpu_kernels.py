@@ -223,6 +223,28 @@ def test_syev_vs_lapack(dev, m):
     assert np.abs(V - vv).max() <= 1e-9
 
 
+@pytest.mark.parametrize("m,lo,hi,workers", [(30, 1, 30, 1), (80, 1, 64, 1), (80, 5, 17, 1),
+                                             (200, 1, 160, 1), (200, 1, 160, 4), (120, 3, 77, 3),
+                                             (16, 2, 9, 1)])
+def test_sym_eig_range_vs_lapack(dev, m, lo, hi, workers):
+    """sym_eig_range (dense.py:93-117): syevdx index ranges, optionally sliced."""
+    from paper_2111_06552_b200.dense import split_ranges, sym_eig_range
+
+    rng = np.random.default_rng(m + lo)
+    a = rng.standard_normal((m, m))
+    a = (a + a.T) / 2
+    dec = sym_eig_range(dev, rm(dev, a), lo, hi, workers=workers)
+    ww, vv = O.eig_range(a, lo, hi)
+    scale = max(1.0, np.abs(ww).max())
+    assert np.abs(host(dec.values) - ww).max() <= 1e-12 * scale
+    V = host(dec.vectors)
+    assert V.shape == (m, hi - lo + 1)
+    assert np.abs(a @ V - V * host(dec.values)).max() <= 1e-11 * scale
+    assert np.abs(V - vv).max() <= 1e-9  # sign rule, non-degenerate random spectrum
+    if workers > 1:
+        assert len(split_ranges(lo, hi, workers)) > 1
+
+
 def test_syev_golden_m8(dev, golden):
     w = dev.empty(8)
     v = dev.empty(8, 8)
