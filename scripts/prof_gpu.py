@@ -53,3 +53,20 @@ print(f"iters {rep.iterations}  wall {wall*1e3:.1f} ms  gpu span {span/1e3:.1f} 
       f"launches {len(ev)}")
 for n, v in agg.most_common(30):
     print(f"{v/1e3:9.2f} ms {cnt[n]:6d}  {v/cnt[n]:8.1f} us  {n}")
+
+# GPU idle gaps: which kernel precedes / follows each gap (host-bound stretches)
+evs = sorted(((e.time_range.start, e.time_range.end, e.name.split("(")[0].split("<")[0][-40:])
+              for e in ev), key=lambda t: t[0])
+gaps = collections.Counter()
+gap_n = collections.Counter()
+last_end, last_name = None, None
+for s, e_, nm in evs:
+    if last_end is not None and s - last_end > 5.0:
+        key = f"{last_name} -> {nm}"
+        gaps[key] += s - last_end
+        gap_n[key] += 1
+    if last_end is None or e_ > last_end:
+        last_end, last_name = e_, nm
+print("---- idle gaps > 5 us (total ms, count): preceding -> following kernel")
+for k, v in gaps.most_common(25):
+    print(f"{v/1e3:8.2f} ms {gap_n[k]:5d}  {k}")
