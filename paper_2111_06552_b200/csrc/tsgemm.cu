@@ -21,6 +21,9 @@
 // and the slab partials by a second kernel with one warp per output, always
 // in a fixed order — bit-identical run to run (test_kernels.py:74-85).
 
+#include <stdint.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace gcg {
@@ -397,6 +400,173 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tall-skinny LinComb, d <= 64 (W -= [X P] R in the deflation, the Ritz-vector
+// chunks of the convergence test, momentum): Y = alpha X C + beta Y.
+//
+// The m x d coefficient block stays resident in shared memory as DMMA B
+// fragments; each warp streams 8*FM rows of X from HBM straight into DMMA A
+// fragments — one VEC-wide load per lane feeds VEC k-substeps, because the k
+// index inside every 4*VEC chunk is permuted (lane c of a fragment takes
+// k = 4*VEC*chunk + c*VEC + s at substep s), identically for the B fragments —
+// and keeps the next chunk's loads in flight while multiplying the current one.
+// No X staging through shared memory, no block barrier in the main loop: warps
+// are independent, so the X stream is limited only by loads in flight, and a
+// warp writes only rows it alone has read (in-place use is safe for any d).
+__host__ __device__ constexpr int ts_cstride(int fn, int vec) {
+  // >= 8*fn, and vec*stride == 8 (mod 16) so the two k-rows a fragment load pairs
+  // up fall in opposite bank halves
+  int s = 8 * fn;
+  while ((vec * s) % 16 != 8) ++s;
+  return s;
+}
+
+template <int VEC>
+__device__ __forceinline__ void ts_load(double* v, const double* p, int valid) {
+  if (valid >= VEC) {
+    if constexpr (VEC == 4) {
+      const double4 t = *reinterpret_cast<const double4*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+      v[2] = t.z;
+      v[3] = t.w;
+    } else if constexpr (VEC == 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+    } else {
+      v[0] = *p;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < VEC; ++s) v[s] = s < valid ? p[s] : 0.0;
+  }
+}
+
+template <int FM, int FN, int VEC>
+__global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int d, double alpha,
+                                                         const double* X, long long ldx,
+                                                         const double* __restrict__ C,
+                                                         long long ldc, double beta, double* Y,
+                                                         long long ldy) {
+  constexpr int KC = 4 * VEC;
+  constexpr int CW = ts_cstride(FN, VEC);
+  extern __shared__ __align__(16) double cs[];
+  const int mp = (m + KC - 1) / KC * KC;
+  for (int e = threadIdx.x; e < mp * 8 * FN; e += blockDim.x) {
+    const int k = e / (8 * FN), j = e % (8 * FN);
+    cs[k * CW + j] = (k < m && j < d) ? C[(long long)k * ldc + j] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fa = lane >> 2, fc = lane & 3;
+  const long long ntiles = (n + 8 * FM - 1) / (8 * FM);
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+
+  for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += wstride) {
+    const long long r0 = t * 8 * FM;
+    const double* xr[FM];
+    bool rok[FM];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const long long row = r0 + i * 8 + fa;
+      rok[i] = row < n;
+      xr[i] = X + (rok[i] ? row : 0) * ldx;
+    }
+    auto load = [&](double (*v)[VEC], int kc) {
+      const int k = kc + fc * VEC;
+      const int valid = min(VEC, m - k);
+#pragma unroll
+      for (int i = 0; i < FM; ++i) ts_load<VEC>(v[i], xr[i] + k, rok[i] ? valid : 0);
+    };
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto compute = [&](double (*v)[VEC], int kc) {
+#pragma unroll
+      for (int s = 0; s < VEC; ++s) {
+        double b[FN];
+        const double* crow = cs + (kc + fc * VEC + s) * CW + fa;
+#pragma unroll
+        for (int j = 0; j < FN; ++j) b[j] = crow[j * 8];
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], v[i][s], b[j]);
+      }
+    };
+    double va[FM][VEC], vb[FM][VEC];
+    load(va, 0);
+    for (int kc = 0; kc < mp; kc += 2 * KC) {
+      const bool more = kc + KC < mp;
+      if (more) load(vb, kc + KC);
+      compute(va, kc);
+      if (more) {
+        if (kc + 2 * KC < mp) load(va, kc + 2 * KC);
+        compute(vb, kc + KC);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const long long row = r0 + i * 8 + fa;
+      if (row >= n) continue;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = j * 8 + fc * 2 + h;
+          if (col >= d) continue;
+          double* y = Y + row * ldy + col;
+          *y = (beta == 0.0) ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *y);
+        }
+      }
+    }
+  }
+}
+
+template <int FM, int FN, int VEC>
+static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const double* X,
+                          long long ldx, const double* C, long long ldc, double beta, double* Y,
+                          long long ldy) {
+  auto kern = lincomb_ts_kernel<FM, FN, VEC>;
+  const int mp = (m + 4 * VEC - 1) / (4 * VEC) * (4 * VEC);
+  const size_t sm = sizeof(double) * (size_t)mp * ts_cstride(FN, VEC);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, sm);
+  if (occ < 1) occ = 1;
+  const long long ntiles = (n + 8 * FM - 1) / (8 * FM);
+  long long grid = (ntiles + 3) / 4;
+  const long long cap = (long long)occ * c->num_sms;
+  if (grid > cap) grid = cap;
+  kern<<<(unsigned)grid, 128, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+}
+
+template <int VEC>
+static bool lincomb_ts_dispatch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
+                                long long ldx, const double* C, long long ldc, double beta,
+                                double* Y, long long ldy) {
+  const int fn = (d + 7) / 8;
+  const size_t sm = sizeof(double) * (size_t)((m + 4 * VEC - 1) / (4 * VEC) * (4 * VEC)) *
+                    ts_cstride(fn, VEC);
+  if (fn > 8 || sm > 96 * 1024) return false;
+#define TS(fm, fnn) lincomb_ts_go<fm, fnn, VEC>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy)
+  switch (fn) {
+    case 1: TS(4, 1); break;
+    case 2: TS(4, 2); break;
+    case 3: TS(2, 3); break;
+    case 4: TS(2, 4); break;
+    case 5: TS(1, 5); break;
+    case 6: TS(1, 6); break;
+    case 7: TS(1, 7); break;
+    default: TS(1, 8); break;
+  }
+#undef TS
+  return true;
+}
+
 int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
                    long long ldx, const double* C, long long ldc, double beta, double* Y,
                    long long ldy) {
@@ -419,6 +589,22 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   }
   const int ps =
       prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
+  static const bool ts_on = !(getenv("GCG_LINCOMB_TS") && getenv("GCG_LINCOMB_TS")[0] == '0');
+  if (ts_on && d <= 64) {
+    bool done;
+    if (ldx % 4 == 0 && ((uintptr_t)X & 31) == 0)
+      done = lincomb_ts_dispatch<4>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    else if (ldx % 2 == 0 && al16(X))
+      done = lincomb_ts_dispatch<2>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    else
+      done = lincomb_ts_dispatch<1>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    if (done) {
+      prof_stop(c, ps);
+      ++g_launches;
+      GCG_CHECK_LAUNCH();
+      return GCG_OK;
+    }
+  }
   const bool vec = (ldx % 2 == 0) && al16(X);
   // One column tile covers all d <= 256 columns, so X is streamed exactly once:
   // d <= 64: 8 warps stacked along rows (BM = 256, warp tile 32 x BN);
