@@ -9,7 +9,9 @@
 // per-column flags live on the device: the SpMM is done on the full row-major
 // block (an active subset costs the same HBM sectors as the whole row run),
 // the p'q and ||r||^2 reductions are fused into the SpMM / update epilogues,
-// and the scalar recurrences run in 1-CTA "finish" kernels.  No host sync
+// and the scalar recurrences (alpha, beta, stop/freeze flags) are folded into
+// the prologues of the two vector-update kernels — two launches after the SpMM
+// per sweep, no separate finish kernels.  No host sync
 // happens inside the solve: once every column has stopped, a device flag turns
 // the remaining launches into no-ops and the sweep count is read back lazily
 // by the caller.  Per sweep HBM traffic ~ SpMM + 24nk (r -= alpha q) + 40nk
@@ -33,7 +35,7 @@ int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, doub
                 long long ldy);
 
 struct CgState {
-  double* rz;
+  double* rz;  // [2][k]: r'r of the current sweep at parity (sweep & 1), next at the other
   double* rn;
   double* rn0;
   double* target;
@@ -109,72 +111,85 @@ __global__ void cg_init_fin(int k, const double* part, int nparts, double rel_to
   publish_active(s, k, !cv, true);
 }
 
-// den = p'q per active column; freeze on den <= 0, else alpha = rz / den.
-__global__ void cg_fin1(int k, const double* part, int nparts, CgState s) {
-  // `live` tells cg_pupdate_kernel whether this sweep ran (its deferred x update
-  // must still happen in the sweep that raises `skip`)
-  if (*s.skip) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *s.live = 0;
-    return;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *s.live = 1;
-  __shared__ double sm[128];
-  const int c = blockIdx.x;
-  const double den = block_sum_parts(part, nparts, k, c, sm);
-  if (threadIdx.x == 0) {
-    if (c == 0) *s.sweeps += 1;
-    int u = 0;
-    if (!s.conv[c] && !s.frozen[c]) {
-      if (den <= 0.0) {
-        s.frozen[c] = 1;
-      } else {
-        s.alpha[c] = s.rz[c] / den;
-        u = 1;
-      }
+// Fixed-order column sums of an nparts x k block of per-CTA partials, computed
+// redundantly by every CTA of the consumer kernel (256 threads, k <= 256): thread t
+// sums column t % k over parts t / k, t / k + L, ... (L = 256 / k), then the L
+// partials of each column are added in lane order — the same bits in every CTA
+// and run to run.  Replaces a separate 1-CTA "finish" launch per reduction.
+__device__ void cta_column_sums(const double* part, int nparts, int k, double* sm, double* out) {
+  const int L = blockDim.x / k;
+  const int c = threadIdx.x % k, l = threadIdx.x / k;
+  double v = 0.0;
+  if (l < L) {
+    // 8 independent loads in flight per round, added in index order
+    constexpr int U = 8;
+    int b = l;
+    for (; b + (U - 1) * L < nparts; b += U * L) {
+      double t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u] = part[(long long)(b + u * L) * k + c];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v += t[u];
     }
-    s.upd[c] = u;
+    for (; b < nparts; b += L) v += part[(long long)b * k + c];
   }
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double t = 0.0;
+    for (int j = 0; j < L; ++j) t += sm[j * k + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
 }
 
-// rn = ||r||; converge, else beta = rz_new / rz.  Raises the skip flag when no
-// column remains active (the reference's loop exit, cg.py:67-69).
-__global__ void cg_fin2(int k, const double* part, int nparts, CgState s) {
-  if (*s.skip) return;
-  __shared__ double sm[128];
-  const int c = blockIdx.x;
-  const double rr = block_sum_parts(part, nparts, k, c, sm);
-  int active = 0;
-  if (threadIdx.x == 0) {
-    int p = 0;
-    if (s.upd[c]) {
-      const double rn = sqrt(rr);
-      s.rn[c] = rn;
-      if (rn <= s.target[c]) {
-        s.conv[c] = 1;
-      } else {
-        s.beta[c] = rr / s.rz[c];
-        s.rz[c] = rr;
-        p = 1;
-      }
-    }
-    s.pup[c] = p;
-    active = !s.conv[c] && !s.frozen[c];
-  }
-  publish_active(s, k, active, false);
-}
-
-// r -= alpha q ; partial ||r||^2 (updated columns only).  The matching
-// x += alpha p is deferred to cg_pupdate_kernel, which reads the old p anyway:
-// per sweep 24nk + 40nk bytes instead of 48nk + 24nk.
+// r -= alpha q and the ||r||^2 partials, with the alpha step of the recurrence
+// (cg.py:73-84) folded in: every CTA reduces the SpMM's p'q partials itself and
+// takes the per-column decisions (freeze when p'q <= 0, else alpha = r'r / p'q);
+// CTA 0 publishes them (the only state written here; 'frozen' only ever goes
+// 0 -> 1, so a CTA reading it before or after that store decides the same).
 __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, double* r,
                                                         const double* __restrict__ q,
-                                                        long long rows_per_cta, double* part,
-                                                        CgState s, int* prof_skipped) {
+                                                        long long rows_per_cta,
+                                                        const double* spart, int nsp,
+                                                        double* part, CgState s, int par,
+                                                        int* prof_skipped) {
   if (*s.skip) {
-    if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *s.live = 0;
+      if (prof_skipped) *prof_skipped = 1;
+    }
     return;
   }
   __shared__ double sm[256];
+  __shared__ double s_al[256];
+  __shared__ int s_up[256];
+  cta_column_sums(spart, nsp, k, sm, s_al);
+  if (threadIdx.x < k) {
+    const int cc = threadIdx.x;
+    const double den = s_al[cc];
+    int u = 0;
+    double al = 0.0;
+    if (!s.conv[cc] && !s.frozen[cc]) {
+      if (den <= 0.0) {
+        if (blockIdx.x == 0) s.frozen[cc] = 1;
+      } else {
+        al = s.rz[par * k + cc] / den;
+        u = 1;
+      }
+    }
+    s_al[cc] = al;
+    s_up[cc] = u;
+    if (blockIdx.x == 0) {
+      s.alpha[cc] = al;
+      s.upd[cc] = u;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *s.sweeps += 1;
+    *s.live = 1;
+  }
+  __syncthreads();
   const int kc = k;  // k <= 256 (checked by the launcher)
   const int lanes = 256 / kc;
   const int c = threadIdx.x % kc;
@@ -183,8 +198,8 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
   double acc = 0.0;
-  if (rl < lanes && s.upd[c]) {
-    const double al = s.alpha[c];
+  if (rl < lanes && s_up[c]) {
+    const double al = s_al[c];
     constexpr int U = 8;  // rows in flight per thread
     long long i = r0 + rl;
     for (; i + (U - 1) * lanes < r1; i += U * lanes) {
@@ -216,18 +231,60 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   }
 }
 
-// x += alpha p (columns updated this sweep) then p = r + beta p (columns still iterating)
+// x += alpha p (deferred from the r-update) and p = r + beta p, with the beta step
+// (cg.py:86-96) folded in: every CTA reduces the ||r||^2 partials, tests the stop
+// criterion and forms beta; CTA 0 publishes rn, conv, beta, r'r (into the other
+// parity slot, so no CTA can read a value of this sweep's update) and raises the
+// skip flag for the following sweeps once no column is active.
 __global__ void __launch_bounds__(256) cg_pupdate_kernel(long long n, int k, double* x,
                                                          long long ldx,
                                                          const double* __restrict__ r, double* p,
-                                                         long long rows_per_cta, CgState s,
-                                                         int* prof_skipped) {
+                                                         long long rows_per_cta,
+                                                         const double* upart, int nup, CgState s,
+                                                         int par, int* prof_skipped) {
   if (!*s.live) {
     if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
     return;
   }
-  // same (row lane, column) mapping as cg_update_kernel: flags and scalars are
-  // per-thread constants, U rows in flight per thread
+  __shared__ double sm[256];
+  __shared__ double s_be[256], s_al[256];
+  __shared__ int s_ux[256], s_pp[256];
+  __shared__ int nact;
+  if (threadIdx.x == 0) nact = 0;
+  cta_column_sums(upart, nup, k, sm, s_be);
+  if (threadIdx.x < k) {
+    const int cc = threadIdx.x;
+    const double rr = s_be[cc];
+    const int ux = s.upd[cc];
+    int cv = s.conv[cc], pp = 0;
+    double be = 0.0;
+    const double rzo = s.rz[par * k + cc];
+    double rzn = rzo;
+    if (ux) {
+      const double rn = sqrt(rr);
+      if (blockIdx.x == 0) s.rn[cc] = rn;
+      if (rn <= s.target[cc]) {
+        cv = 1;
+      } else {
+        be = rr / rzo;
+        rzn = rr;
+        pp = 1;
+      }
+    }
+    s_be[cc] = be;
+    s_al[cc] = s.alpha[cc];
+    s_ux[cc] = ux;
+    s_pp[cc] = pp;
+    if (blockIdx.x == 0) {
+      s.conv[cc] = cv;
+      s.beta[cc] = be;
+      s.pup[cc] = pp;
+      s.rz[(par ^ 1) * k + cc] = rzn;
+    }
+    if (!cv && !s.frozen[cc]) atomicAdd(&nact, 1);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nact == 0) *s.skip = 1;
   const int lanes = 256 / k;
   const int c = threadIdx.x % k;
   const int rl = threadIdx.x / k;
@@ -235,9 +292,9 @@ __global__ void __launch_bounds__(256) cg_pupdate_kernel(long long n, int k, dou
   const long long r0 = (long long)blockIdx.x * rows_per_cta;
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
-  const bool ux = s.upd[c], up = s.pup[c];
+  const bool ux = s_ux[c], up = s_pp[c];
   if (!ux && !up) return;
-  const double al = s.alpha[c], be = s.beta[c];
+  const double al = s_al[c], be = s_be[c];
   constexpr int U = 8;
   long long i = r0 + rl;
   for (; i + (U - 1) * lanes < r1; i += U * lanes) {
@@ -342,7 +399,7 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   const size_t vec = ((size_t)n * k + 3) & ~(size_t)3;
   const size_t pvec = ((size_t)(n + nghost) * k + 3) & ~(size_t)3;
   const size_t bytes =
-      sizeof(double) * (2 * vec + 2 * pvec + (size_t)nparts_max * k + 6 * (size_t)k) +
+      sizeof(double) * (2 * vec + 2 * pvec + 2 * (size_t)nparts_max * k + 7 * (size_t)k) +
       sizeof(int) * (4 * (size_t)k + 5) + 256;
   GCG_TRY(ensure(c->cg, bytes));
   double* R = (double*)c->cg.ptr;
@@ -355,15 +412,16 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   GCG_TRY(copy_launch(c, n, k, x_user, ldx_user, Xc, k));
   x = Xc;
   ldx = k;
-  double* sd = part + (size_t)nparts_max * k;
+  double* upart = part + (size_t)nparts_max * k;  // r-update partials (SpMM's stay readable)
+  double* sd = upart + (size_t)nparts_max * k;
   CgState s;
-  s.rz = sd;
-  s.rn = sd + k;
-  s.rn0 = sd + 2 * k;
-  s.target = sd + 3 * k;
-  s.alpha = sd + 4 * k;
-  s.beta = sd + 5 * k;
-  int* si = (int*)(sd + 6 * k);
+  s.rz = sd;  // 2k
+  s.rn = sd + 2 * k;
+  s.rn0 = sd + 3 * k;
+  s.target = sd + 4 * k;
+  s.alpha = sd + 5 * k;
+  s.beta = sd + 6 * k;
+  int* si = (int*)(sd + 7 * k);
   s.conv = si;
   s.frozen = si + k;
   s.upd = si + 2 * k;
@@ -403,23 +461,22 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       red = dist->red_buf;
       nred = 1;
     }
-    cg_fin1<<<k, 128, 0, c->stream>>>(k, red, nred, s);
     int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
-    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, R, Q, rpc, part, s, prof_skip_slot(c, ps));
+    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, R, Q, rpc, red, nred, upart, s, it & 1,
+                                                   prof_skip_slot(c, ps));
     prof_stop(c, ps);
-    red = part;
+    red = upart;
     nred = ugrid;
     if (dist) {
-      GCG_TRY(dist_reduce(c, dist, part, ugrid, k));
+      GCG_TRY(dist_reduce(c, dist, upart, ugrid, k));
       red = dist->red_buf;
       nred = 1;
     }
-    cg_fin2<<<k, 128, 0, c->stream>>>(k, red, nred, s);
     ps = prof_start(c, PROF_CG_PUPDATE, 40.0 * n * k);
-    cg_pupdate_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, rpc, s,
-                                                    prof_skip_slot(c, ps));
+    cg_pupdate_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, rpc, red, nred, s,
+                                                    it & 1, prof_skip_slot(c, ps));
     prof_stop(c, ps);
-    g_launches += 4;
+    g_launches += 2;
     GCG_CHECK_LAUNCH();
   }
   GCG_TRY(copy_launch(c, n, k, Xc, k, x_user, ldx_user));

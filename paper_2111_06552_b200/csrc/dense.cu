@@ -421,11 +421,29 @@ int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int s
                                                                         nullptr);
   ++g_launches;
   GCG_CHECK_LAUNCH();
-  const cusolverStatus_t st =
-      jac ? cusolverDnDsyevj(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m,
-                             w, work, lwork, info, jparams)
-          : cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B, m,
-                             w, work, lwork, info);
+  const bool x64 = impl && impl[0] == 'x';  // A/B: the 64-bit generic API (host workspace)
+  cusolverStatus_t st;
+  if (x64) {
+    static cusolverDnParams_t prm = nullptr;
+    if (!prm) cusolverDnCreateParams(&prm);
+    size_t dws = 0, hws = 0;
+    if (cusolverDnXsyevd_bufferSize(c->solver, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    m, CUDA_R_64F, B, m, CUDA_R_64F, w, CUDA_R_64F, &dws,
+                                    &hws) != CUSOLVER_STATUS_SUCCESS)
+      return GCG_ERR_SOLVER;
+    GCG_TRY(ensure(c->eigwork, dws + 64));
+    static std::vector<char> hbuf;
+    if (hbuf.size() < hws + 1) hbuf.resize(hws + 1);
+    int* xinfo = (int*)((char*)c->eigwork.ptr + dws);
+    st = cusolverDnXsyevd(c->solver, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                          CUDA_R_64F, B, m, CUDA_R_64F, w, CUDA_R_64F, c->eigwork.ptr, dws,
+                          hbuf.data(), hws, xinfo);
+  } else {
+    st = jac ? cusolverDnDsyevj(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B,
+                                m, w, work, lwork, info, jparams)
+             : cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, B,
+                                m, w, work, lwork, info);
+  }
   if (st != CUSOLVER_STATUS_SUCCESS) return GCG_ERR_SOLVER;
   // row-major symmetric input == its column-major transpose, so B now holds
   // eigenvector j in column-major column j
