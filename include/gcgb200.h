@@ -228,6 +228,32 @@ int gcg_ritz_residuals(void* ctx, int64_t n, int64_t k, const double* AX, int64_
                        const double* X, int64_t ldx, const double* BX, int64_t ldbx,
                        const double* lam, int mode, double* out);
 
+/* ---- B-orthogonalisation, natively driven (one GPU) ------------------------
+ * The reference's Alg. 3 control flow (orth.py:124-226, 339-372) run by the
+ * library: every repeat / dependence decision is a pinned read of the fused
+ * status record, every long-vector step a library kernel.  B = CSR (n x n,
+ * rowptr/colidx int32 on device) or b_rowptr == NULL for B = I.  Outputs: the
+ * kept column count (0 = all dependent), the reduction count, and the slots
+ * refilled from the rear (first `cap` written, total in *nrep). */
+typedef struct gcg_orth_opts {
+  int64_t svd_leaf;        /* <= 0: min(width, 16) */
+  double reorth_tol;       /* orth.py:59 */
+  double dependence_tol;   /* orth.py:60 */
+  int32_t max_passes;      /* orth.py:61 */
+  int32_t pad_;
+} gcg_orth_opts;
+/* recursive_orth_svd on columns [lo, hi) of X (orth.py:207-226) */
+int gcg_orth_recursive(void* ctx, int64_t n, double* X, int64_t ldx, int64_t lo, int64_t hi,
+                       int64_t b_nnz, const int* b_rowptr, const int* b_colidx,
+                       const double* b_val, const gcg_orth_opts* opts, int64_t* kept,
+                       int64_t* reductions, int64_t* replaced, int64_t cap, int64_t* nrep);
+/* orth_against: X[:, 0:w] against the B-orthonormal basis (n x K, ldb) (orth.py:339-372) */
+int gcg_orth_against(void* ctx, int64_t n, double* X, int64_t ldx, int64_t w,
+                     const double* basis, int64_t ldb, int64_t K, int64_t b_nnz,
+                     const int* b_rowptr, const int* b_colidx, const double* b_val,
+                     const gcg_orth_opts* opts, int64_t* kept, int64_t* reductions,
+                     int64_t* replaced, int64_t cap, int64_t* nrep);
+
 /* ---- MatrixMarket ingestion (host; io.py:108-216 read_matrix_market) ------
  * gcg_mm_open parses the whole file (coordinate entries tokenised by
  * `nthreads` host threads, 0 = all cores) into a handle; on a malformed file it

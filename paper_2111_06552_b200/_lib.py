@@ -60,11 +60,27 @@ _SIGS = {
     "gcg_count_le": [_ptr, _i64, _ptr, _dbl, _ptr],
     "gcg_scale_rsqrt": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _ptr, _i64],
     "gcg_ritz_residuals": [_ptr, _i64, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _int, _ptr],
+    "gcg_orth_recursive": [_ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr,
+                           _ptr, _ptr, _ptr, _i64, _ptr],
+    "gcg_orth_against": [_ptr, _i64, _ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr,
+                         _ptr, _ptr, _ptr, _ptr, _i64, _ptr],
     "gcg_mm_open": [C.c_char_p, _int, C.POINTER(_ptr), _ptr],
     "gcg_mm_fetch": [_ptr, _ptr, _ptr, _ptr],
     "gcg_mm_close": [_ptr],
 }
 _RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64, "gcg_mm_close": None}
+
+
+class OrthOpts(C.Structure):
+    """gcg_orth_opts (include/gcgb200.h)."""
+
+    _fields_ = [
+        ("svd_leaf", C.c_int64),
+        ("reorth_tol", C.c_double),
+        ("dependence_tol", C.c_double),
+        ("max_passes", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
 
 
 class MMInfo(C.Structure):

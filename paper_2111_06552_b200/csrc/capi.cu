@@ -225,6 +225,8 @@ int gcg_ctx_destroy(void* p) {
   release(c->host_tmp3);
   release(c->host_tmp4);
   release(c->dense);
+  release(c->orth);
+  if (c->pinned) cudaFreeHost(c->pinned);
   if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
   return GCG_OK;

@@ -56,6 +56,8 @@ struct Ctx {
   Scratch host_tmp3;
   Scratch host_tmp4;
   Scratch dense;      // small dense temporaries (eigensolver staging)
+  Scratch orth;       // native orthogonalisation: status, Gram, SVQB coefficients, B*block
+  double* pinned = nullptr;  // pinned host slots for decision reads
   int* sync_flag = nullptr;
   cudaEvent_t ev = nullptr;
 };

@@ -31,9 +31,13 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import ctypes as C
+import os
+
 import numpy as np
 import torch
 
+from . import _lib
 from . import device as D
 from .errors import AllDependent, InvalidRange, InvalidShape
 from .mvops import LocalOps
@@ -41,6 +45,10 @@ from .mvops import LocalOps
 __all__ = ["OrthConfig", "OrthOutcome", "modified_block_orth", "recursive_orth_svd", "orth_against"]
 
 _DGKS_RATIO = 0.5  # orth.py:43
+# one GPU: the Alg. 3 decision loop runs natively (gcg_orth_recursive /
+# gcg_orth_against, csrc/orth.cu); the Python control flow below serves the
+# row-partitioned path (collectives per reduction) and Alg. 2.
+_NATIVE = os.environ.get("GCG_ORTH_NATIVE", "1") != "0"
 _REPAIR_RATIO = 1e-8  # orth.py:45
 
 
@@ -228,6 +236,25 @@ def _recurse_svd(st, lo, hi):
     _recurse_svd(st, mid, hi)
 
 
+def _native_ok(ops, b):
+    return _NATIVE and type(ops) is LocalOps and (b is None or hasattr(b, "rowptr"))
+
+
+def _native(name, ops, x, lead, b, cfg, width):
+    """Run gcg_orth_recursive / gcg_orth_against; returns OrthOutcome (kept may be 0)."""
+    o = _lib.OrthOpts(cfg.svd_leaf if cfg.svd_leaf is not None else 0, float(cfg.reorth_tol),
+                      float(cfg.dependence_tol), int(cfg.max_reorth_passes), 0)
+    kept, red, nrep = C.c_int64(), C.c_int64(), C.c_int64()
+    cap = 4 * width + 64
+    rep = (C.c_int64 * cap)()
+    bargs = (b.nnz, D._p(b.rowptr), D._p(b.colidx), D._p(b.val)) if b is not None else \
+        (0, None, None, None)
+    _lib.call(name, ops.dev.h, x.shape[0], D._p(x), D._ld(x), *lead, *bargs, C.byref(o),
+              C.byref(kept), C.byref(red), rep, cap, C.byref(nrep))
+    return OrthOutcome(int(kept.value), [int(v) for v in rep[:min(nrep.value, cap)]],
+                       int(red.value))
+
+
 def recursive_orth_svd(ops, x, s=None, e=None, b=None, cfg=None):
     """B-orthonormalise columns s..e (1-based, inclusive) of device block ``x`` in place."""
     ops = _as_ops(ops)
@@ -238,6 +265,13 @@ def recursive_orth_svd(ops, x, s=None, e=None, b=None, cfg=None):
     if not (1 <= s <= e <= ncols):
         raise InvalidRange(f"column range {s}..{e} invalid for width {ncols}")
     lo, hi = s - 1, e
+    if cfg.svd_leaf is not None and cfg.svd_leaf < 1:
+        raise InvalidShape(f"svd_leaf must be >= 1, got {cfg.svd_leaf}")
+    if _native_ok(ops, b) and x.shape[0] > 0:
+        out = _native("gcg_orth_recursive", ops, x, (lo, hi), b, cfg, hi - lo)
+        if out.num_kept <= 0:
+            raise AllDependent("every column in the block is linearly dependent")
+        return out
     st = _State(ops, x, b, cfg, lo, hi)
     st.leaf_width = cfg.svd_leaf if cfg.svd_leaf is not None else min(hi - lo, 16)
     if st.leaf_width < 1:
@@ -381,6 +415,15 @@ def orth_against(ops, x, basis, b=None, cfg=None):
     if have_basis:
         if basis.shape[0] != x.shape[0]:
             raise InvalidShape(f"basis dim {basis.shape[0]} != block dim {x.shape[0]}")
+    if _native_ok(ops, b) and x.shape[0] > 0:
+        K = basis.shape[1] if have_basis else 0
+        out = _native("gcg_orth_against", ops, x,
+                      (x.shape[1], D._p(basis) if K else None, D._ld(basis) if K else 0, K),
+                      b, cfg, x.shape[1])
+        if out.num_kept <= 0:
+            raise AllDependent("every column in the block is linearly dependent")
+        return out
+    if have_basis:
         _deflate_against(st, basis, 0, x.shape[1])
     inner = recursive_orth_svd(ops, x, 1, x.shape[1], b=b, cfg=cfg)
     kept = inner.num_kept
