@@ -71,6 +71,40 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
                           const double* X, long long ldx, const double* BX, long long ldbx,
                           const double* lam, int mode, double* out);
 
+void kernel_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done) {
+    if (e.first != kern) continue;
+    if (e.second >= bytes) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    e.second = bytes;
+    return;
+  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.emplace_back(kern, bytes);
+}
+
+int kernel_occupancy(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  struct Key {
+    const void* k;
+    int t;
+    size_t s;
+    int occ;
+  };
+  static std::vector<Key> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& e : cache)
+    if (e.k == kern && e.t == threads && e.s == smem) return e.occ;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  if (occ < 1) occ = 1;
+  cache.push_back({kern, threads, smem, occ});
+  return occ;
+}
+
 int ensure(Scratch& s, size_t bytes) {
   if (bytes <= s.bytes) return GCG_OK;
   // the scratch may still be in use by queued work on any stream of this ctx

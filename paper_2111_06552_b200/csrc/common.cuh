@@ -64,6 +64,11 @@ struct Ctx {
 
 int ensure(Scratch& s, size_t bytes);
 
+// cudaFuncSetAttribute / the occupancy query are host API calls of several
+// microseconds; the launchers call these cached forms instead (keyed by kernel).
+void kernel_smem(const void* kern, size_t bytes);
+int kernel_occupancy(const void* kern, int threads, size_t smem);
+
 inline int cuda_status(cudaError_t e) {
   return e == cudaSuccess ? GCG_OK : GCG_ERR_CUDA;
 }

@@ -200,11 +200,11 @@ static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long l
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, nslab);
   if (vec) {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
   } else {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
   }
 }
@@ -391,11 +391,11 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
   dim3 grid((unsigned)((n + BM - 1) / BM), (d + BN - 1) / BN);
   if (vec) {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
   } else {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
   }
 }
@@ -533,10 +533,8 @@ static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const
   auto kern = lincomb_ts_kernel<FM, FN, VEC>;
   const int mp = (m + 4 * VEC - 1) / (4 * VEC) * (4 * VEC);
   const size_t sm = sizeof(double) * (size_t)mp * ts_cstride(FN, VEC);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, sm);
-  if (occ < 1) occ = 1;
+  kernel_smem((const void*)kern, sm);
+  const int occ = kernel_occupancy((const void*)kern, 128, sm);
   const long long ntiles = (n + 8 * FM - 1) / (8 * FM);
   long long grid = (ntiles + 3) / 4;
   const long long cap = (long long)occ * c->num_sms;
