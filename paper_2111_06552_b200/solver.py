@@ -232,21 +232,38 @@ class _Solve:
 
         The Ritz vectors are formed chunk by chunk (basis @ coeffs[:, chunk]) only
         as far as the prefix test reads them; the full X update happens in place
-        afterwards (:meth:`update_in_place`)."""
+        afterwards (:meth:`update_in_place`).
+        The host copy of the Ritz values rides along with the first chunk's
+        residuals (one device->host read instead of two); returns
+        (count, first unconverged residual, Ritz values on the host)."""
         count = 0
         xc = None
+        lam_host = None
         for start in range(0, limit, chunk):
             stop = min(start + chunk, limit)
             if xc is None or xc.shape[1] != stop - start:
                 xc = self.ops.vec(stop - start)
             D.lincomb(self.dev, basis, coeffs[:, start:stop], xc)
-            rel = self.residuals(xc, lam_new_dev[start:stop])
+            if lam_host is None and stop - start <= 256:
+                r = self.residuals_dev(xc, lam_new_dev[start:stop])
+                both = torch.cat([lam_new_dev, r]).cpu().numpy()
+                lam_host, rel = both[:lam_new_dev.shape[0]], both[lam_new_dev.shape[0]:]
+            else:
+                rel = self.residuals(xc, lam_new_dev[start:stop])
             for j in range(stop - start):
                 if rel[j] < tol:
                     count += 1
                 else:
-                    return count, float(rel[j])
-        return count, 0.0
+                    return count, float(rel[j]), lam_host
+        return count, 0.0, lam_host
+
+    def residuals_dev(self, x, lam_dev):
+        """Relative residuals of up to 256 Ritz pairs as a replicated device vector."""
+        ax = self.apply_a(x)
+        bx = self.apply_b(x)
+        r = self.dev.empty(x.shape[1])
+        self.ops.residuals(ax, x, bx, lam_dev, self.res_mode, r)
+        return self.ops.broadcast(r)
 
     def build_p(self, coeffs, num_x_rows, group_start, group_width, dep_tol):
         """solver._build_p (solver.py:167-199) on device; returns phat (m x np) or None."""
@@ -429,12 +446,14 @@ def gcg_solve_ops(ops, cfg, x0=None):
             ops.broadcast(full.vectors)
             lam_new_dev = full.values[:d]
             coeffs = full.vectors[:, :d]
-        lam_new = lam_new_dev.cpu().numpy()
         timer.lap("t_step3")
 
         stored = sum(len(vv) for vv in store_vals)
         limit = max(0, min(sx - locked, ne - stored - locked))
-        newly, first_res = S.count_converged(basis, coeffs, lam_new_dev, limit, bs, cfg.tol)
+        newly, first_res, lam_new = S.count_converged(basis, coeffs, lam_new_dev, limit, bs,
+                                                      cfg.tol)
+        if lam_new is None:
+            lam_new = lam_new_dev.cpu().numpy()
         c = locked + newly
         total_locked = stored + c
         timer.lap("t_step4")
