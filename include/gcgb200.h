@@ -254,6 +254,23 @@ int gcg_orth_against(void* ctx, int64_t n, double* X, int64_t ldx, int64_t w,
                      const gcg_orth_opts* opts, int64_t* kept, int64_t* reductions,
                      int64_t* replaced, int64_t cap, int64_t* nrep);
 
+/* ---- BASELINE operators assembled on the device (problems.py generators) ----
+ * Structured grid n0 x n1 x n2 (n2 fastest; n0 = 1 for 2-D), noff <= 27 offsets
+ * (host int32 triples d0,d1,d2), Dirichlet truncation, rows in lexicographic
+ * order, columns sorted.  Weights: w[t] constant per offset (host), or wrow[t]
+ * a device array of n per-row values (host array of device pointers).  rowptr
+ * (n + 1), colidx and val (nnz, from gcg_stencil_nnz) are caller-owned device
+ * buffers.  Bit-identical to problems.stencil_csr. */
+int gcg_stencil_nnz(int64_t n0, int64_t n1, int64_t n2, int32_t noff, const int32_t* offs,
+                    int64_t* nnz);
+int gcg_stencil_csr(void* ctx, int64_t n0, int64_t n1, int64_t n2, int32_t noff,
+                    const int32_t* offs, const double* w, const double* const* wrow,
+                    int32_t* rowptr, int32_t* colidx, double* val);
+/* per-row weights of the var-coef 7-pt operator (problems.py varcoef_diffusion_3d)
+ * from the N^3 cell field kc (device): out = [diag | -face(ax, s) for (ax, s) in
+ * (0,-1),(0,+1),(1,-1),(1,+1),(2,-1),(2,+1)], 7 arrays of N^3. */
+int gcg_varcoef7_weights(void* ctx, int64_t N, const double* kc, double* out);
+
 /* ---- MatrixMarket ingestion (host; io.py:108-216 read_matrix_market) ------
  * gcg_mm_open parses the whole file (coordinate entries tokenised by
  * `nthreads` host threads, 0 = all cores) into a handle; on a malformed file it

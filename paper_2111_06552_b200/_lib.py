@@ -64,6 +64,9 @@ _SIGS = {
                            _ptr, _ptr, _ptr, _i64, _ptr],
     "gcg_orth_against": [_ptr, _i64, _ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr,
                          _ptr, _ptr, _ptr, _ptr, _i64, _ptr],
+    "gcg_stencil_nnz": [_i64, _i64, _i64, _i32, _ptr, _ptr],
+    "gcg_stencil_csr": [_ptr, _i64, _i64, _i64, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+    "gcg_varcoef7_weights": [_ptr, _i64, _ptr, _ptr],
     "gcg_mm_open": [C.c_char_p, _int, C.POINTER(_ptr), _ptr],
     "gcg_mm_fetch": [_ptr, _ptr, _ptr, _ptr],
     "gcg_mm_close": [_ptr],

@@ -87,6 +87,18 @@ class DeviceProblem:
         self._shift_vals = None
         self._shift_theta = None
 
+    @classmethod
+    def from_device(cls, ctx, A, B=None):
+        """Wrap operators already in HBM (e.g. assembled by devgen); B must share A's pattern."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.A = A
+        self.B = B
+        self.n = A.n
+        self._shift_vals = None
+        self._shift_theta = None
+        return self
+
     def shifted(self, theta):
         """(values, diag_shift) such that op = CSR(values) + diag_shift*I equals A - theta*B."""
         if theta == 0.0:

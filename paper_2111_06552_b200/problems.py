@@ -224,27 +224,39 @@ _BASELINE = {
 }
 
 
-def baseline_problem(cfg, scale=None):
+def baseline_problem(cfg, scale=None, build=True):
     """Build BASELINE.json config ``cfg`` (1-based).  ``scale`` overrides the
-    grid size (for small parity runs of the same operator family)."""
+    grid size (for small parity runs of the same operator family).  With
+    ``build=False`` only the metadata is returned (``a`` is None) — for the
+    device generators (devgen.py)."""
     spec = _BASELINE[cfg]
     b = None
+    a = None
     if cfg == 1:
         N = scale or 100
-        a, grid, desc = laplacian_2d(N), (N, N), f"2-D 5-pt Laplacian {N}^2"
+        grid, desc = (N, N), f"2-D 5-pt Laplacian {N}^2"
+        if build:
+            a = laplacian_2d(N)
     elif cfg == 2:
         N = scale or 64
-        a, grid, desc = laplacian_3d(N), (N, N, N), f"3-D 7-pt Laplacian {N}^3"
+        grid, desc = (N, N, N), f"3-D 7-pt Laplacian {N}^3"
+        if build:
+            a = laplacian_3d(N)
     elif cfg == 3:
         C = scale or 80
-        a, b = fem_p1_cube(C)
         grid, desc = (C - 1,) * 3, f"P1 FEM Kuhn cube {C}^3 cells"
+        if build:
+            a, b = fem_p1_cube(C)
     elif cfg == 4:
         N = scale or 128
-        a, grid, desc = varcoef_diffusion_3d(N, seed=0), (N, N, N), f"var-coef 7-pt {N}^3"
+        grid, desc = (N, N, N), f"var-coef 7-pt {N}^3"
+        if build:
+            a = varcoef_diffusion_3d(N, seed=0)
     elif cfg == 5:
         N = scale or 256
-        a, grid, desc = stencil27(N), (N, N, N), f"27-pt stencil {N}^3"
+        grid, desc = (N, N, N), f"27-pt stencil {N}^3"
+        if build:
+            a = stencil27(N)
     else:
         raise KeyError(cfg)
     return Problem(spec["name"] if scale is None else f"{spec['name']}@{scale}", a, b,
