@@ -17,9 +17,9 @@
 //
 // At the BASELINE shapes the kernel is latency-bound (a row is a 3-deep chain:
 // row pointer -> index/value -> X gathers), so it is software-pipelined: while
-// a warp gathers X for its current rows it already holds the row pointers and
-// the index/value chunk of its NEXT rows in registers, leaving only the X
-// gathers on the critical path.
+// a warp gathers X for its current rows, the index/value chunk of its next rows
+// and the row pointers of the rows after those are already in flight, leaving
+// only the X gathers on the critical path.
 //
 // The epilogue fuses the shifted-operator term (gamma*Z, Z = X for A - theta*I),
 // an axpby with a second input (beta*Yin, used for r = rhs - op x) and an
@@ -184,9 +184,13 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
       v1 = __ldg(a.val + st + i1);
     }
   };
+  // pipeline: row pointers two steps ahead, the first index/value chunk one step
+  // ahead, so neither load is on a step's critical path (only the X gathers are)
+  int pstart = 0, plen = 0;  // row pointers of the step after next
   if (rb < rend) {
     fetch_rowptr(rb, nstart, nlen);
     fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
+    if (rb + stride < rend) fetch_rowptr(rb + stride, pstart, plen);
   }
 
   for (; rb < rend; rb += stride) {
@@ -195,7 +199,10 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
     int col0 = ncol0, col1 = ncol1;
     double val0 = nval0, val1 = nval1;
     const long long rbn = rb + stride;
-    if (rbn < rend) fetch_rowptr(rbn, nstart, nlen);  // lands during the gathers below
+    nstart = pstart;
+    nlen = plen;
+    if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
+    if (rbn + stride < rend) fetch_rowptr(rbn + stride, pstart, plen);
     const int maxlen = __reduce_max_sync(FULL, len);
     double acc[NV][VEC];
 #pragma unroll
@@ -243,8 +250,6 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
       }
     }
-    // first index/value chunk of the next rows (their row pointers have arrived)
-    if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
     if (active && r < rend) {
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
