@@ -132,3 +132,65 @@ def test_alg2_two_ranks(golden_alg2):
         assert res[r][1:3] == (kept, red), res[r][:3]
     full = np.concatenate([res[0][4], res[1][4]])
     assert np.abs(full - golden_alg2["m96_b16_out"]).max() <= 1e-10
+
+
+# ---- native (C++) Alg. 3 driver vs the Python control flow -----------------------------
+
+
+def _run_both(dev, fn, *host_arrays):
+    """Run `fn(native: bool) -> (outcome, result arrays)` with the native driver on and off."""
+    from paper_2111_06552_b200 import orth as O
+
+    saved = O._NATIVE
+    try:
+        O._NATIVE = True
+        a = fn()
+        O._NATIVE = False
+        b = fn()
+    finally:
+        O._NATIVE = saved
+    return a, b
+
+
+@pytest.mark.parametrize("case", ["strict", "default", "against", "against_b", "dependent"])
+def test_native_orth_matches_python_driver(dev, golden, case):
+    from paper_2111_06552_b200 import orth_against, recursive_orth_svd
+
+    def blk(n, m, seed):
+        return np.random.default_rng(seed).uniform(-1, 1, (n, m))
+
+    b = None
+    if case in ("strict", "default"):
+        xin, basis = golden[f"orth_{case}_in"], None
+        cfg = OrthConfig(reorth_tol=1e-15 if case == "strict" else 1e-10)
+    elif case == "against":
+        xin, basis, cfg = golden["oa_in"], golden["oa_basis"], OrthConfig()
+    elif case == "against_b":
+        n = 300
+        bs = _b_for("with_b", n)
+        b = DeviceCsr.from_scipy(dev, bs)
+        basis = blk(n, 12, 5)
+        bt = torch.from_numpy(basis).to(dev.device)
+        recursive_orth_svd(dev, bt, b=b)
+        basis = bt.cpu().numpy()
+        xin, cfg = blk(n, 20, 6), OrthConfig()
+    else:
+        xin = blk(200, 24, 7)
+        xin[:, 5] = xin[:, 2]
+        xin[:, 17] = 0.0
+        basis, cfg = None, OrthConfig()
+
+    def run():
+        x = torch.from_numpy(np.ascontiguousarray(xin)).to(dev.device)
+        if basis is None:
+            out = recursive_orth_svd(dev, x, b=b, cfg=cfg)
+        else:
+            out = orth_against(dev, x, torch.from_numpy(np.ascontiguousarray(basis)).to(dev.device),
+                               b=b, cfg=cfg)
+        return out, x.cpu().numpy()
+
+    (oa, xa), (ob, xb) = _run_both(dev, run)
+    assert (oa.num_kept, oa.reduction_count, oa.replaced_indices) == \
+        (ob.num_kept, ob.reduction_count, ob.replaced_indices)
+    k = oa.num_kept
+    assert np.abs(xa[:, :k] - xb[:, :k]).max() <= 1e-12
