@@ -19,12 +19,63 @@ multi-GPU problem:
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import device as D
 from .cg import CgReport
 
-__all__ = ["LocalOps"]
+__all__ = ["LocalOps", "device_to_host_f"]
+
+_STAGE_BYTES = 32 << 20
+_stage = []  # two reusable pinned staging buffers
+
+
+def device_to_host_f(dev, X):
+    """Device block (row-major view) -> new F-order host array, through two reused pinned
+    staging buffers: the DMA of chunk i+1 overlaps the (multi-threaded) host copy of
+    chunk i, and no per-call page-locking of the result is needed.  A plain .cpu() of
+    the 210 MB cfg2 eigenvector block runs at ~2 GB/s (pageable staging + first-touch
+    page faults); this path is bounded by the host copy."""
+    n, k = X.shape
+    out = np.empty((n, k), order="F")
+    if out.size == 0:
+        return out
+    T = X.t().contiguous()  # k x n row-major == the F-order n x k layout
+    src = T.view(-1)
+    dst = torch.from_numpy(out.reshape(-1, order="F"))
+    total = src.numel()
+    chunk = _STAGE_BYTES // 8
+    if total <= chunk:
+        dst.copy_(src.cpu())
+        return out
+    if not _stage:
+        _stage.extend(torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(2))
+    side = torch.cuda.Stream(device=X.device)
+    side.wait_stream(dev.stream)
+    evs = []
+    with torch.cuda.stream(side):
+        starts = list(range(0, total, chunk))
+        for i, s in enumerate(starts[:2]):
+            e = min(s + chunk, total)
+            _stage[i][: e - s].copy_(src[s:e], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            evs.append(ev)
+        for i, s in enumerate(starts):
+            e = min(s + chunk, total)
+            evs[i].synchronize()
+            dst[s:e].copy_(_stage[i % 2][: e - s])
+            j = i + 2
+            if j < len(starts):
+                s2 = starts[j]
+                e2 = min(s2 + chunk, total)
+                _stage[j % 2][: e2 - s2].copy_(src[s2:e2], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                evs.append(ev)
+    dev.stream.wait_stream(side)
+    return out
 
 
 class LocalOps:
@@ -89,4 +140,4 @@ class LocalOps:
 
     def host_rows(self, X):
         """Local rows of a device block as a host array (F-order)."""
-        return X.t().contiguous().cpu().numpy().T
+        return device_to_host_f(self.dev, X)
