@@ -69,6 +69,10 @@ int64_t gcg_launch_count(void);
  * algorithmic HBM bytes} for cls = 0..4 in that order. */
 int gcg_prof_begin(void* ctx);
 int gcg_prof_end(void* ctx, double* out);
+/* time only every stride-th launch of each class (stride >= 1, default 1): the
+ * event records then perturb a timed region by 1/stride as much; ms, launches
+ * and bytes in gcg_prof_end refer to the sampled launches. */
+int gcg_prof_sample(void* ctx, int stride);
 
 /* ---- tier 1: reference-FFI mirror (host buffers, column-major) ----------- */
 /* out[:, c] = A @ x[:, c];  A is nrow x ncol CSR (int64 indptr/indices, f64 data);

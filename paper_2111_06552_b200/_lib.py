@@ -30,6 +30,7 @@ _SIGS = {
     "gcgeig_axpby": [_dbl, _ptr, _i64, _i64, _i64, _dbl, _ptr, _i64],
     "gcg_prof_begin": [_ptr],
     "gcg_prof_end": [_ptr, _ptr],
+    "gcg_prof_sample": [_ptr, _int],
     "gcg_spmm_csr": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64,
                      _dbl, _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
     "gcg_gram": [_ptr, _i64, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _i64, _ptr,

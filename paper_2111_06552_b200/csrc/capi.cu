@@ -124,6 +124,7 @@ int ensure(Scratch& s, size_t bytes) {
 int prof_start(Ctx* c, int cls, double bytes) {
   Prof& p = c->prof;
   if (!p.on) return -1;
+  if (p.stride > 1 && (p.seen[cls]++ % p.stride) != 0) return -1;
   if (p.used == p.cap) {
     // grow: only between profiled regions is the device flag array reallocated safely,
     // so allocate generously up front and stop recording when full
@@ -289,6 +290,14 @@ int gcg_prof_begin(void* p) {
                                       c->stream)));
   c->prof.on = true;
   c->prof.used = 0;
+  for (long long& v : c->prof.seen) v = 0;
+  return GCG_OK;
+}
+
+int gcg_prof_sample(void* p, int stride) {
+  Ctx* c = CTX(p);
+  if (!c || stride < 1) return GCG_ERR_ARG;
+  c->prof.stride = stride;
   return GCG_OK;
 }
 

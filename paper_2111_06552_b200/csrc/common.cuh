@@ -37,6 +37,8 @@ struct Prof {
   int* d_skipped = nullptr;    // device flags: the launch was a CG early-exit no-op
   int cap = 0;                 // pairs
   int used = 0;
+  int stride = 1;              // time every stride-th launch of each class
+  long long seen[PROF_NCLASS] = {0};
 };
 
 struct Ctx {

@@ -82,19 +82,25 @@ class KernelProfile:
     result[cls] = {"ms": total ms, "launches": n, "bytes": algorithmic HBM bytes}.
     """
 
-    def __init__(self, ctx):
+    def __init__(self, ctx, sample=1):
         self.ctx = ctx
+        self.sample = int(sample)
         self.result = None
 
     def __enter__(self):
+        _lib.call("gcg_prof_sample", self.ctx.h, self.sample)
         _lib.call("gcg_prof_begin", self.ctx.h)
         return self
 
     def __exit__(self, *exc):
         out = (C.c_double * (3 * len(PROF_CLASSES)))()
         _lib.call("gcg_prof_end", self.ctx.h, out)
+        _lib.call("gcg_prof_sample", self.ctx.h, 1)
+        # with sampling, ms / launches / bytes cover the timed launches (every
+        # `sample`-th of each class); rates (bytes / ms) are unaffected
         self.result = {
-            name: {"ms": out[3 * i], "launches": int(out[3 * i + 1]), "bytes": out[3 * i + 2]}
+            name: {"ms": out[3 * i], "launches": int(out[3 * i + 1]), "bytes": out[3 * i + 2],
+                   "sample": self.sample}
             for i, name in enumerate(PROF_CLASSES)
         }
         return False
