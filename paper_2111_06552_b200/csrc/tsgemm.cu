@@ -225,6 +225,26 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
   } while (0)
   if (k1 <= 16 && k2 <= 16) GO(16, 16, 16, 16);
   if (k1 <= 32 && k2 <= 32) GO(32, 32, 32, 32);
+  if (k2 <= 32 && k1 <= 256 && (k1 + 31) / 32 % 2 == 1 && k1 > 64) {
+    // k1 in (64, 96], (128, 160], (192, 224]: tiles of 96 / 160 / 224 rows (4 warps
+    // along M x 2 row groups) instead of the next multiple of 64 — e.g. the 200-row
+    // deflation / cross Grams pay 12 % padding instead of 28 %
+    const int b = (k1 + 31) / 32;  // 3, 5 or 7
+    switch (b * 8 + f2) {
+      case 3 * 8 + 1: GO(96, 8, 24, 8);
+      case 3 * 8 + 2: GO(96, 16, 24, 16);
+      case 3 * 8 + 3: GO(96, 24, 24, 24);
+      case 3 * 8 + 4: GO(96, 32, 24, 32);
+      case 5 * 8 + 1: GO(160, 8, 40, 8);
+      case 5 * 8 + 2: GO(160, 16, 40, 16);
+      case 5 * 8 + 3: GO(160, 24, 40, 24);
+      case 5 * 8 + 4: GO(160, 32, 40, 32);
+      case 7 * 8 + 1: GO(224, 8, 56, 8);
+      case 7 * 8 + 2: GO(224, 16, 56, 16);
+      case 7 * 8 + 3: GO(224, 24, 56, 24);
+      default: GO(224, 32, 56, 32);
+    }
+  }
   if (k2 <= 32 && k1 <= 256) {
     switch (f1 * 8 + f2) {
       case 1 * 8 + 1: GO(64, 8, 8, 8);
