@@ -269,10 +269,120 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
 #undef GO
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric small Gram X'X, k <= 32 (the SVQB leaf and block Grams with B = I):
+// each lane's loads X[row][8f + a] are simultaneously its A fragment (m = a,
+// k = row) and its B fragment (k = row, n = a) of column block f, so a warp
+// reads every X element once, straight into registers (four 4-row k-steps in
+// flight), and issues FN*FN DMMAs per k-step.  Warps own contiguous row
+// ranges; the CTA's warp partials are summed in warp order and the CTA
+// partials by gram_finish2_kernel — deterministic.
+template <int FN>
+__global__ void __launch_bounds__(256) gram_sym_kernel(long long n, int k,
+                                                       const double* __restrict__ X, long long ldx,
+                                                       long long rps, double* part) {
+  constexpr int U = 4;  // k-steps in flight
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fa = lane >> 2, fc = lane & 3;
+  const long long c0 = (long long)blockIdx.x * rps;
+  const long long c1 = min(n, c0 + rps);
+  const long long wr = ((c1 - c0 + 7) / 8 + 3) / 4 * 4;  // rows per warp, multiple of 4
+  const long long r0 = c0 + warp * wr;
+  const long long r1 = min(c1, r0 + wr);
+  double acc[FN][FN][2];
+#pragma unroll
+  for (int i = 0; i < FN; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (long long r = r0; r < r1; r += 4 * U) {
+    double v[U][FN];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long row = r + 4 * u + fc;
+      const bool ok = row < r1;
+#pragma unroll
+      for (int f = 0; f < FN; ++f) {
+        const int col = 8 * f + fa;
+        v[u][f] = (ok && col < k) ? X[row * ldx + col] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < FN; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], v[u][i], v[u][j]);
+  }
+  // warp partials: warps 4..7 park theirs, warps 0..3 add them (fixed pairing), then
+  // the four pair sums are added in order
+  constexpr int KW = 8 * FN;
+  __shared__ double red[4][KW * KW];
+  if (warp >= 4) {
+#pragma unroll
+    for (int i = 0; i < FN; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          red[warp - 4][(8 * i + fa) * KW + 8 * j + 2 * fc + h] = acc[i][j][h];
+  }
+  __syncthreads();
+  if (warp < 4) {
+#pragma unroll
+    for (int i = 0; i < FN; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double& t = red[warp][(8 * i + fa) * KW + 8 * j + 2 * fc + h];
+          t = acc[i][j][h] + t;
+        }
+  }
+  __syncthreads();
+  double* out = part + (long long)blockIdx.x * k * k;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int a = e / k, b = e % k;
+    out[e] = ((red[0][a * KW + b] + red[1][a * KW + b]) + red[2][a * KW + b]) + red[3][a * KW + b];
+  }
+}
+
+static int gram_sym_launch(Ctx* c, long long n, int k, const double* X, long long ldx,
+                           double alpha, double beta, double* G, long long grs, long long gcs) {
+  long long nslab = 2LL * c->num_sms;
+  const long long max_slab = (n + 1023) / 1024;
+  if (nslab > max_slab) nslab = max_slab;
+  if (nslab < 1) nslab = 1;
+  long long rps = (n + nslab - 1) / nslab;
+  rps = (rps + 31) / 32 * 32;
+  nslab = (n + rps - 1) / rps;
+  if (nslab < 1) nslab = 1;
+  GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)nslab * k * k));
+  double* part = (double*)c->partials.ptr;
+  const int ps = prof_start(c, PROF_GRAM, 8.0 * n * k);
+  switch ((k + 7) / 8) {
+    case 1: gram_sym_kernel<1><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
+    case 2: gram_sym_kernel<2><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
+    case 3: gram_sym_kernel<3><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
+    default: gram_sym_kernel<4><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
+  }
+  prof_stop(c, ps);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  const long long outs = (long long)k * k;
+  gram_finish2_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, c->stream>>>(
+      k, k, (int)nslab, part, alpha, beta, G, grs, gcs);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
 int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                 const double* Y, long long ldy, double alpha, double beta, double* G,
                 long long grs, long long gcs) {
   if (k1 <= 0 || k2 <= 0) return GCG_OK;
+  static const bool sym_on = !(getenv("GCG_GRAM_SYM") && getenv("GCG_GRAM_SYM")[0] == '0');
+  if (sym_on && X == Y && ldx == ldy && k1 == k2 && k1 <= 32 && n >= 4096)
+    return gram_sym_launch(c, n, k1, X, ldx, alpha, beta, G, grs, gcs);
   // skinny on the left: compute G' = Y'X with roles swapped (write through swapped strides)
   if (k1 <= 32 && k2 > 32 && k2 <= 256)
     return gram_launch(c, n, k2, k1, Y, ldy, X, ldx, alpha, beta, G, gcs, grs);
