@@ -67,13 +67,43 @@ __device__ __forceinline__ void stage_elems(double* dst, const double* src, int 
 
 constexpr int kStages = 3;
 
+// Bulk (TMA-engine) row copies global -> shared with mbarrier completion: one
+// instruction per row segment instead of one cp.async per 16 bytes.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)));
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
 // smem stride (doubles) >= w, even, and 4 (mod 16)
 __host__ __device__ constexpr int frag_stride(int w) { return ((w + 11) / 16) * 16 + 4; }
 
 // ---------------------------------------------------------------------------
 // Gram: CTA tile BM x BN; warps tile it WM x WN; the remaining warps split rows.
 
-template <int BM, int BN, int WM, int WN, int R, bool VEC16>
+template <int BM, int BN, int WM, int WN, int R, bool VEC16, bool BULK = false>
 __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int k2,
                                                         const double* __restrict__ X,
                                                         long long ldx,
@@ -98,18 +128,48 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
   const int nch = (int)((r1 - r0 + R - 1) / R);
   const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column (m or n)
 
+  __shared__ __align__(8) unsigned long long mbar[kStages];
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto load = [&](int ch, int st) {
     const long long rb = r0 + (long long)ch * R;
-    constexpr int PX = BM / V, PY = BN / V, P = PX + PY;
-    for (int e = tid; e < R * P; e += 256) {
-      const int rr = e / P, cc = e % P;
-      const long long row = rb + rr;
-      double* dst = smg + (st * R + rr) * W;
-      const bool ok = row < r1;
-      if (cc < PX)
-        stage_elems<VEC16>(dst, X + (ok ? row : r0) * ldx + tm0, cc, ok ? vx : 0, X);
-      else
-        stage_elems<VEC16>(dst + BM, Y + (ok ? row : r0) * ldy + tn0, cc - PX, ok ? vy : 0, Y);
+    if constexpr (BULK) {
+      // one bulk copy per row segment (threads 0.. for X, 128.. for Y); an odd
+      // trailing column and the rows past the slab end are filled by plain stores
+      const int nr = (int)min((long long)R, r1 - rb);
+      const int bx = (vx * 8) & ~15, by = (vy * 8) & ~15;
+      double* base = smg + st * R * W;
+      if (tid == 0) mbar_expect(&mbar[st], (unsigned)(nr * (bx + by)));
+      if (tid < nr) {
+        const long long row = rb + tid;
+        const double* src = X + row * ldx + tm0;
+        if (bx) bulk_g2s(base + tid * W, src, bx, &mbar[st]);
+        if (vx & 1) base[tid * W + vx - 1] = src[vx - 1];
+      } else if (tid >= 128 && tid - 128 < nr) {
+        const int t = tid - 128;
+        const long long row = rb + t;
+        const double* src = Y + row * ldy + tn0;
+        if (by) bulk_g2s(base + t * W + BM, src, by, &mbar[st]);
+        if (vy & 1) base[t * W + BM + vy - 1] = src[vy - 1];
+      }
+      for (int e = tid; e < (R - nr) * W; e += 256) base[nr * W + e] = 0.0;
+    } else {
+      constexpr int PX = BM / V, PY = BN / V, P = PX + PY;
+      for (int e = tid; e < R * P; e += 256) {
+        const int rr = e / P, cc = e % P;
+        const long long row = rb + rr;
+        double* dst = smg + (st * R + rr) * W;
+        const bool ok = row < r1;
+        if (cc < PX)
+          stage_elems<VEC16>(dst, X + (ok ? row : r0) * ldx + tm0, cc, ok ? vx : 0, X);
+        else
+          stage_elems<VEC16>(dst + BM, Y + (ok ? row : r0) * ldy + tn0, cc - PX, ok ? vy : 0, Y);
+      }
     }
   };
 
@@ -125,7 +185,8 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
     cp_commit();
   }
   for (int ch = 0; ch < nch; ++ch) {
-    cp_wait<kStages - 2>();
+    if constexpr (BULK) mbar_wait(&mbar[ch % kStages], (unsigned)((ch / kStages) & 1));
+    else cp_wait<kStages - 2>();
     __syncthreads();
     if (ch + kStages - 1 < nch) load(ch + kStages - 1, (ch + kStages - 1) % kStages);
     cp_commit();
@@ -198,7 +259,14 @@ static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long l
   const size_t sm_red = sizeof(double) * (size_t)RG * BM * BN;
   const size_t sm = sm_stage > sm_red ? sm_stage : sm_red;
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, nslab);
-  if (vec) {
+  static const bool bulk_on = !(getenv("GCG_GRAM_BULK") && getenv("GCG_GRAM_BULK")[0] == '0');
+  if (vec && bulk_on) {
+    // row segments staged by the bulk-copy engine: one instruction per row and
+    // operand per stage instead of one cp.async per 16 bytes
+    auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true, true>;
+    kernel_smem((const void*)kern, sm);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+  } else if (vec) {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true>;
     kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
