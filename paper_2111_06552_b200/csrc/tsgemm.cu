@@ -487,7 +487,7 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
 // LinComb  Y = alpha X C + beta Y: CTA tile BM rows x BN columns, warp tile
 // WM x WN, K (= m) in BK = 16 chunks through the cp.async ring.
 
-template <int BM, int BN, int WM, int WN, bool VEC16>
+template <int BM, int BN, int WM, int WN, bool VEC16, bool BULK = false>
 __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, int d,
                                                            double alpha,
                                                            const double* X,
@@ -513,9 +513,41 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
   const int vc = min(BN, d - c0);
   const int fr = lane & 3, fc = lane >> 2;
 
+  __shared__ __align__(8) unsigned long long mbar[kStages];
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto load = [&](int kb, int st) {
     const int k0 = kb * BK;
     const int vk = min(BK, m - k0);
+    if constexpr (BULK) {
+      // bulk copies: threads 0..BM-1 one X row chunk each, threads BM.. one C row each;
+      // a K tail zero-fills the unused X columns and C rows (stale shared memory could
+      // hold non-finite bit patterns), an odd trailing element is a plain store
+      const int bk = (vk * 8) & ~15, bc = (vc * 8) & ~15;
+      const int nr = (int)min((long long)BM, n - r0);
+      if (tid == 0) mbar_expect(&mbar[st], (unsigned)(nr * bk + vk * bc));
+      double* xd = xs + st * XS;
+      double* cd = cs + st * CS;
+      if (tid < nr) {
+        const double* src = X + (r0 + tid) * ldx + k0;
+        if (bk) bulk_g2s(xd + tid * XW, src, bk, &mbar[st]);
+        if (vk & 1) xd[tid * XW + vk - 1] = src[vk - 1];
+        for (int e = vk; e < BK; ++e) xd[tid * XW + e] = 0.0;
+      }
+      const int kk = BM < 256 ? tid - BM : tid;  // the C row this thread stages
+      if (kk >= 0 && kk < vk) {
+        const double* src = C + (long long)(k0 + kk) * ldc + c0;
+        if (bc) bulk_g2s(cd + kk * CW, src, bc, &mbar[st]);
+        if (vc & 1) cd[kk * CW + vc - 1] = src[vc - 1];
+      }
+      for (int e = tid; e < (BK - vk) * CW; e += 256) cd[vk * CW + e] = 0.0;
+      return;
+    }
     constexpr int PX = BK / V;
     for (int e = tid; e < BM * PX; e += 256) {
       const int rr = e / PX, cc = e % PX;
@@ -543,7 +575,8 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
     cp_commit();
   }
   for (int kb = 0; kb < nk; ++kb) {
-    cp_wait<kStages - 2>();
+    if constexpr (BULK) mbar_wait(&mbar[kb % kStages], (unsigned)((kb / kStages) & 1));
+    else cp_wait<kStages - 2>();
     __syncthreads();
     if (kb + kStages - 1 < nk) load(kb + kStages - 1, (kb + kStages - 1) % kStages);
     cp_commit();
@@ -587,7 +620,13 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
   const size_t sm =
       sizeof(double) * (size_t)kStages * (BM * frag_stride(16) + 16 * frag_stride(BN));
   dim3 grid((unsigned)((n + BM - 1) / BM), (d + BN - 1) / BN);
-  if (vec) {
+  static const bool bulk_on = !(getenv("GCG_LINCOMB_BULK") && getenv("GCG_LINCOMB_BULK")[0] == '0');
+  if (BM < 256 && vec && bulk_on && al16(C) && ldc % 2 == 0) {
+    // X row chunks and C rows staged by the bulk-copy engine (one instruction per row)
+    auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true, true>;
+    kernel_smem((const void*)kern, sm);
+    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+  } else if (vec) {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true>;
     kernel_smem((const void*)kern, sm);
     kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
