@@ -329,7 +329,8 @@ def _mgs_block(st, start, stop):
         D.col_scale(dev, torch.full((1,), inv, dtype=torch.float64, device=dev.device), col)
         if fwd.size:
             cf = fwd * inv
-            D.lincomb(dev, col, torch.from_numpy(cf[None, :].copy()).to(dev.device),
+            D.lincomb(dev, col, torch.from_numpy(cf[None, :].copy()).pin_memory().to(
+                dev.device, non_blocking=True),
                       st.x[:, j + 1:stop], alpha=-1.0, beta=1.0)
             st.d[j + 1:stop] = np.maximum(st.d[j + 1:stop] - cf * cf, 0.0)
         st.d[j] = 1.0

@@ -139,6 +139,14 @@ def _stagnation_flag(history, window):
     return not (tail[-1].first_unconverged_residual < 0.9 * tail[0].first_unconverged_residual)
 
 
+def _h2d(dev, arr):
+    """Small host vector -> device without a host sync: staged through pinned memory
+    (torch's caching host allocator) and copied asynchronously on the solver stream.
+    A pageable-memory copy would wait for all queued device work first."""
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).pin_memory().to(
+        dev.device, non_blocking=True)
+
+
 class _Timer:
     """Per-step GPU time of one iteration (the reference's t_step* wall clocks,
     solver.py:269-445): a CUDA event is recorded on the solver stream at every step
@@ -424,7 +432,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
                 aw = S.apply_a(v[:, sx + np_:sx + np_ + nw])
                 cross = dev.empty(m, nw)
                 ops.gram(basis, aw, cross)
-            lam_x = torch.from_numpy(lam[locked:sx].copy()).to(dev.device)
+            lam_x = _h2d(dev, lam[locked:sx])
             D.abar_assemble(dev, d, lam_x, p_coupling if np_ else None, cross, abar)
         abar_defect = None
         if cfg.cross_check_abar and abar_prev is not None:
@@ -539,7 +547,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
             # STEP 6: damped inverse power via block CG (solver.py:386-396)
             x_act = v[:, locked:locked + bs_eff]
             w_region = v[:, sx + np_:sx + np_ + bs_eff]
-            scale = torch.from_numpy(lam[locked:locked + bs_eff] - theta).to(dev.device)
+            scale = _h2d(dev, lam[locked:locked + bs_eff] - theta)
             rhs = dev.empty(nloc, bs_eff)
             if Bop is not None:
                 ops.spmm(Bop, x_act, rhs)
