@@ -127,6 +127,13 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
   const int vx = min(BM, k1 - tm0), vy = min(BN, k2 - tn0);
   const int nch = (int)((r1 - r0 + R - 1) / R);
   const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column (m or n)
+  // Bulk mode: row runs that start 8 bytes past a 16-byte boundary (views at an odd
+  // column of an even-ld arena) are copied from one element earlier, so the tile
+  // sits at +1 in its shared-memory row; the Y part starts at BM + 2 (16-B aligned).
+  static_assert(!BULK || W >= BM + BN + 3, "room for the shifted runs");
+  const int sxo = BULK ? (int)(((uintptr_t)(X + tm0) >> 3) & 1) : 0;
+  const int syo = BULK ? (int)(((uintptr_t)(Y + tn0) >> 3) & 1) : 0;
+  const int xo = sxo, yo = BULK ? BM + 2 + syo : BM;  // shared-memory column of element 0
 
   __shared__ __align__(8) unsigned long long mbar[kStages];
   if constexpr (BULK) {
@@ -142,20 +149,21 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
       // one bulk copy per row segment (threads 0.. for X, 128.. for Y); an odd
       // trailing column and the rows past the slab end are filled by plain stores
       const int nr = (int)min((long long)R, r1 - rb);
-      const int bx = (vx * 8) & ~15, by = (vy * 8) & ~15;
+      const int ex = vx + sxo, ey = vy + syo;  // elements copied, incl. the lead-in
+      const int bx = (ex * 8) & ~15, by = (ey * 8) & ~15;
       double* base = smg + st * R * W;
       if (tid == 0) mbar_expect(&mbar[st], (unsigned)(nr * (bx + by)));
       if (tid < nr) {
         const long long row = rb + tid;
-        const double* src = X + row * ldx + tm0;
+        const double* src = X + row * ldx + tm0 - sxo;
         if (bx) bulk_g2s(base + tid * W, src, bx, &mbar[st]);
-        if (vx & 1) base[tid * W + vx - 1] = src[vx - 1];
+        if (ex & 1) base[tid * W + ex - 1] = src[ex - 1];
       } else if (tid >= 128 && tid - 128 < nr) {
         const int t = tid - 128;
         const long long row = rb + t;
-        const double* src = Y + row * ldy + tn0;
-        if (by) bulk_g2s(base + t * W + BM, src, by, &mbar[st]);
-        if (vy & 1) base[t * W + BM + vy - 1] = src[vy - 1];
+        const double* src = Y + row * ldy + tn0 - syo;
+        if (by) bulk_g2s(base + t * W + BM + 2, src, by, &mbar[st]);
+        if (ey & 1) base[t * W + BM + 2 + ey - 1] = src[ey - 1];
       }
       for (int e = tid; e < (R - nr) * W; e += 256) base[nr * W + e] = 0.0;
     } else {
@@ -196,9 +204,9 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
       const double* rowp = base + (ks * 4 + fr) * W;
       double a[FM], b[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) a[i] = rowp[wm0 + i * 8 + fc];
+      for (int i = 0; i < FM; ++i) a[i] = rowp[xo + wm0 + i * 8 + fc];
 #pragma unroll
-      for (int j = 0; j < FN; ++j) b[j] = rowp[BM + wn0 + j * 8 + fc];
+      for (int j = 0; j < FN; ++j) b[j] = rowp[yo + wn0 + j * 8 + fc];
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -260,7 +268,9 @@ static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long l
   const size_t sm = sm_stage > sm_red ? sm_stage : sm_red;
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, nslab);
   static const bool bulk_on = !(getenv("GCG_GRAM_BULK") && getenv("GCG_GRAM_BULK")[0] == '0');
-  if (vec && bulk_on) {
+  // bulk staging needs every row run at the same 16-byte phase: even leading dimensions
+  // (a run starting 8 bytes past a boundary is copied from one element earlier)
+  if (bulk_on && ldx % 2 == 0 && ldy % 2 == 0) {
     // row segments staged by the bulk-copy engine: one instruction per row and
     // operand per stage instead of one cp.async per 16 bytes
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true, true>;
@@ -517,6 +527,7 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
   const int nk = (m + BK - 1) / BK;
   const int vc = min(BN, d - c0);
   const int fr = lane & 3, fc = lane >> 2;
+  const int xo = BULK ? (int)(((uintptr_t)X >> 3) & 1) : 0;  // X runs' 8-byte phase
 
   __shared__ __align__(8) unsigned long long mbar[kStages];
   if constexpr (BULK) {
@@ -533,16 +544,19 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
       // bulk copies: threads 0..BM-1 one X row chunk each, threads BM.. one C row each;
       // a K tail zero-fills the unused X columns and C rows (stale shared memory could
       // hold non-finite bit patterns), an odd trailing element is a plain store
-      const int bk = (vk * 8) & ~15, bc = (vc * 8) & ~15;
+      // (rows starting 8 bytes past a 16-byte boundary are copied from one element
+      // earlier and sit at +1 in shared memory, see xo)
+      const int ex = vk + xo;
+      const int bk = (ex * 8) & ~15, bc = (vc * 8) & ~15;
       const int nr = (int)min((long long)BM, n - r0);
       if (tid == 0) mbar_expect(&mbar[st], (unsigned)(nr * bk + vk * bc));
       double* xd = xs + st * XS;
       double* cd = cs + st * CS;
       if (tid < nr) {
-        const double* src = X + (r0 + tid) * ldx + k0;
+        const double* src = X + (r0 + tid) * ldx + k0 - xo;
         if (bk) bulk_g2s(xd + tid * XW, src, bk, &mbar[st]);
-        if (vk & 1) xd[tid * XW + vk - 1] = src[vk - 1];
-        for (int e = vk; e < BK; ++e) xd[tid * XW + e] = 0.0;
+        if (ex & 1) xd[tid * XW + ex - 1] = src[ex - 1];
+        for (int e = vk; e < BK; ++e) xd[tid * XW + xo + e] = 0.0;
       }
       const int kk = BM < 256 ? tid - BM : tid;  // the C row this thread stages
       if (kk >= 0 && kk < vk) {
@@ -591,7 +605,7 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
     for (int ks = 0; ks < BK / 4; ++ks) {
       double a[FM], b[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) a[i] = xb[(wm0 + i * 8 + fc) * XW + ks * 4 + fr];
+      for (int i = 0; i < FM; ++i) a[i] = xb[(wm0 + i * 8 + fc) * XW + ks * 4 + fr + xo];
 #pragma unroll
       for (int j = 0; j < FN; ++j) b[j] = cb[(ks * 4 + fr) * CW + wn0 + j * 8 + fc];
 #pragma unroll
@@ -626,7 +640,7 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
       sizeof(double) * (size_t)kStages * (BM * frag_stride(16) + 16 * frag_stride(BN));
   dim3 grid((unsigned)((n + BM - 1) / BM), (d + BN - 1) / BN);
   static const bool bulk_on = !(getenv("GCG_LINCOMB_BULK") && getenv("GCG_LINCOMB_BULK")[0] == '0');
-  if (BM < 256 && vec && bulk_on && al16(C) && ldc % 2 == 0) {
+  if (BM < 256 && bulk_on && ldx % 2 == 0 && al16(C) && ldc % 2 == 0) {
     // X row chunks and C rows staged by the bulk-copy engine (one instruction per row)
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true, true>;
     kernel_smem((const void*)kern, sm);

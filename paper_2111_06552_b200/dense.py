@@ -50,7 +50,9 @@ def sym_eig_full(ctx, m, symmetrize=False):
         m = m.clone()
         D.symmetrize(ctx, m)
     w = ctx.empty(n)
-    v = ctx.empty(n, n)
+    # even row stride: coefficient blocks sliced from it stay 16-byte aligned row by
+    # row, which the bulk-staged LinComb needs
+    v = ctx.empty(n, n + (n & 1))[:, :n]
     D.syev(ctx, m, w, v)
     return SpectralDecomposition(w, v)
 

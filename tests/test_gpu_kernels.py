@@ -134,6 +134,31 @@ def test_gram_vs_numpy(dev, n, k1, k2):
     assert torch.equal(g, g2)  # deterministic: bit-stable run to run (test_kernels.py:74-85)
 
 
+@pytest.mark.parametrize("off1,k1,off2,k2", [(3, 200, 205, 20), (1, 199, 210, 21), (0, 160, 161, 40),
+                                              (5, 96, 101, 96), (2, 17, 40, 7)])
+def test_gram_lincomb_odd_column_views(dev, off1, k1, off2, k2):
+    """Views at odd columns of an even-ld arena (basis = v[:, locked:], locked odd):
+    the bulk-staged kernels copy those rows from one element earlier."""
+    n = 40000
+    rng = np.random.default_rng(off1 + k1)
+    arena = rng.standard_normal((n, 260))
+    A = rm(dev, arena)
+    x, y = arena[:, off1:off1 + k1], arena[:, off2:off2 + k2]
+    g = dev.empty(k1, k2)
+    D.gram(dev, A[:, off1:off1 + k1], A[:, off2:off2 + k2], g)
+    scale = np.sqrt((x * x).sum(0)).max() * np.sqrt((y * y).sum(0)).max()
+    assert np.abs(host(g) - x.T @ y).max() / scale <= 1e-13
+    c = rng.standard_normal((k1, k2 + 70))
+    out = dev.empty(n, k2 + 70)
+    D.lincomb(dev, A[:, off1:off1 + k1], rm(dev, c), out)
+    assert rel_err(host(out), x @ c) <= 1e-13
+    # in place over the leading columns of the odd-offset view (the [X|P] update)
+    d = min(k1, k2 + 70)
+    cc = rng.standard_normal((k1, d))
+    D.lincomb(dev, A[:, off1:off1 + k1], rm(dev, cc), A[:, off1:off1 + d])
+    assert rel_err(host(A[:, off1:off1 + d]), x @ cc) <= 1e-13
+
+
 def test_gram_strided_out_and_accumulate(dev):
     rng = np.random.default_rng(9)
     x, y = rng.standard_normal((300, 3)), rng.standard_normal((300, 2))
