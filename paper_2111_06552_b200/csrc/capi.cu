@@ -476,7 +476,9 @@ int gcg_syev(void* p, int64_t m, const double* A, int64_t lda, double* w, double
              int64_t ldv) {
   Ctx* c = CTX(p);
   if (!c || m <= 0 || lda < m || ldv < m) return GCG_ERR_ARG;
-  if (m <= 64) return dense_syev_jacobi(c, (int)m, A, lda, w, V, ldv);
+  static const char* impl = getenv("GCG_SYEV");
+  const bool tri_small = impl && impl[0] == 't';  // GCG_SYEV=tri: tridiagonal path for m <= 64 too
+  if (m <= 64 && !tri_small) return dense_syev_jacobi(c, (int)m, A, lda, w, V, ldv);
   return dense_syev_cusolver(c, (int)m, A, lda, w, V, ldv);
 }
 

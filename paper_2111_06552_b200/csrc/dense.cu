@@ -389,9 +389,15 @@ __global__ void vec_fix_kernel(int m, const double* Vcm, double* V, long long ld
   for (int i = threadIdx.x; i < m; i += blockDim.x) V[(long long)i * ldv + j] = sg * col[i];
 }
 
+bool dense_syev_tridiag_ok(int m);
+int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, double* w,
+                       double* V, long long ldv);
+
 int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int symmetrize,
                             double* w, double* V, long long ldv) {
   if (m <= 0) return GCG_ERR_ARG;
+  // orders up to 232: the one-CTA tridiagonalisation path (eig.cu), no cuSOLVER
+  if (dense_syev_tridiag_ok(m)) return dense_syev_tridiag(c, m, A, lda, symmetrize, w, V, ldv);
   cusolverDnSetStream(c->solver, c->stream);
   int lwork = 0;
   const size_t mat = (size_t)m * m;

@@ -231,7 +231,7 @@ def test_axpby_copy_scale_dots(dev):
     assert rel_err(host(out), (x * y).sum(0)) <= 1e-12
 
 
-@pytest.mark.parametrize("m", [1, 2, 5, 16, 33, 64, 65, 120, 200])
+@pytest.mark.parametrize("m", [1, 2, 5, 16, 33, 64, 65, 120, 200, 231, 232, 233])
 def test_syev_vs_lapack(dev, m):
     rng = np.random.default_rng(m)
     a = rng.standard_normal((m, m))
@@ -246,6 +246,66 @@ def test_syev_vs_lapack(dev, m):
     assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12
     # sign rule of dense.py:63-71 (non-degenerate random spectrum => columns match LAPACK's)
     assert np.abs(V - vv).max() <= 1e-9
+
+
+def _degenerate(m, seed, kind):
+    rng = np.random.default_rng(seed)
+    if kind == "lap3d":          # 6^3 Laplacian: eigenvalue multiplicities 1, 3 and 6
+        n1 = round(m ** (1 / 3))
+        t = 2 * np.eye(n1) - np.eye(n1, k=1) - np.eye(n1, k=-1)
+        i = np.eye(n1)
+        return np.kron(np.kron(t, i), i) + np.kron(np.kron(i, t), i) + np.kron(np.kron(i, i), t)
+    if kind == "clusters":       # rotated spectrum with exact and 1e-9-close clusters, a 0
+        w = np.repeat(rng.standard_normal(m // 4), 4)[:m].copy()
+        w[: m // 8] += 1e-9 * np.arange(m // 8)
+        w[-1] = 0.0
+        q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+        a = (q * w) @ q.T
+        return (a + a.T) / 2
+    if kind == "rr":             # Rayleigh-Ritz shape: diag(Ritz values) coupled to a P/W block
+        d = 160 if m > 160 else m - 10
+        a = np.zeros((m, m))
+        a[:d, :d] = np.diag(np.sort(rng.uniform(0.006, 0.3, d)))
+        b = 1e-3 * rng.standard_normal((m - d, d))
+        c = rng.standard_normal((m - d, m - d))
+        a[d:, :d] = b
+        a[:d, d:] = b.T
+        a[d:, d:] = 0.5 * (c + c.T) + 2 * np.eye(m - d)
+        return a
+    if kind == "diag":           # already tridiagonal-free: every reflector is the identity
+        return np.diag(np.arange(m, dtype=float)[::-1] % 7)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("m,kind", [(216, "lap3d"), (125, "lap3d"), (200, "clusters"),
+                                    (96, "clusters"), (200, "rr"), (120, "rr"), (100, "diag")])
+def test_syev_degenerate_spectra(dev, m, kind):
+    """Eigensolver on the structures RR matrices have: exact multiplicities (grid
+    symmetries), near-degenerate clusters, an exact zero, the diag + coupling shape.
+    Eigenvalues vs LAPACK; vectors by residual, orthonormality and the cluster
+    subspaces (any orthonormal basis of a degenerate eigenspace is valid)."""
+    a = _degenerate(m, m, kind)
+    w = dev.empty(m)
+    v = dev.empty(m, m)
+    D.syev(dev, rm(dev, a), w, v)
+    ww, vv = np.linalg.eigh(a)
+    scale = max(1.0, np.abs(ww).max())
+    lam, V = host(w), host(v)
+    assert np.abs(lam - ww).max() <= 1e-13 * scale * 10
+    assert np.abs(a @ V - V * lam).max() <= 1e-12 * scale
+    assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12
+    # the span of each cluster matches LAPACK's
+    edges = np.flatnonzero(np.diff(ww) > 1e-6 * scale) + 1
+    for blk in np.split(np.arange(m), edges):
+        s = np.linalg.svd(vv[:, blk].T @ V[:, blk], compute_uv=False)
+        assert s.min() >= 1 - 1e-10
+    # sign rule of dense.py:63-71: the largest-magnitude entry of every column is positive
+    lead = np.abs(V).argmax(axis=0)
+    assert (V[lead, np.arange(m)] > 0).all()
+    # bit-stable run to run
+    w2, v2 = dev.empty(m), dev.empty(m, m)
+    D.syev(dev, rm(dev, a), w2, v2)
+    assert torch.equal(w, w2) and torch.equal(v, v2)
 
 
 @pytest.mark.parametrize("m,lo,hi,workers", [(30, 1, 30, 1), (80, 1, 64, 1), (80, 5, 17, 1),
