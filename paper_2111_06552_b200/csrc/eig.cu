@@ -401,7 +401,17 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
   // the unnormalised solution is at most ~1/eps times the start vector
 }
 
-// 4. Orthonormalise each cluster (consecutive eigenvalues with gaps <= ortol):
+// Eigenvalues closer than kTightGap ||T|| form a tight cluster: inverse iteration
+// gives them vectors that are arbitrary inside the (near-)invariant subspace, so
+// they are Gram-Schmidt orthogonalised.  Every other pair is already orthogonal to
+// ~eps ||T|| / gap <= ~1e-9 and is finished by the global first-order Loewdin step
+// (loewdin_*), which, like Gram-Schmidt, moves each vector only along eigenvectors
+// whose eigenvalue differs by the gap that caused the error — residuals stay at
+// eps ||T|| (dstein clusters at 1e-3 ||T|| instead, which on Rayleigh-Ritz spectra
+// chains most eigenvalues into one long sequential Gram-Schmidt).
+constexpr double kTightGap = 1e-7;
+
+// 4. Orthonormalise each tight cluster (consecutive eigenvalues, gaps <= ortol):
 // one CTA per potential cluster start; classical Gram-Schmidt twice per vector
 // against the earlier members, then 2-norm normalisation (fixed-order sums).
 __global__ void __launch_bounds__(256) cluster_kernel(int m, const double* __restrict__ lam,
@@ -409,7 +419,7 @@ __global__ void __launch_bounds__(256) cluster_kernel(int m, const double* __res
   __shared__ double red[8][33];
   __shared__ double coef[kEigMaxM];
   const int b = blockIdx.x;
-  const double ortol = 1e-3 * norms[0];
+  const double ortol = kTightGap * norms[0];
   if (b > 0 && lam[b] - lam[b - 1] <= ortol) return;  // not a cluster start
   int end = b + 1;
   while (end < m && lam[end] - lam[end - 1] <= ortol) ++end;
@@ -519,6 +529,36 @@ __global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, const doub
     }
 }
 
+// 4b. Global first-order Loewdin orthonormalisation Z <- Z (3/2 I - 1/2 Z'Z) (the
+// residual non-orthogonality after 4 is <= ~1e-9, so the result is orthonormal to
+// ~1e-18).  G = Z'Z: one CTA per column j of G, one warp per entry (fixed order).
+__global__ void __launch_bounds__(256) loewdin_gram_kernel(int m, const double* __restrict__ Z,
+                                                           double* __restrict__ G) {
+  const int j = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* zj = Z + (size_t)j * m;
+  for (int i = warp; i < m; i += 8) {
+    const double* zi = Z + (size_t)i * m;
+    double s = 0.0;
+    for (int k = lane; k < m; k += 32) s = fma(zi[k], zj[k], s);
+    s = warp_sum(s);
+    if (lane == 0) G[(size_t)j * m + i] = s;
+  }
+}
+// Z2[:, j] = 3/2 z_j - 1/2 sum_i z_i G[i, j]; one CTA per column j, thread per row
+__global__ void __launch_bounds__(256) loewdin_apply_kernel(int m, const double* __restrict__ Z,
+                                                            const double* __restrict__ G,
+                                                            double* __restrict__ Z2) {
+  __shared__ double gj[kEigMaxM];
+  const int j = blockIdx.x;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) gj[i] = G[(size_t)j * m + i];
+  __syncthreads();
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s = fma(Z[(size_t)i * m + k], gj[i], s);
+    Z2[(size_t)j * m + k] = fma(1.5, Z[(size_t)j * m + k], -0.5 * s);
+  }
+}
+
 __global__ void vec_fix_kernel(int m, const double* Vcm, double* V, long long ldv);
 
 bool dense_syev_tridiag_ok(int m) {
@@ -551,10 +591,15 @@ int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, d
     invit_kernel<<<(m + 31) / 32, 32, 0, c->stream>>>(m, dd, ee, w, Z, W, pass, norms);
     cluster_kernel<<<m, 256, 0, c->stream>>>(m, w, Z, norms);
   }
+  double* G = W;            // the inverse-iteration factors are dead now
+  double* Z2 = W + mm;
+  loewdin_gram_kernel<<<m, 256, 0, c->stream>>>(m, Z, G);
+  loewdin_apply_kernel<<<m, 256, 0, c->stream>>>(m, Z, G, Z2);
+  Z = Z2;
   backtr_kernel<<<(m + kBtWarps * kBtCols - 1) / (kBtWarps * kBtCols), 32 * kBtWarps, 0,
                   c->stream>>>(m, Vr, tt, Z);
   vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, Z, V, ldv);
-  g_launches += 8;
+  g_launches += 10;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
 }

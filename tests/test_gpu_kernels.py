@@ -292,8 +292,8 @@ def test_syev_degenerate_spectra(dev, m, kind):
     scale = max(1.0, np.abs(ww).max())
     lam, V = host(w), host(v)
     assert np.abs(lam - ww).max() <= 1e-13 * scale * 10
-    assert np.abs(a @ V - V * lam).max() <= 1e-12 * scale
-    assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12
+    assert np.abs(a @ V - V * lam).max() <= 1e-13 * scale
+    assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-13
     # the span of each cluster matches LAPACK's
     edges = np.flatnonzero(np.diff(ww) > 1e-6 * scale) + 1
     for blk in np.split(np.arange(m), edges):
