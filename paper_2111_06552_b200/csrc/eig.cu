@@ -47,7 +47,7 @@ __host__ __device__ inline int tri_off(int m, int j) { return j * m - (j * (j - 
 
 static size_t tri_smem(int m) {
   // packed lower triangle | (v, w) previous step | (v, w) current | p | slots
-  return sizeof(double) * ((size_t)m * (m + 1) / 2 + 1 + 9 * (size_t)m + 64);
+  return sizeof(double) * ((size_t)m * (m + 1) / 2 + 1 + 8 * (size_t)m + 64);
 }
 
 // 1. Householder tridiagonalisation (dsytd2, UPLO = 'L') in one CTA, the packed
@@ -73,8 +73,7 @@ __global__ void __launch_bounds__(kTriThreads)
   // (v, w) pairs: previous step's (the deferred update) and the current step's
   double2* P = reinterpret_cast<double2*>(L + (((size_t)m * (m + 1) / 2 + 1) & ~(size_t)1));
   double2* Q = P + m;
-  double* pv = reinterpret_cast<double*>(Q + m);  // p = tau A22 v
-  double* part = pv + m;                          // [4][m] C1 row partial sums
+  double* part = reinterpret_cast<double*>(Q + m);  // [4][m] row partial sums of p
   double* slot = part + 4 * m;                    // scalars
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // load: coalesced row-major reads, scattered shared-memory writes
@@ -190,19 +189,31 @@ __global__ void __launch_bounds__(kTriThreads)
     }
     if (row < m) part[q * m + row] = acc;
     __syncthreads();
-    for (int i = s0 + tid; i < m; i += kTriThreads)
-      pv[i] = t * (((part[i] + part[m + i]) + part[2 * m + i]) + part[3 * m + i]);
-    __syncthreads();
-    // D. w = p - (t/2)(p'v) v (warp 0)
-    if (warp == 0 && !(dbg & 4)) {
+    // D. (warp 0) p = t * (sum of the 4 row partials, fixed order), w = p - (t/2)(p'v) v.
+    // No barrier after it: warp 0 goes straight on to the next step's B, the other
+    // warps wait at B's barrier.
+    if (warp == 0) {
+      constexpr int kPer = (kEigMaxM + 31) / 32;
+      double pl[kPer];
       double s = 0.0;
-#pragma unroll 8
-      for (int i = s0 + lane; i < m; i += 32) s = fma(pv[i], Q[i].x, s);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = s0 + lane + 32 * u;
+        pl[u] = 0.0;
+        if (i < m) {
+          pl[u] = t * (((part[i] + part[m + i]) + part[2 * m + i]) + part[3 * m + i]);
+          s = fma(pl[u], Q[i].x, s);
+        }
+      }
       const double a2 = -0.5 * t * warp_sum(s);
-#pragma unroll 8
-      for (int i = lane; i < m; i += 32) Q[i].y = i >= s0 ? fma(a2, Q[i].x, pv[i]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = s0 + lane + 32 * u;
+        if (i < m) Q[i].y = fma(a2, Q[i].x, pl[u]);
+      }
+      for (int i = lane; i < s0; i += 32) Q[i].y = 0.0;
+      __syncwarp();
     }
-    __syncthreads();
     double2* tq = P;  // the current (v, w) become the deferred update of the next step
     P = Q;
     Q = tq;
