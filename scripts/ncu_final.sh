@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo "launch list rc=$?"
 python scripts/launch_shares.py gpurun_out/launches_bench.csv gpurun_out/launch_shares.txt "$SHORT" > /dev/null
 gzip -f gpurun_out/launches_bench.csv
-for K in ${KERNELS:-spmm_csr_kernel gram_dmma_kernel lincomb_ts_kernel lincomb_dmma_kernel cg_update_kernel cg_pupdate_kernel gram_sym_kernel}; do
+for K in ${KERNELS:-spmm_csr_kernel gram_dmma_kernel lincomb_ts_kernel lincomb_dmma_kernel cg_update_kernel cg_pupdate_kernel gram_sym_kernel tridiag_kernel}; do
   ncu --set full --clock-control none --import-source on -k regex:$K -s ${SKIP:-40} -c 1 \
       -o gpurun_out/full_$K $SHORT > gpurun_out/ncu_full_$K.log 2>&1
   echo "$K rc=$?"
