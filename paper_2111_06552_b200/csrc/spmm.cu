@@ -114,7 +114,7 @@ __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
   return doubles > 0 ? 4 : 4;  // every shape: 64 registers, one grid size
 }
 
-template <int VEC, int NV>
+template <int VEC, int NV, bool SELF>
 __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
     spmm_csr_kernel(SpmmArgs a) {
   if (a.skip != nullptr && *a.skip) {
@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
     if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
     if (rbn + stride < rend) fetch_rowptr(rbn + stride, pstart, plen);
     const int maxlen = __reduce_max_sync(FULL, len);
+    // SELF (Z and/or W are X itself): keep the row's own X values from the
+    // diagonal gather instead of re-reading them in the epilogue
+    double xr[SELF ? NV : 1][VEC];
+    bool have_diag = false;
     double acc[NV][VEC];
 #pragma unroll
     for (int q = 0; q < NV; ++q)
@@ -242,6 +246,17 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             }
           }
         }
+        if constexpr (SELF) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool dg = ok[u] && (long long)j[u] == r;
+            have_diag |= dg;
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) xr[q][e] = dg ? xv[u][q][e] : xr[q][e];
+          }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -258,8 +273,12 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
         double y[VEC], t[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = a.alpha * acc[q][e];
+        const bool self_ok = SELF && have_diag;
         if (a.gamma != 0.0) {
-          if (a.vepi) {
+          if (SELF && self_ok && a.Z == a.X) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) t[e] = xr[SELF ? q : 0][e];
+          } else if (a.vepi) {
             VecT<VEC>::ld(a.Z + r * a.ldz + c, t);
           } else {
 #pragma unroll
@@ -285,7 +304,10 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
           for (int e = 0; e < VEC; ++e) a.Y[r * a.ldy + c + e] = y[e];
         }
         if (a.dot_mode == 1) {
-          if (a.vepi) {
+          if (SELF && self_ok && a.W == a.X) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) t[e] = xr[SELF ? q : 0][e];
+          } else if (a.vepi) {
             VecT<VEC>::ld(a.W + r * a.ldw + c, t);
           } else {
 #pragma unroll
@@ -355,7 +377,14 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
 
 template <int VEC, int NV>
 static void launch_one(Ctx* c, const SpmmArgs& a, int grid) {
-  spmm_csr_kernel<VEC, NV><<<grid, kSpmmThreads, 0, c->stream>>>(a);
+  // the CG forms (shift and/or dot against X itself, same ld): own row from the gathers
+  static const bool self_env = getenv("GCG_SPMM_SELF") ? atoi(getenv("GCG_SPMM_SELF")) != 0 : true;
+  const bool self = self_env && ((a.gamma != 0.0 && a.Z == a.X && a.ldz == a.ldx) ||
+                                 (a.dot_mode == 1 && a.W == a.X && a.ldw == a.ldx));
+  if (self)
+    spmm_csr_kernel<VEC, NV, true><<<grid, kSpmmThreads, 0, c->stream>>>(a);
+  else
+    spmm_csr_kernel<VEC, NV, false><<<grid, kSpmmThreads, 0, c->stream>>>(a);
 }
 
 template <int VEC>
