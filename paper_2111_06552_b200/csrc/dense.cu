@@ -110,8 +110,12 @@ __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJac
         const double apq = a[p][q], app = a[p][p], aqq = a[q][q];
         double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq)) && apq != 0.0) {
-          const double theta = (aqq - app) * (0.5 / apq);
-          t = 1.0 / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+          // Rutishauser's rotation with reciprocals instead of divisions (the
+          // rotation chain is the round's critical path: ~4 long-latency ops)
+          const double theta = (aqq - app) * (0.5 * __drcp_rn(apq));
+          const double h2 = fma(theta, theta, 1.0);
+          const double h = h2 * rsqrt(h2);  // sqrt(1 + theta^2)
+          t = __drcp_rn(fabs(theta) + h);
           if (theta < 0.0) t = -t;
           c = rsqrt(fma(t, t, 1.0));
           s = t * c;
