@@ -90,19 +90,38 @@ struct VecT<2> {
     *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
   }
 };
-// 32-byte accesses (LDG.E.ENL2.256 on sm_100): a 20-column row is 5 lanes
+// 32-byte accesses: a 20-column row is 5 lanes.  Explicit 256-bit PTX vectors —
+// a double4 dereference is emitted as two LDG.E.128 whenever ptxas cannot prove
+// the 32-byte alignment from the address arithmetic (the gathers' row pointers),
+// and two 16-byte halves of each 32-byte sector double the L1 sector traffic.
 template <>
 struct VecT<4> {
   static __device__ __forceinline__ void load(const double* p, double* o) {
-    const double4 v = *reinterpret_cast<const double4*>(p);
-    o[0] = v.x;
-    o[1] = v.y;
-    o[2] = v.z;
-    o[3] = v.w;
+    long long a, b, c, d;
+    asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+        : "l"(p));
+    o[0] = __longlong_as_double(a);
+    o[1] = __longlong_as_double(b);
+    o[2] = __longlong_as_double(c);
+    o[3] = __longlong_as_double(d);
   }
-  static __device__ __forceinline__ void ld(const double* p, double* o) { load(p, o); }
+  static __device__ __forceinline__ void ld(const double* p, double* o) {
+    long long a, b, c, d;
+    asm volatile("ld.global.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p)
+                 : "memory");
+    o[0] = __longlong_as_double(a);
+    o[1] = __longlong_as_double(b);
+    o[2] = __longlong_as_double(c);
+    o[3] = __longlong_as_double(d);
+  }
   static __device__ __forceinline__ void st(double* p, const double* o) {
-    *reinterpret_cast<double4*>(p) = make_double4(o[0], o[1], o[2], o[3]);
+    asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(__double_as_longlong(o[0])),
+                 "l"(__double_as_longlong(o[1])), "l"(__double_as_longlong(o[2])),
+                 "l"(__double_as_longlong(o[3]))
+                 : "memory");
   }
 };
 
@@ -378,7 +397,7 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
 template <int VEC, int NV>
 static void launch_one(Ctx* c, const SpmmArgs& a, int grid) {
   // the CG forms (shift and/or dot against X itself, same ld): own row from the gathers
-  static const bool self_env = getenv("GCG_SPMM_SELF") ? atoi(getenv("GCG_SPMM_SELF")) != 0 : true;
+  static const bool self_env = getenv("GCG_SPMM_SELF") ? atoi(getenv("GCG_SPMM_SELF")) != 0 : false;
   const bool self = self_env && ((a.gamma != 0.0 && a.Z == a.X && a.ldz == a.ldx) ||
                                  (a.dot_mode == 1 && a.W == a.X && a.ldw == a.ldx));
   if (self)
