@@ -18,12 +18,13 @@
 //                       range, ~11 rounds), dstebz's pivmin safeguard.
 //   3. invit_kernel     eigenvectors of T by inverse iteration (dstein): one
 //                       thread per eigenvalue, LU of T - lambda I with partial
-//                       pivoting (dlagtf / dlagts, tiny pivots perturbed).
-//   4. cluster_kernel   classical Gram-Schmidt twice inside each cluster of
-//                       eigenvalues closer than 1e-3 ||T||_1 (dstein's ORTOL),
-//                       then normalisation; (3)+(4) run twice.
-//   5. backtr_kernel    Z = Q Z_T, reflectors applied in reverse order, one CTA
-//                       per 8-column block of Z held in shared memory.
+//                       pivoting (dlagtf / dlagts, tiny pivots perturbed); the
+//                       second pass reuses the factors.
+//   4. cluster_kernel   classical Gram-Schmidt twice inside each tight cluster
+//                       (gaps <= 1e-7 ||T||_1), then normalisation; (3)+(4) run
+//                       twice; then a global first-order Loewdin step.
+//   5. backtr_kernel    Z = Q Z_T, reflectors applied in reverse order, each warp
+//                       holding 4 columns of Z in registers.
 // then the reference's sign rule (vec_fix_kernel in dense.cu).
 //
 // Every reduction has a fixed order (bit-stable run to run).  Eigenvalues agree
@@ -67,7 +68,7 @@ static size_t tri_smem(int m) {
 // column j holds v_j in rows j+1..m-1, v_j[j+1] = 1).
 __global__ void __launch_bounds__(kTriThreads)
     tridiag_kernel(int m, const double* __restrict__ A, long long lda, int sym, double* d,
-                   double* e, double* tau, double* Vr, int dbg) {
+                   double* e, double* tau, double* Vr) {
   extern __shared__ double tsm[];
   double* L = tsm;                          // packed lower triangle, by columns
   // (v, w) pairs: previous step's (the deferred update) and the current step's
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kTriThreads)
   for (int j = 0; j + 2 < m; ++j) {
     const int s0 = j + 1;
     // B. column j: deferred update, reflector (warp 0)
-    if (warp == 0 && !(dbg & 8)) {
+    if (warp == 0) {
       const int oj = tri_off(m, j);
       const double2 pj = P[j];
       const double vpj = pj.x, wpj = pj.y;
@@ -349,15 +350,17 @@ __device__ __forceinline__ double start_entry(int j, int k) {
 // 3. Inverse iteration for eigenvector j of T: solve (T - lam_j I) z = b by LU with
 // partial pivoting (dlagtf), b = start vector (pass 0) or the current column of Z
 // (pass 1); writes z (unnormalised) into column j of Z (column-major, ld m).
-// Per-thread factors interleaved [k][m] in W (coalesced across threads); the
-// backward pass multiplies by stored reciprocal pivots, so the only long-latency
-// operation left on the dependent chain is one reciprocal per non-swapping step.
+// Per-thread factors interleaved [k][m] in W (coalesced across threads).  Pass 0
+// factors (one reciprocal per step on the dependent chain) and keeps the
+// multipliers and row swaps; pass 1 only re-runs the substitutions (one FMA per
+// step on the chain).  The backward pass multiplies by stored reciprocal pivots.
 __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const double* e,
                                                    const double* __restrict__ lam,
                                                    double* __restrict__ Z, double* __restrict__ W,
                                                    int pass,
                                                    const double* __restrict__ norms) {
   __shared__ double sdv[kEigMaxM], sev[kEigMaxM];
+  extern __shared__ double ysm[];  // [m][32]: this thread's forward-substituted rhs
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
     sdv[k] = d[k];
     sev[k] = k + 1 < m ? e[k] : 0.0;
@@ -367,47 +370,110 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
   e = sev;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  double* R1 = W;                    // 1 / U(k, k)
-  double* U2 = W + (size_t)m * m;
-  double* U3 = W + 2 * (size_t)m * m;
-  double* Y = W + 3 * (size_t)m * m;
-  const double lj = lam[j];
-  const double tnorm = norms[0];
-  const double tiny = fmax(tnorm, 1e-300) * 2.220446049250313e-16;
-  auto fixp = [&](double u) { return fabs(u) < tiny ? (u < 0.0 ? -tiny : tiny) : u; };
+  const size_t mm = (size_t)m * m;
+  double* R1 = W;            // 1 / U(k, k)
+  double* U2 = W + mm;
+  double* U3 = W + 2 * mm;
+  double* const Yb = ysm + threadIdx.x;  // Yb[k * 32]
+#define YS(k) Yb[(size_t)(k) * 32]
+  double* ML = W + 4 * mm;   // multipliers; negative zero-bias flag in SW
+  double* SW = W + 5 * mm;   // 1.0 where rows k, k+1 were swapped
   double* z = Z + (size_t)j * m;
-  double dg = d[0] - lj;            // current pivot-row diagonal
-  double sp = m > 1 ? e[0] : 0.0;   // current pivot-row superdiagonal
-  double yk = pass == 0 ? start_entry(j, 0) : z[0];
+  if (pass == 0) {
+    const double lj = lam[j];
+    const double tnorm = norms[0];
+    const double tiny = fmax(tnorm, 1e-300) * 2.220446049250313e-16;
+    auto fixp = [&](double u) { return fabs(u) < tiny ? (u < 0.0 ? -tiny : tiny) : u; };
+    double dg = d[0] - lj;            // current pivot-row diagonal
+    double sp = m > 1 ? e[0] : 0.0;   // current pivot-row superdiagonal
+    double yk = start_entry(j, 0);
 #pragma unroll 4
-  for (int k = 0; k + 1 < m; ++k) {
-    const double sub = e[k];                        // T(k+1, k)
-    const double a1 = d[k + 1] - lj;                // T(k+1, k+1)
-    const double s1 = k + 2 < m ? e[k + 1] : 0.0;   // T(k+1, k+2)
-    const double bk1 = pass == 0 ? start_entry(j, k + 1) : z[k + 1];
-    const size_t o = (size_t)k * m + j;
-    // partial pivoting without divergence: swap rows k, k+1 when |sub| > |dg|
-    const bool sw = fabs(sub) > fabs(dg);
-    const double rp = __drcp_rn(sw ? sub : fixp(dg));
-    const double mult = (sw ? dg : sub) * rp;
-    R1[o] = rp;
-    U2[o] = sw ? a1 : sp;
-    U3[o] = sw ? s1 : 0.0;
-    Y[o] = sw ? bk1 : yk;
-    yk = fma(-mult, sw ? bk1 : yk, sw ? yk : bk1);
-    dg = fma(-mult, sw ? a1 : sp, sw ? sp : a1);
-    sp = sw ? -mult * s1 : s1;
+    for (int k = 0; k + 1 < m; ++k) {
+      const double sub = e[k];                        // T(k+1, k)
+      const double a1 = d[k + 1] - lj;                // T(k+1, k+1)
+      const double s1 = k + 2 < m ? e[k + 1] : 0.0;   // T(k+1, k+2)
+      const double bk1 = start_entry(j, k + 1);
+      const size_t o = (size_t)k * m + j;
+      // partial pivoting without divergence: swap rows k, k+1 when |sub| > |dg|
+      const bool sw = fabs(sub) > fabs(dg);
+      const double rp = __drcp_rn(sw ? sub : fixp(dg));
+      const double mult = (sw ? dg : sub) * rp;
+      R1[o] = rp;
+      U2[o] = sw ? a1 : sp;
+      U3[o] = sw ? s1 : 0.0;
+      YS(k) = sw ? bk1 : yk;
+      ML[o] = mult;
+      SW[o] = sw ? 1.0 : 0.0;
+      yk = fma(-mult, sw ? bk1 : yk, sw ? yk : bk1);
+      dg = fma(-mult, sw ? a1 : sp, sw ? sp : a1);
+      sp = sw ? -mult * s1 : s1;
+    }
+    R1[(size_t)(m - 1) * m + j] = __drcp_rn(fixp(dg));
+    YS(m - 1) = yk;
+  } else {
+    // forward substitution of the new right-hand side with the stored factors
+    // loads are batched 8 steps ahead of the chain: the stores to Y would otherwise
+    // keep the compiler from hoisting the ML / SW / z loads (same base pointer)
+    double yk = z[0];
+    constexpr int B = 8;
+    int k = 0;
+    for (; k + B < m; k += B) {
+      double mlb[B], swb[B], bb[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const size_t o = (size_t)(k + u) * m + j;
+        mlb[u] = ML[o];
+        swb[u] = SW[o];
+        bb[u] = z[k + u + 1];
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const bool sw = swb[u] != 0.0;
+        YS(k + u) = sw ? bb[u] : yk;
+        yk = fma(-mlb[u], sw ? bb[u] : yk, sw ? yk : bb[u]);
+      }
+    }
+    for (; k + 1 < m; ++k) {
+      const size_t o = (size_t)k * m + j;
+      const double bk1 = z[k + 1];
+      const bool sw = SW[o] != 0.0;
+      YS(k) = sw ? bk1 : yk;
+      yk = fma(-ML[o], sw ? bk1 : yk, sw ? yk : bk1);
+    }
+    YS(m - 1) = yk;
   }
-  double x2 = 0.0, x1 = yk * __drcp_rn(fixp(dg));
+  double x2 = 0.0, x1 = YS(m - 1) * R1[(size_t)(m - 1) * m + j];
   z[m - 1] = x1;
-#pragma unroll 8
-  for (int k = m - 2; k >= 0; --k) {
-    const size_t o = (size_t)k * m + j;
-    const double x0 = (Y[o] - U2[o] * x1 - U3[o] * x2) * R1[o];
-    z[k] = x0;
-    x2 = x1;
-    x1 = x0;
+  {
+    constexpr int B = 8;
+    int k = m - 2;
+    for (; k - B + 1 >= 0; k -= B) {
+      double yb[B], u2[B], u3[B], r1[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const size_t o = (size_t)(k - u) * m + j;
+        yb[u] = YS(k - u);
+        u2[u] = U2[o];
+        u3[u] = U3[o];
+        r1[u] = R1[o];
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double x0 = (yb[u] - u2[u] * x1 - u3[u] * x2) * r1[u];
+        z[k - u] = x0;
+        x2 = x1;
+        x1 = x0;
+      }
+    }
+    for (; k >= 0; --k) {
+      const size_t o = (size_t)k * m + j;
+      const double x0 = (YS(k) - U2[o] * x1 - U3[o] * x2) * R1[o];
+      z[k] = x0;
+      x2 = x1;
+      x1 = x0;
+    }
   }
+#undef YS
   // no normalisation here: the cluster kernel normalises every column (2-norm);
   // the unnormalised solution is at most ~1/eps times the start vector
 }
@@ -584,22 +650,23 @@ int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, d
                        double* V, long long ldv) {
   if (m < 3 || m > kEigMaxM) return GCG_ERR_ARG;
   const size_t mm = (size_t)m * m;
-  // workspace: d, e, tau (3m) | Vr (m^2) | Z (m^2) | inverse-iteration factors (4 m^2) | norms
-  GCG_TRY(ensure(c->dense, sizeof(double) * (3 * (size_t)m + 6 * mm + 8) + 256));
+  // workspace: d, e, tau (3m) | Vr (m^2) | Z (m^2) | inverse-iteration factors (6 m^2) | norms
+  GCG_TRY(ensure(c->dense, sizeof(double) * (3 * (size_t)m + 8 * mm + 8) + 256));
   double* dd = (double*)c->dense.ptr;
   double* ee = dd + m;
   double* tt = ee + m;
   double* Vr = tt + m;
   double* Z = Vr + mm;
   double* W = Z + mm;
-  double* norms = W + 4 * mm;
+  double* norms = W + 6 * mm;
   const size_t smem = tri_smem(m);
   kernel_smem((const void*)tridiag_kernel, smem);
-  static const int tdbg = getenv("GCG_TRI_DBG") ? atoi(getenv("GCG_TRI_DBG")) : 0;
-  tridiag_kernel<<<1, kTriThreads, smem, c->stream>>>(m, A, lda, sym, dd, ee, tt, Vr, tdbg);
+  tridiag_kernel<<<1, kTriThreads, smem, c->stream>>>(m, A, lda, sym, dd, ee, tt, Vr);
   bisect_kernel<<<(m + 7) / 8, 256, 0, c->stream>>>(m, dd, ee, w, norms);
   for (int pass = 0; pass < 2; ++pass) {
-    invit_kernel<<<(m + 31) / 32, 32, 0, c->stream>>>(m, dd, ee, w, Z, W, pass, norms);
+    const size_t ysm = sizeof(double) * 32 * (size_t)m;
+    kernel_smem((const void*)invit_kernel, ysm);
+    invit_kernel<<<(m + 31) / 32, 32, ysm, c->stream>>>(m, dd, ee, w, Z, W, pass, norms);
     cluster_kernel<<<m, 256, 0, c->stream>>>(m, w, Z, norms);
   }
   double* G = W;            // the inverse-iteration factors are dead now
