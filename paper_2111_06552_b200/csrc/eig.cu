@@ -35,6 +35,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "async.cuh"
 #include "common.cuh"
 
 namespace gcg {
@@ -537,66 +538,89 @@ __global__ void __launch_bounds__(256) cluster_kernel(int m, const double* __res
 // registers (lane holds rows lane + 32 s) and applies all reflectors last-first,
 // with the next reflector's loads issued before the current one's reductions; no
 // block barriers.
-constexpr int kBtWarps = 2;
+constexpr int kBtWarps = 8;
 constexpr int kBtCols = 4;
 constexpr int kBtRows = (kEigMaxM + 31) / 32;
+constexpr int kBtChunk = 16;  // reflectors per shared-memory stage
+static size_t backtr_smem(int m) { return sizeof(double) * 2 * kBtChunk * ((size_t)m + 1); }
 __global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, const double* __restrict__ Vr,
                                                                const double* __restrict__ tau,
                                                                double* Z) {
+  extern __shared__ __align__(16) double bsm[];  // [2][kBtChunk][m] reflectors + [2][kBtChunk] tau
+  double* vbuf = bsm;
+  double* tbuf = bsm + 2 * kBtChunk * (size_t)m;
   const int lane = threadIdx.x & 31;
   const int col0 = (blockIdx.x * kBtWarps + (threadIdx.x >> 5)) * kBtCols;
-  if (col0 >= m) return;
+  const bool live = col0 < m;
   double r[kBtCols][kBtRows];
 #pragma unroll
   for (int cc = 0; cc < kBtCols; ++cc)
 #pragma unroll
     for (int s = 0; s < kBtRows; ++s) {
       const int k = lane + 32 * s;
-      r[cc][s] = (k < m && col0 + cc < m) ? Z[(size_t)(col0 + cc) * m + k] : 0.0;
+      r[cc][s] = (live && k < m && col0 + cc < m) ? Z[(size_t)(col0 + cc) * m + k] : 0.0;
     }
-  auto load_v = [&](int j, double* vv) {
-    const double* vj = Vr + (size_t)j * m;
-#pragma unroll
-    for (int s = 0; s < kBtRows; ++s) {
-      const int k = lane + 32 * s;
-      vv[s] = (k > j && k < m) ? __ldg(vj + k) : 0.0;
+  // reflectors are applied last-first: chunk c covers j = jtop - c*kBtChunk down to ..-kBtChunk+1
+  const int jtop = m - 3;
+  const int nchunks = jtop >= 0 ? jtop / kBtChunk + 1 : 0;
+  auto stage = [&](int cidx, int buf) {
+    const int jhi = jtop - cidx * kBtChunk;
+    const int cnt = min(kBtChunk, jhi + 1);
+    double* dst = vbuf + (size_t)buf * kBtChunk * m;
+    for (int e = threadIdx.x; e < cnt * m; e += blockDim.x) {
+      const int q = e / m, k = e - q * m;
+      const int j = jhi - q;
+      cp_async8(dst + (size_t)q * m + k, Vr + (size_t)j * m + k, k > j);
     }
+    if (threadIdx.x < cnt) cp_async8(tbuf + buf * kBtChunk + threadIdx.x, tau + jhi - threadIdx.x, true);
+    cp_commit();
   };
-  double vv[kBtRows], vn[kBtRows];
-  int j = m - 3;
-  double t = 0.0, tn = 0.0;
-  if (j >= 0) {
-    load_v(j, vv);
-    t = __ldg(tau + j);
-  }
-  for (; j >= 0; --j) {
-    if (j > 0) {
-      load_v(j - 1, vn);
-      tn = __ldg(tau + j - 1);
+  if (nchunks > 0) stage(0, 0);
+  for (int cidx = 0; cidx < nchunks; ++cidx) {
+    const int buf = cidx & 1;
+    if (cidx + 1 < nchunks) {
+      stage(cidx + 1, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
-    if (t != 0.0) {
-      double dot[kBtCols];
+    __syncthreads();
+    const int jhi = jtop - cidx * kBtChunk;
+    const int cnt = min(kBtChunk, jhi + 1);
+    const double* vb = vbuf + (size_t)buf * kBtChunk * m;
+    if (live) {
+      for (int q = 0; q < cnt; ++q) {
+        const double t = tbuf[buf * kBtChunk + q];
+        if (t == 0.0) continue;
+        const double* vj = vb + (size_t)q * m;
+        double vv[kBtRows];
 #pragma unroll
-      for (int cc = 0; cc < kBtCols; ++cc) {
-        dot[cc] = 0.0;
+        for (int s = 0; s < kBtRows; ++s) {
+          const int k = lane + 32 * s;
+          vv[s] = k < m ? vj[k] : 0.0;  // zero-filled above the reflector's first row
+        }
+        double dot[kBtCols];
 #pragma unroll
-        for (int s = 0; s < kBtRows; ++s) dot[cc] = fma(vv[s], r[cc][s], dot[cc]);
-      }
+        for (int cc = 0; cc < kBtCols; ++cc) {
+          dot[cc] = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+          for (int s = 0; s < kBtRows; ++s) dot[cc] = fma(vv[s], r[cc][s], dot[cc]);
+        }
 #pragma unroll
-        for (int cc = 0; cc < kBtCols; ++cc) dot[cc] += __shfl_xor_sync(0xffffffffu, dot[cc], o);
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int cc = 0; cc < kBtCols; ++cc) {
-        const double f = t * dot[cc];
+          for (int cc = 0; cc < kBtCols; ++cc) dot[cc] += __shfl_xor_sync(0xffffffffu, dot[cc], o);
 #pragma unroll
-        for (int s = 0; s < kBtRows; ++s) r[cc][s] = fma(-f, vv[s], r[cc][s]);
+        for (int cc = 0; cc < kBtCols; ++cc) {
+          const double f = t * dot[cc];
+#pragma unroll
+          for (int s = 0; s < kBtRows; ++s) r[cc][s] = fma(-f, vv[s], r[cc][s]);
+        }
       }
     }
-#pragma unroll
-    for (int s = 0; s < kBtRows; ++s) vv[s] = vn[s];
-    t = tn;
+    __syncthreads();  // buffer 'buf' is restaged two chunks later
   }
+  if (!live) return;
 #pragma unroll
   for (int cc = 0; cc < kBtCols; ++cc)
 #pragma unroll
@@ -674,8 +698,9 @@ int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, d
   loewdin_gram_kernel<<<m, 256, 0, c->stream>>>(m, Z, G);
   loewdin_apply_kernel<<<m, 256, 0, c->stream>>>(m, Z, G, Z2);
   Z = Z2;
-  backtr_kernel<<<(m + kBtWarps * kBtCols - 1) / (kBtWarps * kBtCols), 32 * kBtWarps, 0,
-                  c->stream>>>(m, Vr, tt, Z);
+  kernel_smem((const void*)backtr_kernel, backtr_smem(m));
+  backtr_kernel<<<(m + kBtWarps * kBtCols - 1) / (kBtWarps * kBtCols), 32 * kBtWarps,
+                  backtr_smem(m), c->stream>>>(m, Vr, tt, Z);
   vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, Z, V, ldv);
   g_launches += 10;
   GCG_CHECK_LAUNCH();
