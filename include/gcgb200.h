@@ -208,6 +208,13 @@ int gcg_svqb_prepare(void* ctx, int64_t w, const double* G, int64_t ldg, double 
 int gcg_deflate_status(void* ctx, int64_t K, int64_t w, const double* R, int64_t ldr,
                        const double* dnew, int64_t dstride, double dgks, double* status);
 /* out = #{ j : vals[j] <= rel * max(max(vals), 0) } written as a double. */
+/* solver._build_p (solver.py:167-199) on one device: writes the momentum block's
+ * coefficients (m x kept, row-major, ldp) into phat and kept into *kept_out (0 = no
+ * momentum block).  coeffs is the m x d Ritz coefficient block (ldc); the group is
+ * columns gs..gs+gw-1 with its first num_x_rows rows zeroed.  Two host reads. */
+int gcg_build_p(void* ctx, int64_t m, int64_t d, const double* coeffs, int64_t ldc,
+                int64_t num_x_rows, int64_t gs, int64_t gw, double dep_tol, double* phat,
+                int64_t ldp, int64_t* kept_out);
 int gcg_count_le(void* ctx, int64_t len, const double* vals, double rel, double* out);
 /* out[:, j] = V[:, off + j] / sqrt(w[off + j]) for j < m - off. */
 int gcg_scale_rsqrt(void* ctx, int64_t m, int64_t off, const double* V, int64_t ldv,

@@ -33,6 +33,8 @@ _SIGS = {
     "gcg_prof_sample": [_ptr, _int],
     "gcg_spmm_csr": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64,
                      _dbl, _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
+    "gcg_build_p": [_ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _i64, _dbl, _ptr, _i64,
+                    C.POINTER(_i64)],
     "gcg_gram": [_ptr, _i64, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _i64, _ptr,
                  _i64, _ptr],
     "gcg_lincomb": [_ptr, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64],

@@ -261,6 +261,7 @@ int gcg_ctx_destroy(void* p) {
   release(c->host_tmp4);
   release(c->dense);
   release(c->orth);
+  release(c->buildp);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
@@ -533,6 +534,92 @@ int gcg_max_abs_diff(void* p, int64_t m, int64_t n, const double* A, int64_t lda
   Ctx* c = CTX(p);
   if (!c || m < 0 || n < 0 || lda < n || (B && ldb < n) || !out) return GCG_ERR_ARG;
   return max_abs_diff_launch(c, (int)m, (int)n, A, lda, B, ldb, out);
+}
+
+// ---- native momentum block -------------------------------------------------
+
+static int syev_dispatch(Ctx* c, int m, const double* A, long long lda, double* w, double* V,
+                         long long ldv) {
+  static const char* impl = getenv("GCG_SYEV");
+  const bool tri_small = impl && impl[0] == 't';
+  if (m <= 64 && !tri_small) return dense_syev_jacobi(c, m, A, lda, w, V, ldv);
+  return dense_syev_cusolver(c, m, A, lda, w, V, ldv);
+}
+
+static int read_pinned(Ctx* c, const double* dev, int count) {
+  if (!c->pinned) {
+    if (cudaHostAlloc((void**)&c->pinned, 64 * sizeof(double), cudaHostAllocDefault) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return GCG_ERR_ALLOC;
+    }
+  }
+  GCG_TRY(cuda_status(cudaMemcpyAsync(c->pinned, dev, sizeof(double) * count,
+                                      cudaMemcpyDeviceToHost, c->stream)));
+  return cuda_status(cudaStreamSynchronize(c->stream));
+}
+
+// solver._orthonormalize_small (solver.py:167-199 helper): g = pt'pt, eigh, drop
+// eigenvalues <= rel * max, q = pt V / sqrt(w) over the kept ones; one host read.
+static int orth_small(Ctx* c, int m, int gw, const double* pt, long long ldpt, double rel,
+                      double* q, long long ldq, int* kept, double* g, double* V, double* w,
+                      double* scaled, double* status) {
+  GCG_TRY(dgemm_launch(c, 1, 0, gw, gw, m, 1.0, pt, ldpt, pt, ldpt, 0.0, g, gw));
+  GCG_TRY(symmetrize_launch(c, gw, g, gw));
+  GCG_TRY(syev_dispatch(c, gw, g, gw, w, V, gw));
+  GCG_TRY(count_le_launch(c, gw, w, rel, status));
+  GCG_TRY(read_pinned(c, status, 1));
+  const int bad = (int)c->pinned[0];
+  *kept = 0;
+  if (bad >= gw) return GCG_OK;
+  const int k = gw - bad;
+  GCG_TRY(scale_rsqrt_launch(c, gw, bad, V, gw, w, scaled, k));
+  GCG_TRY(dgemm_launch(c, 0, 0, m, k, gw, 1.0, pt, ldpt, scaled, k, 0.0, q, ldq));
+  *kept = k;
+  return GCG_OK;
+}
+
+// solver._build_p (solver.py:167-199) for one device: the momentum block's Ritz
+// coefficients, projected against the new X coefficients (twice), orthonormalised
+// (dropping dependent directions, dep_tol), projected once more and
+// re-orthonormalised (1e-4).  Same operations and decisions as the Python
+// driver's build_p, two pinned host reads instead of two Python round trips.
+int gcg_build_p(void* p, int64_t m, int64_t d, const double* coeffs, int64_t ldc,
+                int64_t num_x_rows, int64_t gs, int64_t gw, double dep_tol, double* phat,
+                int64_t ldp, int64_t* kept_out) {
+  Ctx* c = CTX(p);
+  if (!c || !kept_out) return GCG_ERR_ARG;
+  *kept_out = 0;
+  if (gw <= 0 || m <= num_x_rows) return GCG_OK;
+  if (m <= 0 || d <= 0 || gs < 0 || gs + gw > d || ldc < d || !coeffs || !phat || ldp < gw ||
+      num_x_rows < 0 || gw > 1024)
+    return GCG_ERR_ARG;
+  const size_t sz_pt = (size_t)m * gw, sz_tmp = (size_t)d * gw, sz_g = (size_t)gw * gw;
+  GCG_TRY(ensure(c->buildp, sizeof(double) * (2 * sz_pt + sz_tmp + 3 * sz_g + gw + 8) + 256));
+  double* pt = (double*)c->buildp.ptr;
+  double* q = pt + sz_pt;
+  double* tmp = q + sz_pt;
+  double* g = tmp + sz_tmp;
+  double* V = g + sz_g;
+  double* scaled = V + sz_g;
+  double* w = scaled + sz_g;
+  double* status = w + gw;
+  const int M = (int)m, D = (int)d, GW = (int)gw;
+  GCG_TRY(copy_launch(c, m, GW, coeffs + gs, ldc, pt, GW));
+  if (num_x_rows > 0) GCG_TRY(fill_launch(c, num_x_rows, GW, 0.0, pt, GW));
+  for (int rep = 0; rep < 2; ++rep) {
+    GCG_TRY(dgemm_launch(c, 1, 0, D, GW, M, 1.0, coeffs, ldc, pt, GW, 0.0, tmp, GW));
+    GCG_TRY(dgemm_launch(c, 0, 0, M, GW, D, -1.0, coeffs, ldc, tmp, GW, 1.0, pt, GW));
+  }
+  int kept = 0;
+  GCG_TRY(orth_small(c, M, GW, pt, GW, dep_tol, q, GW, &kept, g, V, w, scaled, status));
+  if (kept == 0) return GCG_OK;
+  GCG_TRY(dgemm_launch(c, 1, 0, D, kept, M, 1.0, coeffs, ldc, q, GW, 0.0, tmp, kept));
+  GCG_TRY(dgemm_launch(c, 0, 0, M, kept, D, -1.0, coeffs, ldc, tmp, kept, 1.0, q, GW));
+  int kept2 = 0;
+  GCG_TRY(orth_small(c, M, kept, q, GW, 1e-4, phat, ldp, &kept2, g, V, w, scaled, status));
+  *kept_out = kept2;
+  return GCG_OK;
 }
 
 int gcg_count_le(void* p, int64_t len, const double* vals, double rel, double* out) {

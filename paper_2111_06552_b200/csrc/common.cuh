@@ -59,6 +59,7 @@ struct Ctx {
   Scratch host_tmp4;
   Scratch dense;      // small dense temporaries (eigensolver staging)
   Scratch orth;       // native orthogonalisation: status, Gram, SVQB coefficients, B*block
+  Scratch buildp;     // native momentum block (gcg_build_p)
   double* pinned = nullptr;  // pinned host slots for decision reads
   int* sync_flag = nullptr;
   cudaEvent_t ev = nullptr;

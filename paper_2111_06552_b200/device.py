@@ -230,6 +230,18 @@ def dgemm(ctx, A, B, Cm, ta=False, tb=False, alpha=1.0, beta=0.0):
     return Cm
 
 
+def build_p(ctx, coeffs, num_x_rows, group_start, group_width, dep_tol):
+    """solver._build_p on one device (gcg_build_p): the momentum coefficients (m x kept) or None."""
+    m, d = coeffs.shape
+    phat = ctx.empty(m, group_width)
+    kept = C.c_int64(0)
+    _lib.call("gcg_build_p", ctx.h, m, d, _p(coeffs), _ld(coeffs), int(num_x_rows),
+              int(group_start), int(group_width), float(dep_tol), _p(phat), _ld(phat),
+              C.byref(kept))
+    k = int(kept.value)
+    return phat[:, :k] if k > 0 else None
+
+
 def symmetrize(ctx, A):
     _lib.call("gcg_symmetrize", ctx.h, A.shape[0], _p(A), _ld(A))
     return A

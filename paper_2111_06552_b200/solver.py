@@ -20,6 +20,8 @@ Two parity switches that the reference does not have:
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 
@@ -28,6 +30,9 @@ import torch
 
 from . import device as D
 from .dense import sym_eig_full, sym_eig_range_split
+
+# GCG_PY_BUILD_P=1: the Python driver for the momentum block (A/B and debugging)
+_PY_BUILD_P = os.environ.get("GCG_PY_BUILD_P", "0") == "1"
 from .errors import AllDependent, InvalidShape
 from .mvops import LocalOps
 from .operators import DeviceProblem, as_device_problem
@@ -280,6 +285,9 @@ class _Solve:
         if group_width <= 0 or m <= num_x_rows:
             return None
         d = coeffs.shape[1]
+        if self.ops.size == 1 and not _PY_BUILD_P:
+            # native: same operations and decisions, two pinned host reads (gcg_build_p)
+            return D.build_p(dev, coeffs, num_x_rows, group_start, group_width, dep_tol)
         pt = dev.empty(m, group_width)
         D.copy(dev, coeffs[:, group_start:group_start + group_width], pt)
         D.fill(dev, pt[:num_x_rows], 0.0)
