@@ -245,3 +245,45 @@ def test_history_bookkeeping():
     assert all(y >= x for x, y in zip(conv, conv[1:]))
     assert rep.total_reductions >= sum(h.orth_reductions for h in rep.history)
     assert rep.max_projection_dim <= 14 + 2 * 2 or rep.max_projection_dim <= 40
+
+
+@pytest.mark.parametrize("m,d,nx,gs,gw,dep", [(200, 160, 160, 20, 20, 1e-10), (120, 80, 80, 0, 20, 1e-10),
+                                              (60, 40, 40, 10, 20, 1e-10), (90, 60, 45, 30, 30, 1e-3)])
+def test_native_build_p_matches_python_driver(m, d, nx, gs, gw, dep):
+    """gcg_build_p (solver.py:167-199 on device, two pinned reads) equals the Python
+    driver's sequence of the same kernels: same kept width, same block."""
+    import torch
+
+    from paper_2111_06552_b200 import device as D
+    from paper_2111_06552_b200 import solver as S
+
+    dev = D.default_context()
+    rng = np.random.default_rng(m + gw)
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    coeffs = torch.from_numpy(np.ascontiguousarray(q[:, :d])).to(dev.device)
+    if dep > 1e-6:  # force dependent directions in the projected group
+        coeffs[:, gs + gw - 3:gs + gw] = coeffs[:, gs:gs + 3]
+    native = D.build_p(dev, coeffs, nx, gs, gw, dep)
+
+    class _Ops:  # the single-device ops surface build_p uses (broadcast is a no-op)
+        size = 1
+
+        @staticmethod
+        def broadcast(t):
+            return t
+
+    helper = S._Solve.__new__(S._Solve)
+    helper.dev = dev
+    helper.ops = _Ops()
+    helper.scalar = dev.empty(8)
+    old = S._PY_BUILD_P
+    try:
+        S._PY_BUILD_P = True
+        py = helper.build_p(coeffs, nx, gs, gw, dep)
+    finally:
+        S._PY_BUILD_P = old
+    if native is None or py is None:
+        assert native is None and py is None
+        return
+    assert native.shape == py.shape
+    assert torch.equal(native, py)  # same kernels in the same order: same bits
