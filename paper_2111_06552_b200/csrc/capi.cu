@@ -71,6 +71,12 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
                           const double* X, long long ldx, const double* BX, long long ldbx,
                           const double* lam, int mode, double* out);
 
+// GCG_PDL=0 turns programmatic dependent launch off (A/B switch)
+bool pdl_enabled() {
+  static const bool on = !(getenv("GCG_PDL") && getenv("GCG_PDL")[0] == '0');
+  return on;
+}
+
 void kernel_smem(const void* kern, size_t bytes) {
   static std::mutex mu;
   static std::vector<std::pair<const void*, size_t>> done;

@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
                                                         const double* spart, int nsp,
                                                         double* part, CgState s, int par,
                                                         int* prof_skipped) {
+  pdl_wait();
+  pdl_trigger();
   if (*s.skip) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       *s.live = 0;
@@ -242,6 +244,8 @@ __global__ void __launch_bounds__(256) cg_pupdate_kernel(long long n, int k, dou
                                                          long long rows_per_cta,
                                                          const double* upart, int nup, CgState s,
                                                          int par, int* prof_skipped) {
+  pdl_wait();
+  pdl_trigger();
   if (!*s.live) {
     if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
     return;
@@ -462,8 +466,8 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       nred = 1;
     }
     int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
-    cg_update_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, R, Q, rpc, red, nred, upart, s, it & 1,
-                                                   prof_skip_slot(c, ps));
+    pdl_launch(cg_update_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, R, (const double*)Q,
+               (long long)rpc, red, nred, upart, s, it & 1, prof_skip_slot(c, ps));
     prof_stop(c, ps);
     red = upart;
     nred = ugrid;
@@ -473,8 +477,8 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       nred = 1;
     }
     ps = prof_start(c, PROF_CG_PUPDATE, 40.0 * n * k);
-    cg_pupdate_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, x, ldx, R, P, rpc, red, nred, s,
-                                                    it & 1, prof_skip_slot(c, ps));
+    pdl_launch(cg_pupdate_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, x, (long long)ldx,
+               (const double*)R, P, (long long)rpc, red, nred, s, it & 1, prof_skip_slot(c, ps));
     prof_stop(c, ps);
     g_launches += 2;
     GCG_CHECK_LAUNCH();

@@ -111,6 +111,36 @@ inline int grid_for(long long work_items, int items_per_cta, int ctas_per_sm, in
   return (int)(need < cap ? need : cap);
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with pdl_launch may be
+// scheduled while its predecessor on the stream drains; it must call pdl_wait()
+// before touching anything the predecessor writes (the wait returns once the
+// predecessor grid has completed and its memory is visible; a no-op for ordinary
+// launches).  pdl_trigger() lets the successor start launching early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, block, smem, stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // profiling: prof_start returns a pair slot (or -1 when off), prof_stop closes it
 int prof_start(Ctx* c, int cls, double bytes);
 void prof_stop(Ctx* c, int slot);

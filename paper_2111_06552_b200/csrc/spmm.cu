@@ -136,6 +136,8 @@ __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
 template <int VEC, int NV, bool SELF>
 __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
     spmm_csr_kernel(SpmmArgs a) {
+  pdl_wait();
+  pdl_trigger();
   if (a.skip != nullptr && *a.skip) {
     if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
     return;
@@ -401,9 +403,9 @@ static void launch_one(Ctx* c, const SpmmArgs& a, int grid) {
   const bool self = self_env && ((a.gamma != 0.0 && a.Z == a.X && a.ldz == a.ldx) ||
                                  (a.dot_mode == 1 && a.W == a.X && a.ldw == a.ldx));
   if (self)
-    spmm_csr_kernel<VEC, NV, true><<<grid, kSpmmThreads, 0, c->stream>>>(a);
+    pdl_launch(spmm_csr_kernel<VEC, NV, true>, dim3(grid), dim3(kSpmmThreads), 0, c->stream, a);
   else
-    spmm_csr_kernel<VEC, NV, false><<<grid, kSpmmThreads, 0, c->stream>>>(a);
+    pdl_launch(spmm_csr_kernel<VEC, NV, false>, dim3(grid), dim3(kSpmmThreads), 0, c->stream, a);
 }
 
 template <int VEC>
