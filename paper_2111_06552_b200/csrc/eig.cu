@@ -54,8 +54,8 @@ static size_t tri_smem(int m) {
 
 // 1. Householder tridiagonalisation (dsytd2, UPLO = 'L') in one CTA, the packed
 // lower triangle in shared memory.  Step j:
-//   B  (warp 0) column j gets the deferred rank-2 update of step j-1, then the
-//      reflector v_j, tau_j (dlarfg; rsqrt / reciprocal instead of divisions);
+//   B  (warps 0-7, a thread per row) column j gets the deferred rank-2 update of
+//      step j-1, then the reflector v_j, tau_j (dlarfg; rsqrt / reciprocals);
 //   C1 row i (4 warps: columns split mod 4, lane = row so one access reads 32
 //      consecutive rows of a column) applies step j-1's deferred update to its
 //      lower-part elements L(i, c), s0 <= c <= i, stores them and accumulates
@@ -63,7 +63,8 @@ static size_t tri_smem(int m) {
 //   C2 after a barrier the same threads add the upper part sum_{c > i} L(c, i) v_c
 //      (column i of the packed storage, already updated), so p = A22 v needs no
 //      scatter: each row's sum is its 4 quarter partials, added in fixed order;
-//   D  (warp 0) w = tau p - (tau^2 / 2)(p'v) v, which becomes the deferred update.
+//   D  (warps 0-7) w = tau p - (tau^2 / 2)(p'v) v, the next deferred update; D of
+//      step j and B of step j+1 run back to back between named barriers.
 // Every element is read and written once per step; all sums have a fixed order.
 // Outputs: d[m], e[m-1], tau[m-1] and the reflectors in Vr (column-major m x m,
 // column j holds v_j in rows j+1..m-1, v_j[j+1] = 1).
@@ -90,50 +91,73 @@ __global__ void __launch_bounds__(kTriThreads)
   for (int i = tid; i < m; i += kTriThreads) P[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const int row = 32 * (warp & 7) + lane, q = warp >> 3;  // C1: row, column residue mod 4
+  double* redb = slot + 8;   // [8] warp partials of B's norm
+  double* redd = slot + 16;  // [8] warp partials of D's p'v
+  // B. column j: deferred update with (v_{j-1}, w_{j-1}), then the reflector (dlarfg;
+  // rsqrt / reciprocals instead of divisions).  Warps 0-7, thread t owns row j + t;
+  // the norm is a fixed-order sum of 8 warp partials (named barrier 1).
+  auto phase_B = [&](int j) {
+    const int oj = tri_off(m, j);
+    const double2 pj = P[j];
+    const int i = j + tid;
+    double x = 0.0;
+    if (i < m) {
+      const double2 pi = P[i];
+      x = L[oj + tid] - fma(pi.x, pj.y, pi.y * pj.x);
+      L[oj + tid] = x;
+    }
+    double sq = (tid >= 2 && i < m) ? x * x : 0.0;
+    sq = warp_sum(sq);
+    if (lane == 0) redb[warp] = sq;
+    if (tid == 0) slot[2] = x;  // d_j
+    if (tid == 1) slot[3] = x;  // alpha
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    double s = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) s += redb[w2];
+    const double alpha = slot[3], djj = slot[2];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (s > 0.0) {
+      const double nrm2 = fma(alpha, alpha, s);
+      const double rn = rsqrt(nrm2);  // beta = -sign(alpha) ||x||
+      beta = alpha >= 0.0 ? -nrm2 * rn : nrm2 * rn;
+      t = (beta - alpha) * __drcp_rn(beta);
+      scal = __drcp_rn(alpha - beta);
+    }
+    if (i < m) {
+      const double vi = i == j ? 0.0 : (i == j + 1 ? 1.0 : x * scal);
+      Q[i].x = t != 0.0 ? vi : 0.0;
+      if (i > j) Vr[(long long)j * m + i] = vi;
+    }
+    if (tid == 0) {
+      d[j] = djj;
+      e[j] = beta;
+      tau[j] = t;
+      slot[0] = t;
+    }
+  };
+  // D. p = t * (sum of the 4 row partials, fixed order), w = p - (t/2)(p'v) v; warps 0-7
+  auto phase_D = [&](int s0, double t) {
+    const int i = s0 + tid;
+    double pl = 0.0, dv = 0.0;
+    if (i < m) {
+      pl = t * (((part[i] + part[m + i]) + part[2 * m + i]) + part[3 * m + i]);
+      dv = pl * Q[i].x;
+    }
+    dv = warp_sum(dv);
+    if (lane == 0) redd[warp] = dv;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    double ds = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) ds += redd[w2];
+    const double a2 = -0.5 * t * ds;
+    if (i < m) Q[i].y = fma(a2, Q[i].x, pl);
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // w_{s0} is read by every B thread
+  };
+  if (warp < 8) phase_B(0);
+  __syncthreads();
   for (int j = 0; j + 2 < m; ++j) {
     const int s0 = j + 1;
-    // B. column j: deferred update, reflector (warp 0)
-    if (warp == 0) {
-      const int oj = tri_off(m, j);
-      const double2 pj = P[j];
-      const double vpj = pj.x, wpj = pj.y;
-      double s = 0.0, alpha = 0.0, djj = 0.0;
-#pragma unroll 8
-      for (int i = j + lane; i < m; i += 32) {
-        const double2 pi = P[i];
-        const double x = L[oj + (i - j)] - fma(pi.x, wpj, pi.y * vpj);
-        L[oj + (i - j)] = x;
-        if (i == j) djj = x;
-        else if (i == j + 1) alpha = x;
-        else s = fma(x, x, s);
-      }
-      s = warp_sum(s);
-      alpha = __shfl_sync(0xffffffffu, alpha, 1);
-      djj = __shfl_sync(0xffffffffu, djj, 0);
-      double t = 0.0, beta = alpha, scal = 0.0;
-      if (s > 0.0) {
-        const double nrm2 = fma(alpha, alpha, s);
-        const double rn = rsqrt(nrm2);  // beta = -sign(alpha) ||x||
-        beta = alpha >= 0.0 ? -nrm2 * rn : nrm2 * rn;
-        t = (beta - alpha) * __drcp_rn(beta);
-        scal = __drcp_rn(alpha - beta);
-      }
-      const bool live = t != 0.0;
-#pragma unroll 8
-      for (int i = lane; i < m; i += 32) {
-        const double vi =
-            i <= j ? 0.0 : (i == j + 1 ? 1.0 : L[oj + (i - j)] * scal);
-        Q[i].x = live ? vi : 0.0;
-        if (i > j) Vr[(long long)j * m + i] = vi;
-      }
-      if (lane == 0) {
-        d[j] = djj;
-        e[j] = beta;
-        tau[j] = t;
-        slot[0] = t;
-      }
-    }
-    __syncthreads();
     const double t = slot[0];
     // C1. lower-part elements L(row, c), s0 <= c <= row: warp w takes row block
     // (w & 7) (lane = row: 32 consecutive rows of one column per access, conflict-
@@ -191,34 +215,12 @@ __global__ void __launch_bounds__(kTriThreads)
     }
     if (row < m) part[q * m + row] = acc;
     __syncthreads();
-    // D. (warp 0) p = t * (sum of the 4 row partials, fixed order), w = p - (t/2)(p'v) v.
-    // No barrier after it: warp 0 goes straight on to the next step's B, the other
-    // warps wait at B's barrier.
-    if (warp == 0) {
-      constexpr int kPer = (kEigMaxM + 31) / 32;
-      double pl[kPer];
-      double s = 0.0;
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int i = s0 + lane + 32 * u;
-        pl[u] = 0.0;
-        if (i < m) {
-          pl[u] = t * (((part[i] + part[m + i]) + part[2 * m + i]) + part[3 * m + i]);
-          s = fma(pl[u], Q[i].x, s);
-        }
-      }
-      const double a2 = -0.5 * t * warp_sum(s);
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int i = s0 + lane + 32 * u;
-        if (i < m) Q[i].y = fma(a2, Q[i].x, pl[u]);
-      }
-      for (int i = lane; i < s0; i += 32) Q[i].y = 0.0;
-      __syncwarp();
-    }
+    if (warp < 8) phase_D(s0, t);
     double2* tq = P;  // the current (v, w) become the deferred update of the next step
     P = Q;
     Q = tq;
+    if (warp < 8 && j + 3 < m) phase_B(j + 1);
+    __syncthreads();
   }
   // deferred update of the last 2 x 2 block, then its entries
   if (tid == 0) {
