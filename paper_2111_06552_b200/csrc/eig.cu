@@ -49,7 +49,7 @@ __host__ __device__ inline int tri_off(int m, int j) { return j * m - (j * (j - 
 
 static size_t tri_smem(int m) {
   // packed lower triangle | (v, w) previous step | (v, w) current | p | slots
-  return sizeof(double) * ((size_t)m * (m + 1) / 2 + 1 + 8 * (size_t)m + 64);
+  return sizeof(double) * ((size_t)m * (m + 1) / 2 + 1 + 9 * (size_t)m + 64);
 }
 
 // 1. Householder tridiagonalisation (dsytd2, UPLO = 'L') in one CTA, the packed
@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(kTriThreads)
   double2* P = reinterpret_cast<double2*>(L + (((size_t)m * (m + 1) / 2 + 1) & ~(size_t)1));
   double2* Q = P + m;
   double* part = reinterpret_cast<double*>(Q + m);  // [4][m] row partial sums of p
-  double* slot = part + 4 * m;                    // scalars
+  double* vcur = part + 4 * m;                    // this step's v as plain doubles (C2's
+                                                  // per-lane reads: 8-byte stride)
+  double* slot = vcur + m;                        // scalars
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // load: coalesced row-major reads, scattered shared-memory writes
   for (int idx = tid; idx < m * m; idx += kTriThreads) {
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(kTriThreads)
     if (i < m) {
       const double vi = i == j ? 0.0 : (i == j + 1 ? 1.0 : x * scal);
       Q[i].x = t != 0.0 ? vi : 0.0;
+      vcur[i] = t != 0.0 ? vi : 0.0;
       if (i > j) Vr[(long long)j * m + i] = vi;
     }
     if (tid == 0) {
@@ -206,12 +209,12 @@ __global__ void __launch_bounds__(kTriThreads)
       int c = row + 1 + q;
       for (; c + 12 < m; c += 16) {
         const double y0 = colr[c], y1 = colr[c + 4], y2 = colr[c + 8], y3 = colr[c + 12];
-        acc = fma(y0, Q[c].x, acc);
-        acc = fma(y1, Q[c + 4].x, acc);
-        acc = fma(y2, Q[c + 8].x, acc);
-        acc = fma(y3, Q[c + 12].x, acc);
+        acc = fma(y0, vcur[c], acc);
+        acc = fma(y1, vcur[c + 4], acc);
+        acc = fma(y2, vcur[c + 8], acc);
+        acc = fma(y3, vcur[c + 12], acc);
       }
-      for (; c < m; c += 4) acc = fma(colr[c], Q[c].x, acc);
+      for (; c < m; c += 4) acc = fma(colr[c], vcur[c], acc);
     }
     if (row < m) part[q * m + row] = acc;
     __syncthreads();
