@@ -102,6 +102,24 @@ int gcg_spmm_csr(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr, const
 
 /* G[r*g_rs + c*g_cs] = alpha * sum_i X[i,r] Y[i,c] + beta * G[...]  (beta == 0: no read)
  * optional fused column dots: dots[c] = sum_i T[i,c] Y[i,c] (T may equal Y). */
+/* SELL-C-sigma form of a CSR matrix (C = 32; sigma 1 keeps the row order, any other
+ * value sorts rows by length inside windows of 1024 rows).  gcg_sell_size returns the
+ * slice count and the padded entry count (synchronises); gcg_csr_to_sell fills the
+ * caller's arrays: slice_ptr (nslices + 1), perm (n: sorted position -> row),
+ * sell_col / sell_val (nnz_padded; sell_val may be NULL for a pattern-only copy).
+ * gcg_spmm_sell has gcg_spmm_csr's epilogue and dot modes and gives the same
+ * results.  SURVEY §8(b) MatDotMultiVec -> gcg_spmm_sell; operators.py:103-111. */
+int gcg_sell_size(void* ctx, int64_t n, const int32_t* rowptr, int32_t sigma, int64_t* nslices,
+                  int64_t* nnz_padded);
+int gcg_csr_to_sell(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                    const double* val, int32_t sigma, int64_t* slice_ptr, int32_t* perm,
+                    int32_t* sell_col, double* sell_val);
+int gcg_spmm_sell(void* ctx, int64_t n, int64_t nslices, const int64_t* slice_ptr,
+                  const int32_t* perm, const int32_t* sell_col, const double* sell_val, int64_t k,
+                  const double* X, int64_t ldx, double alpha, double gamma, const double* Z,
+                  int64_t ldz, double beta, const double* Yin, int64_t ldyin, double* Y,
+                  int64_t ldy, int dot_mode, const double* W, int64_t ldw, double* dots);
+
 int gcg_gram(void* ctx, int64_t n, int64_t k1, int64_t k2, const double* X, int64_t ldx,
              const double* Y, int64_t ldy, double alpha, double beta, double* G, int64_t g_rs,
              int64_t g_cs, const double* T, int64_t ldt, double* dots);

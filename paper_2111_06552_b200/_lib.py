@@ -35,6 +35,10 @@ _SIGS = {
                      _dbl, _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
     "gcg_build_p": [_ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _i64, _dbl, _ptr, _i64,
                     C.POINTER(_i64)],
+    "gcg_sell_size": [_ptr, _i64, _ptr, _i32, C.POINTER(_i64), C.POINTER(_i64)],
+    "gcg_csr_to_sell": [_ptr, _i64, _ptr, _ptr, _ptr, _i32, _ptr, _ptr, _ptr, _ptr],
+    "gcg_spmm_sell": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr,
+                      _i64, _dbl, _ptr, _i64, _ptr, _i64, _int, _ptr, _i64, _ptr],
     "gcg_gram": [_ptr, _i64, _i64, _i64, _ptr, _i64, _ptr, _i64, _dbl, _dbl, _ptr, _i64, _i64, _ptr,
                  _i64, _ptr],
     "gcg_lincomb": [_ptr, _i64, _i64, _i64, _dbl, _ptr, _i64, _ptr, _i64, _dbl, _ptr, _i64],

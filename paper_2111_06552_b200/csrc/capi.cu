@@ -18,6 +18,15 @@ namespace gcg {
 
 extern int64_t g_launches;
 
+int sell_size(Ctx* c, long long n, const int* rowptr, int sigma, long long* nslices,
+              long long* nnz_padded);
+int csr_to_sell(Ctx* c, long long n, const int* rowptr, const int* colidx, const double* val,
+                int sigma, long long* sptr, int* perm, int* scol, double* sval);
+int spmm_sell_launch(Ctx* c, long long n, long long nslices, const long long* sptr,
+                     const int* perm, const int* scol, const double* sval, int k,
+                     const double* X, long long ldx, double alpha, double gamma, const double* Z,
+                     long long ldz, double beta, const double* Yin, long long ldyin, double* Y,
+                     long long ldy, int dot_mode, const double* W, long long ldw, double* dots);
 int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                      const double* val, int k, const double* X, long long ldx, double alpha,
                      double gamma, const double* Z, long long ldz, double beta, const double* Yin,
@@ -353,6 +362,43 @@ int gcg_spmm_csr(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const i
     return GCG_ERR_ARG;
   return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, (int)k, X, ldx, alpha, gamma, Z, ldz, beta,
                           Yin, ldyin, Y, ldy, dot_mode, W, ldw, dots, nullptr, nullptr, nullptr);
+}
+
+int gcg_sell_size(void* p, int64_t n, const int32_t* rowptr, int32_t sigma, int64_t* nslices,
+                  int64_t* nnz_padded) {
+  Ctx* c = CTX(p);
+  if (!c || n <= 0 || !rowptr || !nslices || !nnz_padded) return GCG_ERR_ARG;
+  long long ns = 0, nz = 0;
+  const int st = sell_size(c, n, rowptr, sigma, &ns, &nz);
+  *nslices = ns;
+  *nnz_padded = nz;
+  return st;
+}
+
+int gcg_csr_to_sell(void* p, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                    const double* val, int32_t sigma, int64_t* slice_ptr, int32_t* perm,
+                    int32_t* sell_col, double* sell_val) {
+  Ctx* c = CTX(p);
+  if (!c) return GCG_ERR_ARG;
+  return csr_to_sell(c, n, rowptr, colidx, val, sigma, (long long*)slice_ptr, perm, sell_col,
+                     sell_val);
+}
+
+int gcg_spmm_sell(void* p, int64_t n, int64_t nslices, const int64_t* slice_ptr,
+                  const int32_t* perm, const int32_t* sell_col, const double* sell_val, int64_t k,
+                  const double* X, int64_t ldx, double alpha, double gamma, const double* Z,
+                  int64_t ldz, double beta, const double* Yin, int64_t ldyin, double* Y,
+                  int64_t ldy, int dot_mode, const double* W, int64_t ldw, double* dots) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || nslices < 0 || (n > 0 && (!slice_ptr || !perm || !sell_col ||
+                                                        !sell_val || !X || !Y)))
+    return GCG_ERR_ARG;
+  if (ldx < k || ldy < k || (gamma != 0.0 && !Z) || (beta != 0.0 && !Yin)) return GCG_ERR_ARG;
+  if (dot_mode < 0 || dot_mode > 2 || (dot_mode && !dots) || (dot_mode == 1 && !W))
+    return GCG_ERR_ARG;
+  return spmm_sell_launch(c, n, nslices, (const long long*)slice_ptr, perm, sell_col, sell_val,
+                          (int)k, X, ldx, alpha, gamma, Z, ldz, beta, Yin, ldyin, Y, ldy,
+                          dot_mode, W, ldw, dots);
 }
 
 int gcg_gram(void* p, int64_t n, int64_t k1, int64_t k2, const double* X, int64_t ldx,

@@ -31,7 +31,11 @@
 // Roofline: HBM.  Algorithmic bytes per launch = 12*nnz + 4*(n+1) + 16*n*k
 // (+8*n*k per extra epilogue stream); flops = 2*nnz*k.
 
+#include <limits.h>
 #include <stdlib.h>
+
+#include <cub/block/block_radix_sort.cuh>
+#include <vector>
 
 #include "common.cuh"
 
@@ -578,6 +582,418 @@ int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, con
                       const int* skip) {
   return spmm_launch_impl(c, n, nnz, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta,
                           Yin, ldyin, Y, ldy, dot_mode, W, ldw, nullptr, partials, grid_out, skip);
+}
+
+
+// ---------------------------------------------------------------------------
+// SELL-C-sigma SpMM (MatDotMultiVec on the sliced-ELLPACK format).
+//
+// Rows are sorted by length (descending, stable) inside windows of sigma rows and
+// grouped into slices of kSellC = 32 consecutive sorted rows; slice s stores its
+// width w_s = longest row, entry e of row t at slice_ptr[s] + e * 32 + t
+// (column-major inside the slice: one slice's e-th entries are contiguous, so the
+// index / value stream is read in coalesced 128-byte runs), padded with zero values
+// whose column repeats the row's last column (the padding gather hits L1).  The
+// SpMM kernel walks slices per warp with the CSR kernel's lane groups (LPR lanes,
+// 32-byte gathers) and scatters each row to its original position through perm.
+// Per row, the real entries are summed in CSR order with the same fma chain as the
+// CSR kernel; padding adds exact zeros — results equal the CSR kernel's.
+// Built on the device (gcg_sell_size / gcg_csr_to_sell: block radix sort per
+// window, device exclusive scan of the slice sizes).
+
+constexpr int kSellC = 32;
+constexpr int kSellSigma = 1024;  // rows per sorting window (256 threads x 4 keys)
+
+__global__ void __launch_bounds__(256) sell_sort_kernel(long long n, const int* __restrict__ rowptr,
+                                                        int sorted, int* perm, long long* swidth) {
+  using Sort = cub::BlockRadixSort<int, 256, 4, int>;
+  __shared__ typename Sort::TempStorage tmp;
+  const long long w0 = (long long)blockIdx.x * kSellSigma;
+  int keys[4], vals[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = threadIdx.x * 4 + i;  // blocked: row order = input order (stable sort)
+    const long long r = w0 + idx;
+    if (r < n) {
+      keys[i] = -(rowptr[r + 1] - rowptr[r]);
+      vals[i] = (int)r;
+    } else {
+      keys[i] = INT_MAX;
+      vals[i] = -1;
+    }
+  }
+  if (sorted) Sort(tmp).Sort(keys, vals);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = threadIdx.x * 4 + i;
+    const long long r = w0 + idx;
+    if (r < n) {
+      perm[r] = vals[i];
+      if (idx % kSellC == 0) swidth[r / kSellC] = (long long)(-keys[i]) * kSellC;
+    }
+  }
+}
+
+// unsorted windows: the slice width is the max over its 32 rows
+__global__ void sell_width_fix_kernel(long long n, const int* __restrict__ rowptr,
+                                      const int* __restrict__ perm, long long nslices,
+                                      long long* swidth) {
+  const long long s = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const long long r = s * kSellC + (threadIdx.x & 31);
+  int len = 0;
+  if (r < n) {
+    const int o = perm[r];
+    len = rowptr[o + 1] - rowptr[o];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
+  if ((threadIdx.x & 31) == 0) swidth[s] = (long long)len * kSellC;
+}
+
+__global__ void sell_fill_kernel(long long n, const int* __restrict__ rowptr,
+                                 const int* __restrict__ colidx, const double* __restrict__ val,
+                                 const int* __restrict__ perm, const long long* __restrict__ sptr,
+                                 long long nslices, int* scol, double* sval) {
+  const long long s = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int t = threadIdx.x & 31;
+  const long long base = sptr[s];
+  const int w = (int)((sptr[s + 1] - base) / kSellC);
+  const long long r = s * kSellC + t;
+  int st = 0, len = 0, lastc = 0;
+  if (r < n) {
+    const int o = perm[r];
+    st = rowptr[o];
+    len = rowptr[o + 1] - st;
+    lastc = len > 0 ? colidx[st + len - 1] : o;
+  }
+  for (int e = 0; e < w; ++e) {
+    const bool real = e < len;
+    scol[base + (long long)e * kSellC + t] = real ? colidx[st + e] : lastc;
+    if (val) sval[base + (long long)e * kSellC + t] = real ? val[st + e] : 0.0;
+  }
+}
+
+struct SellArgs {
+  long long n, nslices;
+  const long long* sptr;
+  const int* perm;
+  const int* scol;
+  const double* sval;
+  int k;
+  const double* X;
+  long long ldx;
+  double alpha, gamma, beta;
+  const double* Z;
+  long long ldz;
+  const double* Yin;
+  long long ldyin;
+  double* Y;
+  long long ldy;
+  int dot_mode;
+  int lpr, gpw, vepi;
+  const double* W;
+  long long ldw;
+  double* partials;
+  int pld;
+};
+
+template <int VEC, int NV>
+__global__ void __launch_bounds__(kSpmmThreads) spmm_sell_kernel(SellArgs a) {
+  constexpr int NW = kSpmmThreads / 32;
+  constexpr int U = 4;
+  const int LPR = a.lpr, G = a.gpw;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g0 = lane / LPR;
+  const bool active = g0 < G;
+  const int g = active ? g0 : G - 1;
+  const int sub = lane - g0 * LPR;
+  const int k = a.k;
+  __shared__ double sacc[NW][kSpmmMaxSlots][32];
+  __shared__ double sdot[NW][kSpmmMaxPass];
+  if (a.dot_mode) {
+#pragma unroll
+    for (int q = 0; q < NV * VEC; ++q) sacc[warp][q][lane] = 0.0;
+  }
+  for (long long s = (long long)blockIdx.x * NW + warp; s < a.nslices;
+       s += (long long)gridDim.x * NW) {
+    const long long base = a.sptr[s];
+    const int w = (int)((a.sptr[s + 1] - base) / kSellC);
+    for (int t0 = 0; t0 < kSellC; t0 += G) {
+      const int t = t0 + g;
+      const long long pos = s * kSellC + t;
+      const bool ok_row = t < kSellC && pos < a.n;
+      double acc[NV][VEC];
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
+      if (ok_row) {
+        const int* cp = a.scol + base + t;
+        const double* vp = a.sval + base + t;
+        int e0 = 0;
+        for (; e0 + U <= w; e0 += U) {
+          int j[U];
+          double v[U], xv[U][NV][VEC];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            j[u] = __ldg(cp + (long long)(e0 + u) * kSellC);
+            v[u] = __ldg(vp + (long long)(e0 + u) * kSellC);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const double* xr = a.X + (long long)j[u] * a.ldx;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              const int c = (q * LPR + sub) * VEC;
+              if (c < k) VecT<VEC>::load(xr + c, xv[u][q]);
+              else
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) xv[u][q][e] = 0.0;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
+        }
+        for (; e0 < w; ++e0) {
+          const int j = __ldg(cp + (long long)e0 * kSellC);
+          const double v = __ldg(vp + (long long)e0 * kSellC);
+          const double* xr = a.X + (long long)j * a.ldx;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            const int c = (q * LPR + sub) * VEC;
+            if (c < k) {
+              double xv[VEC];
+              VecT<VEC>::load(xr + c, xv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v, xv[e], acc[q][e]);
+            }
+          }
+        }
+      }
+      if (!(active && ok_row)) continue;
+      const long long r = a.perm[pos];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int c = (q * LPR + sub) * VEC;
+        if (c >= k) continue;
+        double y[VEC], tv[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = a.alpha * acc[q][e];
+        if (a.gamma != 0.0) {
+          if (a.vepi) VecT<VEC>::ld(a.Z + r * a.ldz + c, tv);
+          else
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) tv[e] = a.Z[r * a.ldz + c + e];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(a.gamma, tv[e], y[e]);
+        }
+        if (a.beta != 0.0) {
+          if (a.vepi) VecT<VEC>::ld(a.Yin + r * a.ldyin + c, tv);
+          else
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) tv[e] = a.Yin[r * a.ldyin + c + e];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(a.beta, tv[e], y[e]);
+        }
+        if (a.vepi) VecT<VEC>::st(a.Y + r * a.ldy + c, y);
+        else
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) a.Y[r * a.ldy + c + e] = y[e];
+        if (a.dot_mode == 1) {
+          if (a.vepi) VecT<VEC>::ld(a.W + r * a.ldw + c, tv);
+          else
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) tv[e] = a.W[r * a.ldw + c + e];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sacc[warp][q * VEC + e][lane] = fma(y[e], tv[e], sacc[warp][q * VEC + e][lane]);
+        } else if (a.dot_mode == 2) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sacc[warp][q * VEC + e][lane] = fma(y[e], y[e], sacc[warp][q * VEC + e][lane]);
+        }
+      }
+    }
+  }
+  if (a.dot_mode == 0) return;
+  __syncwarp();
+  if (g0 == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int c = (q * LPR + sub) * VEC + e;
+        double v = 0.0;
+        for (int gg = 0; gg < G; ++gg) v += sacc[warp][q * VEC + e][gg * LPR + sub];
+        if (c < k) sdot[warp][c] = v;
+      }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += kSpmmThreads) {
+    double s = 0.0;
+    for (int ww = 0; ww < NW; ++ww) s += sdot[ww][c];
+    a.partials[(long long)blockIdx.x * a.pld + c] = s;
+  }
+}
+
+template <int VEC, int NV>
+static void sell_launch_one(Ctx* c, const SellArgs& a, int grid) {
+  spmm_sell_kernel<VEC, NV><<<grid, kSpmmThreads, 0, c->stream>>>(a);
+}
+
+// slices and padded entry count of the SELL-C-sigma form (sigma: 1 = keep the row
+// order, else rows sorted by length inside windows of 1024); synchronises once.
+int sell_size(Ctx* c, long long n, const int* rowptr, int sigma, long long* nslices,
+              long long* nnz_padded) {
+  if (n <= 0 || !rowptr) return GCG_ERR_ARG;
+  const long long ns = (n + kSellC - 1) / kSellC;
+  const long long nwin = (n + kSellSigma - 1) / kSellSigma;
+  GCG_TRY(ensure(c->host_tmp3, sizeof(long long) * (size_t)(ns + 1) + sizeof(int) * (size_t)n + 256));
+  long long* sw = (long long*)c->host_tmp3.ptr;
+  int* perm = (int*)(sw + ns + 1);
+  sell_sort_kernel<<<(unsigned)nwin, 256, 0, c->stream>>>(n, rowptr, sigma > 1, perm, sw);
+  if (sigma <= 1)
+    sell_width_fix_kernel<<<(unsigned)((ns + 7) / 8), 256, 0, c->stream>>>(n, rowptr, perm, ns, sw);
+  g_launches += sigma <= 1 ? 2 : 1;
+  GCG_CHECK_LAUNCH();
+  // total = sum of slice sizes (host reduction of ns values is fine at setup time)
+  std::vector<long long> h((size_t)ns);
+  GCG_TRY(cuda_status(cudaMemcpyAsync(h.data(), sw, sizeof(long long) * ns, cudaMemcpyDeviceToHost,
+                                      c->stream)));
+  GCG_TRY(cuda_status(cudaStreamSynchronize(c->stream)));
+  long long tot = 0;
+  for (long long v : h) tot += v;
+  *nslices = ns;
+  *nnz_padded = tot;
+  return GCG_OK;
+}
+
+int csr_to_sell(Ctx* c, long long n, const int* rowptr, const int* colidx, const double* val,
+                int sigma, long long* sptr, int* perm, int* scol, double* sval) {
+  if (n <= 0 || !rowptr || !colidx || !sptr || !perm || !scol) return GCG_ERR_ARG;
+  const long long ns = (n + kSellC - 1) / kSellC;
+  const long long nwin = (n + kSellSigma - 1) / kSellSigma;
+  GCG_TRY(ensure(c->host_tmp3, sizeof(long long) * (size_t)(ns + 1) + 256));
+  long long* sw = (long long*)c->host_tmp3.ptr;
+  sell_sort_kernel<<<(unsigned)nwin, 256, 0, c->stream>>>(n, rowptr, sigma > 1, perm, sw);
+  if (sigma <= 1)
+    sell_width_fix_kernel<<<(unsigned)((ns + 7) / 8), 256, 0, c->stream>>>(n, rowptr, perm, ns, sw);
+  // slice_ptr = exclusive scan of the slice sizes (host: setup-time, ns values)
+  std::vector<long long> h((size_t)ns + 1);
+  GCG_TRY(cuda_status(cudaMemcpyAsync(h.data(), sw, sizeof(long long) * ns, cudaMemcpyDeviceToHost,
+                                      c->stream)));
+  GCG_TRY(cuda_status(cudaStreamSynchronize(c->stream)));
+  long long acc = 0;
+  for (long long s = 0; s < ns; ++s) {
+    const long long v = h[(size_t)s];
+    h[(size_t)s] = acc;
+    acc += v;
+  }
+  h[(size_t)ns] = acc;
+  GCG_TRY(cuda_status(cudaMemcpyAsync(sptr, h.data(), sizeof(long long) * (ns + 1),
+                                      cudaMemcpyHostToDevice, c->stream)));
+  sell_fill_kernel<<<(unsigned)((ns + 7) / 8), 256, 0, c->stream>>>(n, rowptr, colidx, val, perm,
+                                                                    sptr, ns, scol, sval);
+  g_launches += sigma <= 1 ? 3 : 2;
+  GCG_CHECK_LAUNCH();
+  // the host vector is read by the async copy: finish it before returning
+  return cuda_status(cudaStreamSynchronize(c->stream));
+}
+
+int spmm_sell_launch(Ctx* c, long long n, long long nslices, const long long* sptr,
+                     const int* perm, const int* scol, const double* sval, int k,
+                     const double* X, long long ldx, double alpha, double gamma, const double* Z,
+                     long long ldz, double beta, const double* Yin, long long ldyin, double* Y,
+                     long long ldy, int dot_mode, const double* W, long long ldw, double* dots) {
+  if (n <= 0 || k <= 0) return GCG_OK;
+  double* partials = nullptr;
+  const int grid = grid_for(nslices, 8, 4, c->num_sms);
+  if (dot_mode) {
+    GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * kSpmmMaxPass));
+    partials = (double*)c->partials.ptr;
+  }
+  int c0 = 0;
+  while (c0 < k) {
+    const int rest = k - c0;
+    int vec = 1;
+    if (ldx % 4 == 0 && aligned_to(X + c0, 32) && rest >= 4) vec = 4;
+    else if (ldx % 2 == 0 && aligned_to(X + c0, 16) && rest >= 2) vec = 2;
+    auto max_cols = [](int v) { return 32 * v * (kSpmmMaxSlots / v < 4 ? kSpmmMaxSlots / v : 4); };
+    const int npass = (rest + max_cols(vec) - 1) / max_cols(vec);
+    int kc = (rest + npass - 1) / npass;
+    kc = (kc + vec - 1) / vec * vec;
+    if (kc > rest) kc = rest;
+    if (kc % vec) {
+      if (kc > vec) kc -= kc % vec;
+      else vec = 1;
+    }
+    int nv = 1, lpr = 1;
+    spmm_shape((kc + vec - 1) / vec, vec, &nv, &lpr);
+    SellArgs a;
+    a.n = n;
+    a.nslices = nslices;
+    a.sptr = sptr;
+    a.perm = perm;
+    a.scol = scol;
+    a.sval = sval;
+    a.k = kc;
+    a.X = X + c0;
+    a.ldx = ldx;
+    a.alpha = alpha;
+    a.gamma = gamma;
+    a.Z = Z ? Z + c0 : nullptr;
+    a.ldz = ldz;
+    a.beta = beta;
+    a.Yin = Yin ? Yin + c0 : nullptr;
+    a.ldyin = ldyin;
+    a.Y = Y + c0;
+    a.ldy = ldy;
+    a.dot_mode = dot_mode;
+    a.W = W ? W + c0 : nullptr;
+    a.ldw = ldw;
+    a.lpr = lpr;
+    a.gpw = 32 / lpr;
+    a.partials = partials;
+    a.pld = kc;
+    const int vb = 8 * vec;
+    a.vepi = aligned_to(a.Y, vb) && ldy % vec == 0 &&
+             (gamma == 0.0 || (aligned_to(a.Z, vb) && ldz % vec == 0)) &&
+             (beta == 0.0 || (aligned_to(a.Yin, vb) && ldyin % vec == 0)) &&
+             (dot_mode != 1 || (aligned_to(a.W, vb) && ldw % vec == 0));
+    if (vec == 4) {
+      if (nv == 1) sell_launch_one<4, 1>(c, a, grid);
+      else sell_launch_one<4, 2>(c, a, grid);
+    } else if (vec == 2) {
+      switch (nv) {
+        case 1: sell_launch_one<2, 1>(c, a, grid); break;
+        case 2: sell_launch_one<2, 2>(c, a, grid); break;
+        case 3: sell_launch_one<2, 3>(c, a, grid); break;
+        default: sell_launch_one<2, 4>(c, a, grid); break;
+      }
+    } else {
+      switch (nv) {
+        case 1: sell_launch_one<1, 1>(c, a, grid); break;
+        case 2: sell_launch_one<1, 2>(c, a, grid); break;
+        case 3: sell_launch_one<1, 3>(c, a, grid); break;
+        default: sell_launch_one<1, 4>(c, a, grid); break;
+      }
+    }
+    ++g_launches;
+    GCG_CHECK_LAUNCH();
+    if (dot_mode) {
+      GCG_TRY(reduce_partials(c, partials, grid, kc, dots + c0, 1, 0));
+      ++g_launches;
+    }
+    c0 += kc;
+  }
+  return GCG_OK;
 }
 
 }  // namespace gcg

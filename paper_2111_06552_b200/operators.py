@@ -16,10 +16,11 @@ from __future__ import annotations
 import numpy as np
 import scipy.sparse
 
+from . import _lib
 from . import device as D
 from .errors import InvalidMatrix, InvalidShape
 
-__all__ = ["DeviceCsr", "DeviceProblem", "as_device_problem", "validate_symmetric"]
+__all__ = ["DeviceCsr", "DeviceSell", "DeviceProblem", "as_device_problem", "validate_symmetric"]
 
 _SYM_RTOL = 1e-12  # operators.py:26
 
@@ -70,6 +71,45 @@ class DeviceCsr:
     def bytes_per_apply(self, k):
         """Algorithmic HBM bytes of one SpMM with k columns."""
         return 12 * self.nnz + 4 * (self.n + 1) + 16 * self.n * k
+
+
+class DeviceSell:
+    """SELL-C-sigma copy of a DeviceCsr (C = 32, rows length-sorted in windows of 1024
+    unless sigma=1): built on the device (gcg_sell_size / gcg_csr_to_sell), applied by
+    gcg_spmm_sell with the CSR kernel's epilogues and the same results.  MatDotMultiVec
+    on the sliced-ELLPACK format of SURVEY §8(b); the solver's block CG keeps CSR."""
+
+    kind = "sell-sparse"
+
+    def __init__(self, csr, sigma=1024):
+        import ctypes as C
+        import torch
+
+        ctx = csr.ctx
+        self.ctx, self.n, self.dim, self.nnz = ctx, csr.n, csr.n, csr.nnz
+        ns, nz = C.c_int64(0), C.c_int64(0)
+        _lib.call("gcg_sell_size", ctx.h, csr.n, D._p(csr.rowptr), int(sigma), C.byref(ns),
+                  C.byref(nz))
+        self.nslices, self.nnz_padded = int(ns.value), int(nz.value)
+        self.slice_ptr = ctx.empty(self.nslices + 1, dtype=torch.int64)
+        self.perm = ctx.empty(csr.n, dtype=torch.int32)
+        self.col = ctx.empty(max(self.nnz_padded, 1), dtype=torch.int32)
+        self.val = ctx.empty(max(self.nnz_padded, 1))
+        _lib.call("gcg_csr_to_sell", ctx.h, csr.n, D._p(csr.rowptr), D._p(csr.colidx),
+                  D._p(csr.val), int(sigma), D._p(self.slice_ptr), D._p(self.perm),
+                  D._p(self.col), D._p(self.val))
+
+    def apply(self, x, out, alpha=1.0, gamma=0.0, Z=None, beta=0.0, Yin=None, dot_mode=0, W=None,
+              dots=None):
+        n, k = out.shape
+        if x.shape != out.shape or n != self.n:
+            raise InvalidShape(f"sell apply: X {tuple(x.shape)} / Y {tuple(out.shape)} vs dim {self.n}")
+        _lib.call("gcg_spmm_sell", self.ctx.h, n, self.nslices, D._p(self.slice_ptr),
+                  D._p(self.perm), D._p(self.col), D._p(self.val), k, D._p(x), D._ld(x),
+                  float(alpha), float(gamma), D._p(Z), D._ld(Z), float(beta), D._p(Yin),
+                  D._ld(Yin), D._p(out), D._ld(out), int(dot_mode), D._p(W), D._ld(W),
+                  D._p(dots))
+        return out
 
 
 class DeviceProblem:

@@ -61,6 +61,11 @@ def main(cfgs):
         dots = dev.empty(bs)
         t = timeit(lambda: D.spmm(dev, A, Xc, Yc, gamma=-0.1, Z=Xc, dot_mode=1, W=Xc, dots=dots))
         report(f"spmm k={bs} CG form (contig, dots)", t, 12 * nnz + 4 * (n + 1) + 16 * n * bs)
+        from paper_2111_06552_b200.operators import DeviceSell
+        Sl = DeviceSell(A)
+        t = timeit(lambda: Sl.apply(Xc, Yc, gamma=-0.1, Z=Xc, dot_mode=1, W=Xc, dots=dots))
+        report(f"spmm k={bs} CG form, SELL-32-1024 ({Sl.nnz_padded / nnz:.3f}x nnz)", t,
+               12 * nnz + 4 * (n + 1) + 16 * n * bs)
         for k1, k2 in [(m - bs, bs), (bs, bs), (16, 16), (m, m)]:
             G = dev.empty(k1, k2)
             Xg, Yg = V[:, :k1], V[:, m - k2:]

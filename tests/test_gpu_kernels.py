@@ -428,3 +428,61 @@ def test_launch_counter_moves(dev):
     y = dev.empty(10, 2)
     D.fill(dev, y, 1.0)
     assert _lib.launch_count() > before
+
+
+# -- SELL-C-sigma ---------------------------------------------------------------
+
+
+def _ragged(n, seed):
+    """Rows of very different lengths (0 .. 60 nonzeros), symmetric."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 30, n)
+    lens[::17] = 0
+    rows = np.repeat(np.arange(n), lens)
+    cols = rng.integers(0, n, rows.size)
+    m = scipy.sparse.csr_matrix((rng.standard_normal(rows.size), (rows, cols)), shape=(n, n))
+    m = (m + m.T).tocsr()
+    m.sum_duplicates()
+    return m
+
+
+SELL_CASES = [
+    ("lap3d13", lambda: P.laplacian_3d(13)),          # n = 2197: ragged last slice
+    ("27pt10", lambda: P.stencil27(10)),
+    ("fem5", lambda: P.fem_p1_cube(5)[1]),
+    ("ragged", lambda: _ragged(3000, 4)),
+]
+
+
+@pytest.mark.parametrize("name,mk", SELL_CASES)
+@pytest.mark.parametrize("sigma", [1, 1024])
+@pytest.mark.parametrize("k", [1, 7, 20, 40, 300])
+def test_spmm_sell_equals_csr(dev, name, mk, sigma, k):
+    """gcg_spmm_sell (rows length-sorted or not) == gcg_spmm_csr, incl. the fused
+    shift / axpby / dot epilogues, and == the oracle."""
+    from paper_2111_06552_b200.operators import DeviceSell
+
+    a = mk()
+    n = a.shape[0]
+    A = DeviceCsr.from_scipy(dev, a)
+    S = DeviceSell(A, sigma=sigma)
+    assert S.nnz_padded >= a.nnz
+    rng = np.random.default_rng(k + sigma)
+    x = rng.standard_normal((n, k))
+    yin = rng.standard_normal((n, k))
+    xd, yd = rm(dev, x), rm(dev, yin)
+    for kw in (dict(), dict(alpha=-1.0, gamma=0.3, Z=xd, beta=1.0, Yin=yd, dot_mode=2),
+               dict(gamma=-0.7, Z=xd, dot_mode=1, W=xd)):
+        y1, y2 = dev.empty(n, k), dev.empty(n, k)
+        d1, d2 = dev.empty(k), dev.empty(k)
+        extra = dict(dots=d1) if "dot_mode" in kw else {}
+        S.apply(xd, y1, **kw, **extra)
+        D.spmm(dev, A, xd, y2, **kw, **(dict(dots=d2) if "dot_mode" in kw else {}))
+        assert torch.equal(y1, y2), name
+        want = kw.get("alpha", 1.0) * (a @ x) + kw.get("gamma", 0.0) * x
+        if "Yin" in kw:
+            want = want + yin
+        assert rel_err(host(y1), want) <= 1e-13
+        if "dot_mode" in kw:
+            ref = (want * want).sum(0) if kw["dot_mode"] == 2 else (want * x).sum(0)
+            assert rel_err(host(d1), ref) <= 1e-12
