@@ -22,6 +22,8 @@ device tensors are staged through host memory.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -112,21 +114,39 @@ def local_part(a, b, bounds, rank):
 
 
 class Comm:
-    """Collectives over a torch.distributed process group."""
+    """Collectives over a torch.distributed process group.
 
-    def __init__(self, group=None):
+    reduce="allgather" (default): sums are all-gathered and added in rank order on
+    every rank — bit-identical on all ranks and independent of the collective
+    algorithm (the reference's deterministic mode, multivec.py:84-112).
+    reduce="allreduce": one NCCL allreduce (the paper's SUBMAT allreduce,
+    PAPER.md:1126-1163) — identical on all ranks for a given NCCL configuration,
+    fewer bytes at large rank counts.  GCG_DIST_REDUCE selects the default.
+    """
+
+    def __init__(self, group=None, reduce=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
         self.backend = dist.get_backend(group)
         self.staged = self.backend != "nccl"
+        self.reduce = reduce or os.environ.get("GCG_DIST_REDUCE", "allgather")
+        if self.reduce not in ("allgather", "allreduce"):
+            raise ValueError(f"unknown reduce mode {self.reduce!r}")
 
     def _host(self, t):
         return t.cpu() if (self.staged and t.is_cuda) else t
 
     def allgather_sum(self, dev, t):
-        """Sum of `t` over ranks, accumulated in rank order (identical bits everywhere)."""
+        """Sum of `t` over ranks, accumulated in rank order (identical bits everywhere);
+        one allreduce instead in reduce="allreduce" mode."""
         if self.size == 1:
+            return t
+        if self.reduce == "allreduce":
+            h = self._host(t.contiguous())
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            if h is not t:
+                t.copy_(h.to(t.device).view(t.shape))
             return t
         src = self._host(t.contiguous())
         parts = [torch.empty_like(src) for _ in range(self.size)]

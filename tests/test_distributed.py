@@ -99,7 +99,11 @@ def _worker(rank, world, port, q):
         s = t.tolist()
         bt = torch.tensor([float(rank + 7)], dtype=torch.float64)
         comm.broadcast(bt, src=1)
-        q.put((rank, got, s, bt.item()))
+        # allreduce mode (the paper's SUBMAT allreduce): same result on both ranks
+        ar = Comm(reduce="allreduce")
+        u = torch.tensor([0.5, 2.0, -3.0], dtype=torch.float64) * (rank + 1)
+        ar.allgather_sum(None, u)
+        q.put((rank, got, s, bt.item(), u.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -113,8 +117,8 @@ def test_comm_gloo_world2():
         p.start()
     res = dict()
     for _ in range(2):
-        r, got, s, b = q.get(timeout=120)
-        res[r] = (got, s, b)
+        r, got, s, b, u = q.get(timeout=120)
+        res[r] = (got, s, b, u)
     for p in procs:
         p.join(timeout=60)
     assert res[0][0] == [2.0, 4.0, 6.0, 8.0]
@@ -122,3 +126,4 @@ def test_comm_gloo_world2():
     assert res[0][1] == res[1][1]                     # bit-identical on both ranks
     assert res[0][1] == [1e16 + 1.0, 1.0 + 1e16, -1e16 + 1.0]
     assert res[0][2] == res[1][2] == 8.0
+    assert res[0][3] == res[1][3] == [1.5, 6.0, -9.0]
