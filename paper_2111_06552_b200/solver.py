@@ -30,6 +30,7 @@ import torch
 
 from . import device as D
 from .dense import sym_eig_full, sym_eig_range_split
+from .mvops import PrefaultedHost
 
 # GCG_PY_BUILD_P=1: the Python driver for the momentum block (A/B and debugging)
 _PY_BUILD_P = os.environ.get("GCG_PY_BUILD_P", "0") == "1"
@@ -389,6 +390,8 @@ def gcg_solve_ops(ops, cfg, x0=None):
 
     v = ops.vec(sx + 2 * bs, zero=True)
     lam = np.zeros(sx + 2 * bs)
+    # host eigenvector buffer, page-faulted in the background during the solve
+    host_out = None if cfg.return_device else PrefaultedHost(nloc, ne)
     if x0 is None:
         S.set_random(v[:, :sx], cfg.seed)
     else:
@@ -634,7 +637,8 @@ def gcg_solve_ops(ops, cfg, x0=None):
         residuals = S.residuals(vectors, vd)
 
     # one on-device layout transpose, then a single D2H of an F-order block
-    evecs = vectors if cfg.return_device else ops.host_rows(vectors)
+    evecs = vectors if cfg.return_device else \
+        ops.host_rows(vectors, host_out.take(vectors.shape) if host_out is not None else None)
 
     return SolverReport(
         status=status,
