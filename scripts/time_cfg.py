@@ -13,12 +13,19 @@ maxit = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 pr = P.baseline_problem(cfg)
 dev = D.default_context()
 prob = as_device_problem(dev, pr.a, pr.b, validate=False)
+# the seeded N(0,1) PCG64 block (parity with the reference's draw) is host work of
+# ~1.5 s at cfg3; draw it once outside the timed region, as bench.py does
+bs = pr.block_size or -(-pr.num_eigen // 5)
+sx = 3 * bs if pr.moving else min(pr.num_eigen + 3 * bs, pr.a.shape[0])
+t0 = time.perf_counter()
+x0 = torch.from_numpy(np.random.Generator(np.random.PCG64(0)).standard_normal((pr.a.shape[0], sx))).pin_memory()
+print(f"cfg{cfg}: host PCG64 draw of the {pr.a.shape[0]}x{sx} initial block {time.perf_counter() - t0:.3f}s")
 for rep_i in range(2):
     torch.cuda.synchronize()
     l0 = _lib.launch_count(); t0 = time.perf_counter()
     rep = gcg_solve(prob, None, SolverConfig(num_eigen=pr.num_eigen, block_size=pr.block_size, tol=pr.tol,
                     moving=pr.moving, seed=0, init="normal", residual="relative", max_gcg_iters=maxit,
-                    return_device=True))
+                    return_device=True), x0=x0)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
     print(f"cfg{cfg} run{rep_i}: {rep.status} iters={rep.iterations} time={dt:.3f}s launches={_lib.launch_count()-l0} "
           f"maxres={rep.residuals.max():.2e} lam0={rep.eigenvalues[0]:.12f}")
