@@ -154,6 +154,18 @@ int gcg_block_cg(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr, const
                  int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
                  int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres);
 
+/* gcg_block_cg with the initial guess read from x0 (ldx0) instead of x: the iterate is
+ * written to x only (saves the caller's copy of the X block into the W block). */
+int gcg_block_cg_x0(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
+                    const int32_t* colidx, const double* val, double diag_shift, int64_t k,
+                    const double* rhs, int64_t ldr, const double* x0, int64_t ldx0, double* x,
+                    int64_t ldx, int32_t max_iters, double rel_tol, int32_t* d_sweeps,
+                    int8_t* d_converged, int8_t* d_frozen, double* d_relres);
+
+/* Y[i, c] = s[c] * X[i, c] (one pass; the block-CG right-hand side (Lambda - theta) X). */
+int gcg_col_scale_copy(void* ctx, int64_t n, int64_t k, const double* s, const double* X,
+                       int64_t ldx, double* Y, int64_t ldy);
+
 /* Row-partitioned (multi-GPU) block CG.  Rows [0, n) are owned; rows [n, n + nghost)
  * of x (and of the internal direction block) are ghost copies of neighbours' rows
  * that the local CSR references (column indices >= n).  The host exchanges them:

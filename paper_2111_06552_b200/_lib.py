@@ -49,6 +49,9 @@ _SIGS = {
     "gcg_fill": [_ptr, _i64, _i64, _dbl, _ptr, _i64],
     "gcg_block_cg": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64, _i32,
                      _dbl, _ptr, _ptr, _ptr, _ptr],
+    "gcg_block_cg_x0": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64,
+                        _ptr, _i64, _i32, _dbl, _ptr, _ptr, _ptr, _ptr],
+    "gcg_col_scale_copy": [_ptr, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64],
     "gcg_block_cg_dist": [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _dbl, _i64, _ptr, _i64, _ptr, _i64,
                           _i32, _dbl, _ptr, _ptr, _ptr, _ptr, _ptr],
     "gcg_gather_rows": [_ptr, _i64, _ptr, _i64, _ptr, _i64, _ptr, _i64],

@@ -166,6 +166,28 @@ int col_scale_launch(Ctx* c, long long n, int k, const double* s, double* X, lon
   return GCG_OK;
 }
 
+// Y[i, c] = s[c] * X[i, c] in one pass (the block-CG right-hand side scale * X)
+__global__ void col_scale_copy_kernel(long long n, int k, const double* __restrict__ s,
+                                      const double* __restrict__ X, long long ldx, double* Y,
+                                      long long ldy) {
+  const long long tot = n * k;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / k;
+    const int c = (int)(e - i * k);
+    Y[i * ldy + c] = s[c] * X[i * ldx + c];
+  }
+}
+
+int col_scale_copy_launch(Ctx* c, long long n, int k, const double* s, const double* X,
+                          long long ldx, double* Y, long long ldy) {
+  if (n <= 0 || k <= 0) return GCG_OK;
+  col_scale_copy_kernel<<<elem_grid(c, n * k), 256, 0, c->stream>>>(n, k, s, X, ldx, Y, ldy);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
 int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, const double* Y,
                     long long ldy, double* out) {
   if (k <= 0) return GCG_OK;

@@ -44,6 +44,8 @@ int axpby_launch(Ctx* c, long long n, int k, double alpha, const double* X, long
 int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, double* Y,
                 long long ldy);
 int fill_launch(Ctx* c, long long n, int k, double v, double* Y, long long ldy);
+int col_scale_copy_launch(Ctx* c, long long n, int k, const double* s, const double* X,
+                          long long ldx, double* Y, long long ldy);
 int col_scale_launch(Ctx* c, long long n, int k, const double* s, double* X, long long ldx);
 int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, const double* Y,
                     long long ldy, double* out);
@@ -53,8 +55,9 @@ int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, cons
 int symmetrize_launch(Ctx* c, int m, double* A, long long lda);
 int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                     const double* val, double shift, int k, const double* rhs, long long ldr,
-                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                    int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist);
+                    const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
+                    double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
+                    double* d_relres, const gcg_cg_dist* dist);
 int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X, long long ldx,
                        double* out, long long ldo);
 int fp64_peak_launch(Ctx* c, int mode, int iters, double* sink, int* grid_out, int* block_out);
@@ -473,8 +476,32 @@ int gcg_block_cg(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const i
   if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
-  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
-                         max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres, nullptr);
+  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, nullptr, 0,
+                         x, ldx, max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres,
+                         nullptr);
+}
+
+int gcg_block_cg_x0(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
+                    const int32_t* colidx, const double* val, double diag_shift, int64_t k,
+                    const double* rhs, int64_t ldr, const double* x0, int64_t ldx0, double* x,
+                    int64_t ldx, int32_t max_iters, double rel_tol, int32_t* d_sweeps,
+                    int8_t* d_converged, int8_t* d_frozen, double* d_relres) {
+  Ctx* c = CTX(p);
+  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || ldx0 < k || !x0 ||
+      max_iters < 0)
+    return GCG_ERR_ARG;
+  if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
+  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x0, ldx0,
+                         x, ldx, max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres,
+                         nullptr);
+}
+
+int gcg_col_scale_copy(void* p, int64_t n, int64_t k, const double* s, const double* X,
+                       int64_t ldx, double* Y, int64_t ldy) {
+  Ctx* c = CTX(p);
+  if (!c || n < 0 || k < 0 || ldx < k || ldy < k || (n > 0 && k > 0 && (!s || !X || !Y)))
+    return GCG_ERR_ARG;
+  return col_scale_copy_launch(c, n, (int)k, s, X, ldx, Y, ldy);
 }
 
 int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
@@ -487,7 +514,7 @@ int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
       !dist->callback || !dist->red_buf)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
-  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, x, ldx,
+  return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, nullptr, 0, x, ldx,
                          max_iters, rel_tol, d_sweeps, d_converged, d_frozen, d_relres, dist);
 }
 

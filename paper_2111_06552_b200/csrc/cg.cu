@@ -337,8 +337,9 @@ __global__ void cg_final(int k, CgState s, int* d_sweeps, int8_t* conv, int8_t* 
 
 int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                    const double* val, double shift, int k, const double* rhs, long long ldr,
-                   double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                   int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist);
+                   const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
+                   double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
+                   double* d_relres, const gcg_cg_dist* dist);
 
 // The k CG recurrences are independent, so they can run in column chunks (each
 // chunk's sweep count is the same as in the joint run).  GCG_CG_CHUNK=w forces
@@ -348,8 +349,9 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
 // is one chunk.
 int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                     const double* val, double shift, int k, const double* rhs, long long ldr,
-                    double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                    int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist) {
+                    const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
+                    double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
+                    double* d_relres, const gcg_cg_dist* dist) {
   if (k <= 0 || k > 256 || n <= 0) return GCG_ERR_ARG;
   GCG_TRY(cuda_status(cudaMemsetAsync(d_sweeps, 0, sizeof(int), c->stream)));
   static const char* env = getenv("GCG_CG_CHUNK");
@@ -357,9 +359,9 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
   if (kc < 1 || kc > k || dist) kc = k;
   for (int c0 = 0; c0 < k; c0 += kc) {
     const int w = (k - c0) < kc ? (k - c0) : kc;
-    GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr, x + c0, ldx,
-                           max_iters, rel_tol, d_sweeps, d_conv + c0, d_frozen + c0,
-                           d_relres + c0, dist));
+    GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr,
+                           x0 ? x0 + c0 : nullptr, ldx0, x + c0, ldx, max_iters, rel_tol,
+                           d_sweeps, d_conv + c0, d_frozen + c0, d_relres + c0, dist));
   }
   return GCG_OK;
 }
@@ -388,8 +390,9 @@ static int dist_reduce(Ctx* c, const gcg_cg_dist* d, const double* part, int npa
 
 int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
                    const double* val, double shift, int k, const double* rhs, long long ldr,
-                   double* x, long long ldx, int max_iters, double rel_tol, int* d_sweeps,
-                   int8_t* d_conv, int8_t* d_frozen, double* d_relres, const gcg_cg_dist* dist) {
+                   const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
+                   double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
+                   double* d_relres, const gcg_cg_dist* dist) {
   const int sgrid = spmm_grid(c, n);
   int ugrid = grid_for(n, 512, 4, c->num_sms);
   long long rpc = (n + ugrid - 1) / ugrid;
@@ -413,7 +416,8 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   double* part = Xc + pvec;
   double* const x_user = x;
   const long long ldx_user = ldx;
-  GCG_TRY(copy_launch(c, n, k, x_user, ldx_user, Xc, k));
+  // initial guess: x0 when given (the caller's X block), else the iterate's own input
+  GCG_TRY(copy_launch(c, n, k, x0 ? x0 : x_user, x0 ? ldx0 : ldx_user, Xc, k));
   x = Xc;
   ldx = k;
   double* upart = part + (size_t)nparts_max * k;  // r-update partials (SpMM's stay readable)

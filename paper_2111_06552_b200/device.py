@@ -335,8 +335,23 @@ def block_cg_dist(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv,
               _p(sweeps), _p(conv), _p(frozen), _p(relres), C.byref(dist))
 
 
-def block_cg(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
+def block_cg(ctx, A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres,
+             x0=None):
     n, k = x.shape
+    if x0 is not None:
+        if x0.shape != x.shape:
+            raise InvalidShape(f"x0 {tuple(x0.shape)} != x {tuple(x.shape)}")
+        _lib.call("gcg_block_cg_x0", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(vals),
+                  float(shift), k, _p(rhs), _ld(rhs), _p(x0), _ld(x0), _p(x), _ld(x),
+                  int(max_iters), float(rel_tol), _p(sweeps), _p(conv), _p(frozen), _p(relres))
+        return
     _lib.call("gcg_block_cg", ctx.h, n, A.nnz, _p(A.rowptr), _p(A.colidx), _p(vals), float(shift), k,
               _p(rhs), _ld(rhs), _p(x), _ld(x), int(max_iters), float(rel_tol), _p(sweeps),
               _p(conv), _p(frozen), _p(relres))
+
+
+def col_scale_copy(ctx, s, X, Y):
+    """Y = X diag(s) in one pass (gcg_col_scale_copy)."""
+    n, k = X.shape
+    _lib.call("gcg_col_scale_copy", ctx.h, n, k, _p(s), _p(X), _ld(X), _p(Y), _ld(Y))
+    return Y

@@ -144,18 +144,25 @@ class LocalOps:
     def residuals(self, AX, X, BX, lam, mode, out):
         return D.ritz_residuals(self.dev, AX, X, BX, lam, mode, out)
 
-    def block_cg(self, vals, shift, rhs, x, max_iters, rel_tol):
+    def block_cg(self, vals, shift, rhs, x, max_iters, rel_tol, x0=None):
+        """Block CG into x; the initial guess is x0 when given (else x's contents)."""
         k = rhs.shape[1]
         sweeps = self.dev.zeros(1, dtype=torch.int32)
         conv = self.dev.zeros(k, dtype=torch.int8)
         frozen = self.dev.zeros(k, dtype=torch.int8)
         relres = self.dev.zeros(k)
-        self._cg(vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres)
+        if x0 is not None and self.distributed:
+            D.copy(self.dev, x0, x)  # the row-partitioned CG reads its guess from x
+            x0 = None
+        if x0 is None:
+            self._cg(vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres)
+        else:
+            self._cg(vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres, x0=x0)
         return CgReport(sweeps, conv, frozen, relres)
 
-    def _cg(self, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres):
+    def _cg(self, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen, relres, x0=None):
         D.block_cg(self.dev, self.prob.A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv,
-                   frozen, relres)
+                   frozen, relres, x0=x0)
 
     # -- replicated small data ------------------------------------------------
     def broadcast(self, t):

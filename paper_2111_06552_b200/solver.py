@@ -562,12 +562,13 @@ def gcg_solve_ops(ops, cfg, x0=None):
             rhs = dev.empty(nloc, bs_eff)
             if Bop is not None:
                 ops.spmm(Bop, x_act, rhs)
+                D.col_scale(dev, scale, rhs)
             else:
-                D.copy(dev, x_act, rhs)
-            D.col_scale(dev, scale, rhs)
-            D.copy(dev, x_act, w_region)
+                D.col_scale_copy(dev, scale, x_act, rhs)  # rhs = X (Lambda - theta), one pass
             vals, shift = prob.shifted(theta)
-            cg_rep = ops.block_cg(vals, shift, rhs, w_region, cfg.cg_max_iters, cfg.cg_rel_tol)
+            # initial guess W0 = X read straight from the X block (cg.py:40-45)
+            cg_rep = ops.block_cg(vals, shift, rhs, w_region, cfg.cg_max_iters, cfg.cg_rel_tol,
+                                  x0=x_act)
             timer.lap("t_step6")
 
             # STEP 2: W against [store, X, P] (solver.py:398-420)
