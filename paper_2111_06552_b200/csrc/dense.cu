@@ -701,16 +701,35 @@ __global__ void __launch_bounds__(256) ritz_partials_kernel(long long n, int k,
   const long long r0 = (long long)blockIdx.x * rows_per_cta;
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
+  // B = I: BX is X itself — one stream fewer
+  const bool same = (BX == X) && (ldbx == ldx);
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   if (rl < lanes) {
     const double l = lam[c];
-    for (long long i = r0 + rl; i < r1; i += lanes) {
-      const double ax = AX[i * ldax + c], x = X[i * ldx + c], bx = BX[i * ldbx + c];
+    auto add = [&](double ax, double x, double bx) {
       const double res = (mode == 0) ? ax - l * x : ax - l * bx;
       s0 = fma(res, res, s0);
       s1 = fma(x, x, s1);
       s2 = fma(x, bx, s2);
       s3 = fma(bx, bx, s3);
+    };
+    constexpr int U = 8;  // rows in flight per thread
+    long long i = r0 + rl;
+    for (; i + (U - 1) * lanes < r1; i += U * lanes) {
+      double av[U], xv[U], bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long ii = i + u * lanes;
+        av[u] = AX[ii * ldax + c];
+        xv[u] = X[ii * ldx + c];
+        bv[u] = same ? xv[u] : BX[ii * ldbx + c];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) add(av[u], xv[u], bv[u]);
+    }
+    for (; i < r1; i += lanes) {
+      const double x = X[i * ldx + c];
+      add(AX[i * ldax + c], x, same ? x : BX[i * ldbx + c]);
     }
   }
   sm[0][threadIdx.x] = s0;
@@ -727,24 +746,39 @@ __global__ void __launch_bounds__(256) ritz_partials_kernel(long long n, int k,
   }
 }
 
-__global__ void ritz_finish_kernel(int k, int nparts, const double* part, const double* lam,
-                                   int mode, double* out) {
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    double s[4] = {0, 0, 0, 0};
-    for (int b = 0; b < nparts; ++b)
-      for (int q = 0; q < 4; ++q) s[q] += part[((long long)b * 4 + q) * k + c];
+// one 128-thread block per column: the 4 sums over the per-CTA partials in a fixed
+// order (thread t: parts t, t + 128, ...; then a fixed tree), then the residual
+__global__ void __launch_bounds__(128) ritz_finish_kernel(int k, int nparts, const double* part,
+                                                          const double* lam, int mode,
+                                                          double* out) {
+  __shared__ double sm[4][128];
+  const int c = blockIdx.x;
+  double s[4] = {0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nparts; b += 128)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] += part[((long long)b * 4 + q) * k + c];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sm[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int w = 64; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sm[q][threadIdx.x] += sm[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     const double l = lam[c];
     double den;
     if (mode == 2) {
-      den = fabs(l) * sqrt(s[3]);
+      den = fabs(l) * sqrt(sm[3][0]);
     } else if (mode == 1) {
-      den = sqrt(fmax(s[2], 0.0));
+      den = sqrt(fmax(sm[2][0], 0.0));
       if (l > 0.0) den *= l;
     } else {
-      den = sqrt(s[1]);
+      den = sqrt(sm[1][0]);
     }
     if (den == 0.0) den = 1.0;
-    out[c] = sqrt(s[0]) / den;
+    out[c] = sqrt(sm[0][0]) / den;
   }
 }
 
@@ -760,7 +794,7 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
   double* part = (double*)c->partials.ptr;
   ritz_partials_kernel<<<grid, 256, 0, c->stream>>>(n, k, AX, ldax, X, ldx, BX, ldbx, lam, mode,
                                                      rpc, part);
-  ritz_finish_kernel<<<1, 256, 0, c->stream>>>(k, grid, part, lam, mode, out);
+  ritz_finish_kernel<<<k, 128, 0, c->stream>>>(k, grid, part, lam, mode, out);
   g_launches += 2;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -794,7 +828,7 @@ int ritz_sums_launch(Ctx* c, long long n, int k, const double* AX, long long lda
 int ritz_finish_launch(Ctx* c, int k, const double* sums, const double* lam, int mode,
                        double* out) {
   if (k <= 0) return GCG_OK;
-  ritz_finish_kernel<<<1, 256, 0, c->stream>>>(k, 1, sums, lam, mode, out);
+  ritz_finish_kernel<<<k, 128, 0, c->stream>>>(k, 1, sums, lam, mode, out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;

@@ -35,7 +35,7 @@ tot_gap = 0.0
 for s, e, nm in ev[lo:hi]:
     gap = s - last
     tot_gap += max(gap, 0)
-    if gap > 3 or e - s > 30:
+    if gap > 3 or e - s > 30 or len(sys.argv) > 3:
         print(f"gap {gap:7.1f} us  dur {e - s:7.1f} us  {nm}")
     last = max(last, e)
 print(f"iteration span {ev[hi][0] - ev[lo][0]:.1f} us, idle {tot_gap:.1f} us, events {hi - lo}")
