@@ -481,6 +481,7 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     partials = (double*)c->partials.ptr;
   }
   int c0 = 0;
+  int grid_fixed = 0;
   while (c0 < k) {
     const int rest = k - c0;
     // widest access every row start of X allows (rows of X must stay VEC-aligned)
@@ -491,7 +492,16 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     else if (vec_cap >= 2 && ldx % 2 == 0 && aligned_to(X + c0, 16) && rest >= 2) vec = 2;
     // even passes of at most 32 lanes x NV x VEC columns
     auto max_cols = [](int v) { return 32 * v * (kSpmmMaxSlots / v < 4 ? kSpmmMaxSlots / v : 4); };
-    const int npass = (rest + max_cols(vec) - 1) / max_cols(vec);
+    // Column panels of <= 40 for 64 < k <= 128: one pass of k = 100 spreads 25 vec4 chunks
+    // over 13 lanes x 2 (one row per warp); three ~36-column passes run 3 rows per warp
+    // and keep each pass's neighbour rows L2-resident — measured at cfg4 (k = 100,
+    // n = 2.1M): 1.90 -> 1.42 ms for the CG form, 1.71 -> 1.24 ms plain, although the
+    // index/value stream is read three times.  Wider k (cfg5, k = 200) is gather-bound
+    // and gains nothing (scripts/spmm_panel.sh).  GCG_SPMM_PANEL overrides the cap.
+    static const int panel_env = getenv("GCG_SPMM_PANEL") ? atoi(getenv("GCG_SPMM_PANEL")) : -1;
+    const int panel = panel_env >= 0 ? panel_env : (k > 64 && k <= 128 ? 40 : 0);
+    int npass = (rest + max_cols(vec) - 1) / max_cols(vec);
+    if (panel > 0 && (rest + panel - 1) / panel > npass) npass = (rest + panel - 1) / panel;
     int kc = (rest + npass - 1) / npass;
     kc = (kc + vec - 1) / vec * vec;
     if (kc > rest) kc = rest;
@@ -511,7 +521,9 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
         eff = eff2;
       }
     }
-    int grid = spmm_grid_for(c, n, nv * vec);
+    // caller-reduced partials ([grid][k]) need one grid for every pass
+    int grid = grid_fixed ? grid_fixed : spmm_grid_for(c, n, nv * vec);
+    if (partials_ext) grid_fixed = grid;
     long long rpc = 0;
     if (contig) {
       const long long step = 8LL * (32 / lpr);  // rows per CTA step (8 warps)
