@@ -302,8 +302,21 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
   // 128 x 64 tiles (4 x 2 warps, no row-group split: more DMMA per staged element)
   // when they add no padding over 64-row tiles or the N side is narrow; measured
   // 200x200 14.5 vs 10.8 TF/s, 400x40 11.6 vs 9.5, but 160x160 8.6 vs 12.8
-  if (k1 > 96 && ((k1 + 127) / 128 * 128 == (k1 + 63) / 64 * 64 || k2 <= 64))
-    GO(128, 64, 32, 32);
+  const bool t128 = k1 > 96 && ((k1 + 127) / 128 * 128 == (k1 + 63) / 64 * 64 || k2 <= 64);
+  // Wide 160 x 128 tiles (2 x 4 warps of 80 x 32: 40 DMMAs per 14 fragment loads, X read
+  // once and Y twice for k2 <= 128; one CTA per SM) unless they pad clearly more than
+  // the narrow tile.  Measured at n = 2.1M (scripts/gram_wide.sh): 300x100 12.6 -> 20.9
+  // TF/s, 600x200 11.9 -> 21.1, 900x100 12.4 -> 14.5 (before the whole-wave slab count);
+  // 200x200 and 500x100 (1.25x the padded area) stay on 128 x 64.
+  if (k1 > 128 && k2 > 64) {
+    static const char* wide_env = getenv("GCG_GRAM_WIDE");
+    const long long pw = (long long)((k1 + 159) / 160 * 160) * ((k2 + 127) / 128 * 128);
+    const int bm = t128 ? 128 : 64;
+    const long long pn = (long long)((k1 + bm - 1) / bm * bm) * ((k2 + 63) / 64 * 64);
+    const bool wide = wide_env ? wide_env[0] == '1' : 5 * pw < 6 * pn;
+    if (wide) GO(160, 128, 80, 32);
+  }
+  if (t128) GO(128, 64, 32, 32);
   GO(64, 64, 32, 32);
 #undef GO
 }
@@ -428,8 +441,8 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
   int BM = 0, BN = 0;
   gram_dispatch(c, n, k1, k2, X, ldx, Y, ldy, nullptr, 0, 0, false, &BM, &BN);
   const long long tiles = (long long)((k1 + BM - 1) / BM) * ((k2 + BN - 1) / BN);
-  // ~2 CTAs per SM in total, slabs a multiple of 64 rows
-  long long nslab = (2LL * c->num_sms + tiles - 1) / tiles;
+  // ~2 CTAs per SM in total (whole waves: rounded down), slabs a multiple of 64 rows
+  long long nslab = (2LL * c->num_sms) / tiles;
   const long long max_slab = (n + 255) / 256;
   if (nslab > max_slab) nslab = max_slab;
   if (nslab < 1) nslab = 1;

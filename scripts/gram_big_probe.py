@@ -11,7 +11,10 @@ def timeit(fn, reps=10):
     return e0.elapsed_time(e1) / reps / 1e3
 rng = np.random.default_rng(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 524288
-for k1, k2 in ((200, 200), (400, 40), (900, 100), (360, 40), (160, 160)):
+SHAPES = ((200, 200), (400, 40), (900, 100), (360, 40), (160, 160))
+if os.environ.get("SHAPES"):
+    SHAPES = [tuple(int(v) for v in s.split("x")) for s in os.environ["SHAPES"].split(",")]
+for k1, k2 in SHAPES:
     X = torch.from_numpy(rng.standard_normal((n, k1))).to(dev.device)
     Y = torch.from_numpy(rng.standard_normal((n, k2))).to(dev.device)
     G = dev.empty(k1, k2)
