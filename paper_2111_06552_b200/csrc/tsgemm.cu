@@ -855,6 +855,10 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   else if (d <= 128) LC(64, 128, 32, 32);
   else if (d <= 160) LC(64, 160, 32, 40);
   else if (d <= 192) LC(64, 192, 32, 48);
+  // d in (192, 224] (cfg5's bs = 200): 224-wide tile, 12 instead of 22 % padding —
+  // n = 2.1M, 600x200 22.5 -> 20.4 ms, 200x200 8.4 -> 7.8 ms.  (A 128 x 112 tile of
+  // 4 x 2 warps for d in (96, 112] measured slower than 64 x 128: 300x100 6.1 vs 5.5 ms.)
+  else if (d <= 224) LC(64, 224, 32, 56);
   else LC(64, 256, 32, 64);
 #undef LC
   prof_stop(c, ps);

@@ -119,7 +119,10 @@ def test_spmm_self_epilogue(dev, k, diag):
 
 
 @pytest.mark.parametrize("n,k1,k2", [(1, 1, 1), (23, 4, 3), (5000, 6, 4), (262144, 200, 20),
-                                      (100003, 80, 80), (4097, 17, 33), (70000, 120, 7)])
+                                      (100003, 80, 80), (4097, 17, 33), (70000, 120, 7),
+                                      # wide 160 x 128 tiles (cfg4 / cfg5 deflation shapes)
+                                      (50001, 300, 100), (20000, 900, 100), (30011, 600, 200),
+                                      (4099, 161, 65), (8191, 200, 200), (12345, 500, 100)])
 def test_gram_vs_numpy(dev, n, k1, k2):
     rng = np.random.default_rng(n + k1)
     x = rng.standard_normal((n, k1))
@@ -176,7 +179,9 @@ def test_gram_strided_out_and_accumulate(dev):
 
 
 @pytest.mark.parametrize("n,m,d", [(1000, 16, 16), (262144, 200, 160), (5000, 7, 3),
-                                    (77777, 64, 100), (3000, 300, 20)])
+                                    (77777, 64, 100), (3000, 300, 20), (30011, 300, 100),
+                                    (20001, 600, 200), (5003, 150, 210), (4001, 97, 97),
+                                    (9999, 900, 112)])
 def test_lincomb_vs_numpy(dev, n, m, d):
     rng = np.random.default_rng(m * d)
     x = rng.standard_normal((n, m))
@@ -189,7 +194,8 @@ def test_lincomb_vs_numpy(dev, n, m, d):
 
 
 @pytest.mark.parametrize("n,m,d,off", [(5000, 200, 180, 0), (3001, 40, 24, 0),
-                                        (3001, 40, 20, 7), (777, 64, 64, 0)])
+                                        (3001, 40, 20, 7), (777, 64, 64, 0), (5000, 300, 100, 0),
+                                        (3001, 400, 200, 0)])
 def test_lincomb_in_place(dev, n, m, d, off):
     """[X|P] <- basis [coeffs|phat] written over the basis' own columns (solver step 5)."""
     rng = np.random.default_rng(n + d)
