@@ -492,3 +492,22 @@ def test_spmm_sell_equals_csr(dev, name, mk, sigma, k):
         if "dot_mode" in kw:
             ref = (want * want).sum(0) if kw["dot_mode"] == 2 else (want * x).sum(0)
             assert rel_err(host(d1), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (200, 20, 200), (20, 20, 200), (200, 200, 200),
+                                   (17, 33, 300), (40, 13, 129), (5, 7, 128), (300, 40, 1000)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_dgemm_small_vs_numpy(dev, M, N, K, ta, tb):
+    """Small dense GEMM (momentum block, P coupling): every output one fma chain over k."""
+    rng = np.random.default_rng(M * 1000 + N * 10 + K)
+    a = rng.standard_normal((K, M) if ta else (M, K))
+    b = rng.standard_normal((N, K) if tb else (K, N))
+    c0 = rng.standard_normal((M, N))
+    want = 0.75 * ((a.T if ta else a) @ (b.T if tb else b)) - 0.5 * c0
+    cm = rm(dev, c0)
+    D.dgemm(dev, rm(dev, a), rm(dev, b), cm, ta=ta, tb=tb, alpha=0.75, beta=-0.5)
+    assert rel_err(host(cm), want) <= 1e-13
+    # strided views (leading dimension > columns), beta = 0 never reads C
+    big = rm(dev, np.full((M, N + 5), np.nan))
+    D.dgemm(dev, rm(dev, a), rm(dev, b), big[:, 2:2 + N], ta=ta, tb=tb)
+    assert rel_err(host(big[:, 2:2 + N]), (a.T if ta else a) @ (b.T if tb else b)) <= 1e-13
