@@ -309,11 +309,17 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
   // TF/s, 600x200 11.9 -> 21.1, 900x100 12.4 -> 14.5 (before the whole-wave slab count);
   // 200x200 and 500x100 (1.25x the padded area) stay on 128 x 64.
   if (k1 > 128 && k2 > 64) {
+    // k2 in (96, 112] (cfg4's bs = 100): 160 x 112 tiles of 4 x 2 warps (40 x 56) pad
+    // 12 % instead of 28 %: 900x100 18.2 -> 16.3 ms, 300x100 5.5 -> 5.4 ms at n = 2.1M
     static const char* wide_env = getenv("GCG_GRAM_WIDE");
-    const long long pw = (long long)((k1 + 159) / 160 * 160) * ((k2 + 127) / 128 * 128);
+    static const char* g112 = getenv("GCG_GRAM112");
+    const bool n112 = k2 > 96 && k2 <= 112 && !(g112 && g112[0] == '0');
+    const long long pw =
+        (long long)((k1 + 159) / 160 * 160) * (n112 ? 112 : (k2 + 127) / 128 * 128);
     const int bm = t128 ? 128 : 64;
     const long long pn = (long long)((k1 + bm - 1) / bm * bm) * ((k2 + 63) / 64 * 64);
     const bool wide = wide_env ? wide_env[0] == '1' : 5 * pw < 6 * pn;
+    if (wide && n112) GO(160, 112, 40, 56);
     if (wide) GO(160, 128, 80, 32);
   }
   if (t128) GO(128, 64, 32, 32);
@@ -852,12 +858,17 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   else if (d <= 48) LC(256, 48, 32, 48);
   else if (d <= 64) LC(256, 64, 32, 64);
   else if (d <= 96) LC(64, 96, 32, 24);
+  // d in (96, 112] (cfg4's bs = 100): 4 x 2 warps of 16 x 56 — 12 % padding instead of
+  // the 128-wide tile's 28 %: 300x100 5.50 -> 4.33 ms, 900x100 15.4 -> 12.5 ms at n = 2.1M
+  // (29-30 TF/s; a 128 x 112 tile of 32 x 56 warps was slower, 6.1 ms)
+  else if (d <= 112 && !(getenv("GCG_LC112") && getenv("GCG_LC112")[0] == '0'))
+    LC(64, 112, 16, 56);
   else if (d <= 128) LC(64, 128, 32, 32);
   else if (d <= 160) LC(64, 160, 32, 40);
   else if (d <= 192) LC(64, 192, 32, 48);
   // d in (192, 224] (cfg5's bs = 200): 224-wide tile, 12 instead of 22 % padding —
   // n = 2.1M, 600x200 22.5 -> 20.4 ms, 200x200 8.4 -> 7.8 ms.  (A 128 x 112 tile of
-  // 4 x 2 warps for d in (96, 112] measured slower than 64 x 128: 300x100 6.1 vs 5.5 ms.)
+  // 4 x 2 warps of 32 x 56 for d in (96, 112] measured slower than 64 x 128.)
   else if (d <= 224) LC(64, 224, 32, 56);
   else LC(64, 256, 32, 64);
 #undef LC
