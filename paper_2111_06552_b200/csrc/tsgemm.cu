@@ -322,6 +322,12 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
     if (wide && n112) GO(160, 112, 40, 56);
     if (wide) GO(160, 128, 80, 32);
   }
+  // k1 > 128, k2 in (32, 48] (cfg3's bs = 40 deflation shapes): 160 x 48 tiles of 4 x 2
+  // warps (40 x 24) instead of 64-wide ones that pad k2 = 40 by 60 %; at n = 493k:
+  // 400x40 1.38 -> 1.00 ms, 320x40 1.04 -> 0.68 ms, 600x40 1.72 -> 1.33 ms
+  // (`profiles/r01_tile48.txt`)
+  static const char* g48 = getenv("GCG_GRAM48");
+  if (!(g48 && g48[0] == '0') && k1 > 128 && k2 > 32 && k2 <= 48) GO(160, 48, 40, 24);
   if (t128) GO(128, 64, 32, 32);
   GO(64, 64, 32, 32);
 #undef GO
