@@ -80,6 +80,17 @@ int gcg_prof_sample(void* ctx, int stride);
 int gcgeig_csr_matvec(const int64_t* indptr, const int64_t* indices, const double* data,
                       int64_t nrow, int64_t ncol, const double* x, int64_t k, int64_t ldx,
                       double* out, int64_t ldo);
+/* A CSR operator kept resident in HBM — replaces CsrOperator.apply
+ * (operators.py:103-111; the reference's `kernels.csr_matvec` per call re-reads
+ * the matrix).  create uploads indptr/indices (int64, validated: monotone row
+ * pointers, column indices in [0, ncol)) and data once; apply computes
+ * out[:, c] = A @ x[:, c] for F-order host blocks (x: ncol x k, column stride
+ * ldx; out: nrow x k, column stride ldo); destroy frees it (NULL is a no-op). */
+int gcgeig_csr_create(const int64_t* indptr, const int64_t* indices, const double* data,
+                      int64_t nrow, int64_t ncol, void** handle);
+int gcgeig_csr_apply(void* handle, const double* x, int64_t k, int64_t ldx, double* out,
+                     int64_t ldo);
+int gcgeig_csr_destroy(void* handle);
 /* out[r*out_rs + c*out_cs] = sum_i x[i + r*ldx] * y[i + c*ldy]  (x: n x kx, y: n x ky).
  * Always bit-stable run to run; `chunk`/`deterministic` are accepted for interface parity. */
 int gcgeig_inner_product(const double* x, int64_t n, int64_t kx, int64_t ldx, const double* y,

@@ -26,6 +26,9 @@ _SIGS = {
     "gcg_ctx_set_stream": [_ptr, _ptr],
     "gcg_ctx_sync": [_ptr],
     "gcgeig_csr_matvec": [_ptr, _ptr, _ptr, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64],
+    "gcgeig_csr_create": [_ptr, _ptr, _ptr, _i64, _i64, C.POINTER(_ptr)],
+    "gcgeig_csr_apply": [_ptr, _ptr, _i64, _i64, _ptr, _i64],
+    "gcgeig_csr_destroy": [_ptr],
     "gcgeig_inner_product": [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _int],
     "gcgeig_axpby": [_dbl, _ptr, _i64, _i64, _i64, _dbl, _ptr, _i64],
     "gcg_prof_begin": [_ptr],

@@ -473,7 +473,7 @@ int gcg_block_cg(void* p, int64_t n, int64_t nnz, const int32_t* rowptr, const i
                  int64_t ldr, double* x, int64_t ldx, int32_t max_iters, double rel_tol,
                  int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen, double* d_relres) {
   Ctx* c = CTX(p);
-  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0)
+  if (!c || n <= 0 || k <= 0 || ldr < k || ldx < k || max_iters < 0)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
   return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, nullptr, 0,
@@ -487,7 +487,7 @@ int gcg_block_cg_x0(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
                     int64_t ldx, int32_t max_iters, double rel_tol, int32_t* d_sweeps,
                     int8_t* d_converged, int8_t* d_frozen, double* d_relres) {
   Ctx* c = CTX(p);
-  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || ldx0 < k || !x0 ||
+  if (!c || n <= 0 || k <= 0 || ldr < k || ldx < k || ldx0 < k || !x0 ||
       max_iters < 0)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
@@ -510,7 +510,7 @@ int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
                       double rel_tol, int32_t* d_sweeps, int8_t* d_converged, int8_t* d_frozen,
                       double* d_relres, const gcg_cg_dist* dist) {
   Ctx* c = CTX(p);
-  if (!c || n <= 0 || k <= 0 || k > 256 || ldr < k || ldx < k || max_iters < 0 || !dist ||
+  if (!c || n <= 0 || k <= 0 || ldr < k || ldx < k || max_iters < 0 || !dist ||
       !dist->callback || !dist->red_buf)
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
@@ -808,6 +808,104 @@ int gcgeig_csr_matvec(const int64_t* indptr, const int64_t* indices, const doubl
   GCG_CHECK_LAUNCH();
   GCG_TRY(d2h_cm(c, d_ycm, nrow, k, out, ldo));
   return cuda_status(cudaStreamSynchronize(s));
+}
+
+// A CSR operator resident in HBM for the reference's operator protocol
+// (CsrOperator.apply, operators.py:103-111): the pattern and values are uploaded
+// once, each apply moves only the F-order multivector in and the product out.
+struct HostCsr {
+  long long n = 0, ncol = 0, nnz = 0;
+  int* rowptr = nullptr;  // n + 1, then nnz column indices (one allocation)
+  double* val = nullptr;
+};
+
+int gcgeig_csr_create(const int64_t* indptr, const int64_t* indices, const double* data,
+                      int64_t nrow, int64_t ncol, void** handle) {
+  if (!handle) return GCG_ERR_ARG;
+  *handle = nullptr;
+  if (nrow < 0 || ncol < 0 || !indptr || nrow >= (1LL << 31) || ncol >= (1LL << 31))
+    return GCG_ERR_ARG;
+  const long long nnz = indptr[nrow] - indptr[0];
+  if (indptr[0] != 0 || nnz < 0 || nnz >= (1LL << 31)) return GCG_ERR_ARG;
+  for (long long i = 0; i < nrow; ++i)
+    if (indptr[i + 1] < indptr[i]) return GCG_ERR_ARG;
+  for (long long e = 0; e < nnz; ++e)
+    if (indices[e] < 0 || indices[e] >= ncol) return GCG_ERR_ARG;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  Ctx* c;
+  GCG_TRY(host_ctx(&c));
+  HostCsr* h = new HostCsr();
+  h->n = nrow;
+  h->ncol = ncol;
+  h->nnz = nnz;
+  const size_t nidx = (size_t)nrow + 1 + (size_t)nnz;
+  if (cudaMalloc((void**)&h->rowptr, sizeof(int) * nidx) != cudaSuccess ||
+      cudaMalloc((void**)&h->val, sizeof(double) * (size_t)(nnz > 0 ? nnz : 1)) != cudaSuccess) {
+    cudaFree(h->rowptr);
+    delete h;
+    return GCG_ERR_ALLOC;
+  }
+  GCG_TRY(ensure(c->host_tmp, sizeof(long long) * nidx + 64));
+  long long* d_i64 = (long long*)c->host_tmp.ptr;
+  cudaStream_t s = c->stream;
+  GCG_TRY(cuda_status(cudaMemcpyAsync(d_i64, indptr, sizeof(long long) * (nrow + 1),
+                                      cudaMemcpyHostToDevice, s)));
+  if (nnz > 0) {
+    GCG_TRY(cuda_status(cudaMemcpyAsync(d_i64 + nrow + 1, indices, sizeof(long long) * nnz,
+                                        cudaMemcpyHostToDevice, s)));
+    GCG_TRY(cuda_status(
+        cudaMemcpyAsync(h->val, data, sizeof(double) * nnz, cudaMemcpyHostToDevice, s)));
+  }
+  i64_to_i32_kernel<<<elem_grid_host(c, (long long)nidx), 256, 0, s>>>((long long)nidx, d_i64,
+                                                                       h->rowptr);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(cuda_status(cudaStreamSynchronize(s)));
+  *handle = h;
+  return GCG_OK;
+}
+
+int gcgeig_csr_apply(void* handle, const double* x, int64_t k, int64_t ldx, double* out,
+                     int64_t ldo) {
+  HostCsr* h = (HostCsr*)handle;
+  if (!h || k < 0 || ldx < h->ncol || ldo < h->n) return GCG_ERR_ARG;
+  if (h->n == 0 || k == 0) return GCG_OK;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  Ctx* c;
+  GCG_TRY(host_ctx(&c));
+  const size_t b_x = sizeof(double) * (size_t)h->ncol * k;
+  const size_t b_y = sizeof(double) * (size_t)h->n * k;
+  GCG_TRY(ensure(c->host_tmp2, 2 * b_x + 64));
+  GCG_TRY(ensure(c->host_tmp3, 2 * b_y + 64));
+  double* d_xcm = (double*)c->host_tmp2.ptr;
+  double* d_xrm = d_xcm + (size_t)h->ncol * k;
+  double* d_yrm = (double*)c->host_tmp3.ptr;
+  double* d_ycm = d_yrm + (size_t)h->n * k;
+  cudaStream_t s = c->stream;
+  GCG_TRY(h2d_cm(c, x, h->ncol, k, ldx, d_xcm));
+  cm_to_rm_kernel<<<elem_grid_host(c, h->ncol * k), 256, 0, s>>>(h->ncol, (int)k, d_xcm,
+                                                                 h->ncol, d_xrm);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(spmm_launch_impl(c, h->n, h->nnz, h->rowptr, h->rowptr + h->n + 1, h->val, (int)k,
+                           d_xrm, k, 1.0, 0.0, nullptr, 0, 0.0, nullptr, 0, d_yrm, k, 0, nullptr,
+                           0, nullptr, nullptr, nullptr, nullptr));
+  rm_to_cm_kernel<<<elem_grid_host(c, h->n * k), 256, 0, s>>>(h->n, (int)k, d_yrm, d_ycm);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  GCG_TRY(d2h_cm(c, d_ycm, h->n, k, out, ldo));
+  return cuda_status(cudaStreamSynchronize(s));
+}
+
+int gcgeig_csr_destroy(void* handle) {
+  HostCsr* h = (HostCsr*)handle;
+  if (!h) return GCG_OK;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  if (g_host_ctx) cudaStreamSynchronize(g_host_ctx->stream);
+  cudaFree(h->rowptr);
+  cudaFree(h->val);
+  delete h;
+  return GCG_OK;
 }
 
 int gcgeig_inner_product(const double* x, int64_t n, int64_t kx, int64_t ldx, const double* y,

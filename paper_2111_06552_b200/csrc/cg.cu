@@ -352,11 +352,15 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
                     const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
                     double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
                     double* d_relres, const gcg_cg_dist* dist) {
-  if (k <= 0 || k > 256 || n <= 0) return GCG_ERR_ARG;
+  if (k <= 0 || n <= 0) return GCG_ERR_ARG;
   GCG_TRY(cuda_status(cudaMemsetAsync(d_sweeps, 0, sizeof(int), c->stream)));
   static const char* env = getenv("GCG_CG_CHUNK");
   int kc = env ? atoi(env) : k;
-  if (kc < 1 || kc > k || dist) kc = k;
+  if (kc < 1 || kc > k) kc = k;
+  // the sweep kernels hold one column per thread slot of a 256-thread CTA: wider
+  // blocks (block_size > 256, e.g. nev > 1280) run in column chunks, each with
+  // the same sweep count as the joint run (the reported count is the max)
+  if (kc > 256) kc = (k + (k + 255) / 256 - 1) / ((k + 255) / 256);
   for (int c0 = 0; c0 < k; c0 += kc) {
     const int w = (k - c0) < kc ? (k - c0) : kc;
     GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr,
@@ -393,6 +397,7 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
                    const double* x0, long long ldx0, double* x, long long ldx, int max_iters,
                    double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
                    double* d_relres, const gcg_cg_dist* dist) {
+  if (k <= 0 || k > 256) return GCG_ERR_ARG;
   const int sgrid = spmm_grid(c, n);
   int ugrid = grid_for(n, 512, 4, c->num_sms);
   long long rpc = (n + ugrid - 1) / ugrid;

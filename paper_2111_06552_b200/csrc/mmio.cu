@@ -25,6 +25,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <exception>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
@@ -249,6 +251,12 @@ void read_array(MMFile& f, size_t first, long long nrows, long long ncols) {
   gcg_mm_info* info = &f.info;
   const size_t nl = f.lb.size();
   long long expected;
+  // the header is untrusted: check the value count for overflow and never size a
+  // buffer from it (the reference counts the values first, io.py:214-222)
+  if (nrows < 0 || ncols < 0 || (ncols > 0 && nrows > (1LL << 62) / ncols)) {
+    set_err(info, 1, (long long)first, "array dimensions too large");
+    return;
+  }
   if (info->symmetric) {
     if (nrows != ncols) {
       set_err(info, 1, (long long)first, "symmetric array must be square");
@@ -259,7 +267,6 @@ void read_array(MMFile& f, size_t first, long long nrows, long long ncols) {
     expected = nrows * ncols;
   }
   std::vector<double> v;
-  v.reserve((size_t)expected);
   std::vector<size_t> tb(64), te(64);
   for (size_t ln = first; ln < nl; ++ln) {
     if (skip_line(f, ln)) continue;
@@ -400,7 +407,13 @@ int gcg_mm_open(const char* path, int nthreads, void** handle, gcg_mm_info* info
     return GCG_ERR_IO;
   }
   fclose(fp);
-  parse_file(*f, nthreads);
+  try {
+    parse_file(*f, nthreads);
+  } catch (const std::bad_alloc&) {
+    set_err(&f->info, 3, 0, "out of host memory while parsing");
+  } catch (const std::exception& e) {
+    set_err(&f->info, 1, 0, std::string("parse failed: ") + e.what());
+  }
   *info = f->info;
   if (f->info.err_kind) {
     const int st = f->info.err_kind == 1 ? GCG_ERR_PARSE : (f->info.err_kind == 2 ? GCG_ERR_UNSUPPORTED : GCG_ERR_IO);

@@ -857,6 +857,7 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   // d <= 64: 8 warps stacked along rows (BM = 256, warp tile 32 x BN);
   // d  > 64: 2 x 4 warps (BM = 64, warp tile 32 x BN/4).
 #define LC(bm, bn, wm, wn) lincomb_go<bm, bn, wm, wn>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec)
+  static const bool lc112 = !(getenv("GCG_LC112") && getenv("GCG_LC112")[0] == '0');
   if (d <= 8) LC(256, 8, 32, 8);
   else if (d <= 16) LC(256, 16, 32, 16);
   else if (d <= 24) LC(256, 24, 32, 24);
@@ -867,7 +868,7 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   // d in (96, 112] (cfg4's bs = 100): 4 x 2 warps of 16 x 56 — 12 % padding instead of
   // the 128-wide tile's 28 %: 300x100 5.50 -> 4.33 ms, 900x100 15.4 -> 12.5 ms at n = 2.1M
   // (29-30 TF/s; a 128 x 112 tile of 32 x 56 warps was slower, 6.1 ms)
-  else if (d <= 112 && !(getenv("GCG_LC112") && getenv("GCG_LC112")[0] == '0'))
+  else if (d <= 112 && lc112)
     LC(64, 112, 16, 56);
   else if (d <= 128) LC(64, 128, 32, 32);
   else if (d <= 160) LC(64, 160, 32, 40);

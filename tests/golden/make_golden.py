@@ -7,6 +7,7 @@ into oracle/_ref (oracle/build_ref.sh) or importable from /root/reference:
     python tests/golden/make_golden.py --alg2     # Alg. 2 cases only -> golden_alg2.npz
     python tests/golden/make_golden.py --cfg 2    # BASELINE config 2 (~8 min)
     python tests/golden/make_golden.py --cfg 3    # BASELINE config 3 (~1-2 h)
+    python tests/golden/make_golden.py --mid      # cfg4/cfg5-family mid-size moving runs
 
 The outputs are committed; the GPU box (which has no /root/reference) only
 reads them.  Parity cases follow SURVEY.md §8(c): the reference's own KAT
@@ -202,6 +203,40 @@ def cfg_run(cfg):
     )
 
 
+def mid_cases():
+    """Mid-size members of the config 4 / config 5 families (moving window), run by the
+    reference with the BASELINE.md §3 patch: cfg4's variable-coefficient operator at 32^3
+    (nev = 100) and cfg5's 27-point stencil at 64^3 (nev = 100, tol 1e-7) — the
+    scaled-down cases the row-partitioned and arena tests compare against."""
+    return [
+        ("varcoef32_moving", P.varcoef_diffusion_3d(32, seed=0), None,
+         dict(num_eigen=100, seed=0, moving=True, tol=1e-8)),
+        ("stencil27_64_moving", P.stencil27(64), None,
+         dict(num_eigen=100, seed=0, moving=True, tol=1e-7)),
+    ]
+
+
+def mid(names=None):
+    K.use_backend("numpy")
+    path = os.path.join(HERE, "golden_mid.json")
+    res = json.load(open(path)) if os.path.exists(path) else {}
+    for name, a, b, kw in mid_cases():
+        if names and name not in names:
+            continue
+        t0 = time.perf_counter()
+        rep = run_solver(a, b, kw, True)
+        dt = time.perf_counter() - t0
+        res[name] = dict(kw=kw, status=rep.status, iterations=rep.iterations, seconds=dt,
+                         cpu_count=os.cpu_count(), backend="numpy",
+                         eigenvalues=rep.eigenvalues.tolist(), residuals=rep.residuals.tolist(),
+                         converged=[h.num_converged for h in rep.history],
+                         total_reductions=rep.total_reductions,
+                         max_projection_dim=rep.max_projection_dim)
+        print(f"{name}: {rep.status} iters={rep.iterations} {dt:.1f}s", flush=True)
+        with open(path, "w") as f:
+            json.dump(res, f, indent=1)
+
+
 def alg2_cases():
     """modified_block_orth (Alg. 2) inputs following test_orth.py:46-67, 145-178."""
     def blk(n, m, seed):
@@ -247,7 +282,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=0, help="full BASELINE config run (2 or 3)")
     ap.add_argument("--alg2", action="store_true", help="only the Alg. 2 vectors -> golden_alg2.npz")
+    ap.add_argument("--mid", nargs="*", default=None,
+                    help="mid-size cfg4/cfg5-family moving-window runs -> golden_mid.json")
     args = ap.parse_args()
+    if args.mid is not None:
+        mid(args.mid)
+        return
     if args.alg2 or not args.cfg:
         o2 = {}
         alg2(o2)

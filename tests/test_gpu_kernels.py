@@ -5,6 +5,8 @@ reference ops") measured normwise and the reference's own
 kernel tests (test_kernels.py:43-102).
 """
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse
@@ -16,6 +18,8 @@ from paper_2111_06552_b200 import device as D
 from paper_2111_06552_b200 import problems as P
 from paper_2111_06552_b200 import refbackend
 from paper_2111_06552_b200.operators import DeviceCsr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -511,3 +515,55 @@ def test_dgemm_small_vs_numpy(dev, M, N, K, ta, tb):
     big = rm(dev, np.full((M, N + 5), np.nan))
     D.dgemm(dev, rm(dev, a), rm(dev, b), big[:, 2:2 + N], ta=ta, tb=tb)
     assert rel_err(host(big[:, 2:2 + N]), (a.T if ta else a) @ (b.T if tb else b)) <= 1e-13
+
+
+# Tile shapes added late in round 1 (160 x 48 Gram for k1 > 128, k2 in (32, 48];
+# 112-wide Gram / LinComb tiles for k2, d in (96, 112]) on ODD leading dimensions —
+# an arena of width sx + 2 bs is odd whenever nev is odd, and then the staged kernels
+# take their non-bulk (VEC16 / scalar cp.async) paths.
+ODD_LD_SHAPES = [(300, 40, 0), (140, 33, 0), (600, 100, 0), (200, 97, 112), (40, 8, 100)]
+
+
+def _odd_ld_case(dev, k1, k2, d, seed):
+    n = 20011
+    ld = k1 + max(k2, d) + 3
+    ld += 1 - ld % 2  # odd
+    rng = np.random.default_rng(seed)
+    arena = rng.standard_normal((n, ld))
+    A = rm(dev, arena)
+    x, y = arena[:, :k1], arena[:, k1:k1 + k2]
+    g = dev.empty(k1, k2)
+    D.gram(dev, A[:, :k1], A[:, k1:k1 + k2], g)
+    scale = np.sqrt((x * x).sum(0)).max() * np.sqrt((y * y).sum(0)).max()
+    assert np.abs(host(g) - x.T @ y).max() / scale <= 1e-13
+    if d:
+        c = rng.standard_normal((k1, d))
+        out = dev.empty(n, d)
+        D.lincomb(dev, A[:, :k1], rm(dev, c), out)
+        assert rel_err(host(out), x @ c) <= 1e-13
+        dd = min(k1, d)
+        D.lincomb(dev, A[:, 1:1 + k1], rm(dev, c[:, :dd]), A[:, 1:1 + dd])  # odd offset, in place
+        assert rel_err(host(A[:, 1:1 + dd]), arena[:, 1:1 + k1] @ c[:, :dd]) <= 1e-13
+
+
+@pytest.mark.parametrize("k1,k2,d", ODD_LD_SHAPES)
+def test_gram_lincomb_new_tiles_odd_ld(dev, k1, k2, d):
+    _odd_ld_case(dev, k1, k2, d, k1 * 7 + k2)
+
+
+def test_gram_lincomb_new_tiles_odd_ld_without_bulk_copies():
+    """Same shapes with GCG_GRAM_BULK=0 / GCG_LINCOMB_BULK=0 (switches read once per
+    process, so in a subprocess): the cp.async staging paths."""
+    import subprocess
+    import sys
+
+    code = ("import tests.test_gpu_kernels as T\n"
+            "from paper_2111_06552_b200 import device as D\n"
+            "dev = D.default_context()\n"
+            "for i, (k1, k2, d) in enumerate(T.ODD_LD_SHAPES):\n"
+            "    T._odd_ld_case(dev, k1, k2, d, 100 + i)\n"
+            "print('ok')\n")
+    env = dict(os.environ, GCG_GRAM_BULK="0", GCG_LINCOMB_BULK="0")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=ROOT, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
