@@ -6,19 +6,27 @@
 //
 // B200 design.  The reference compacts the still-active columns every sweep
 // (gather copies, cg.py:67-71).  Here all k columns stay in place and
-// per-column flags live on the device: the SpMM is done on the full row-major
-// block (an active subset costs the same HBM sectors as the whole row run),
-// the p'q and ||r||^2 reductions are fused into the SpMM / update epilogues,
-// and the scalar recurrences (alpha, beta, stop/freeze flags) are folded into
-// the prologues of the two vector-update kernels — two launches after the SpMM
-// per sweep, no separate finish kernels.  No host sync
-// happens inside the solve: once every column has stopped, a device flag turns
-// the remaining launches into no-ops and the sweep count is read back lazily
-// by the caller.  Per sweep HBM traffic ~ SpMM + 24nk (r -= alpha q) + 40nk
-// (x += alpha p, p = r + beta p).
+// per-column flags live on the device, and a sweep is TWO kernels:
+//
+//   1. the fused sweep SpMM (spmm.cu, CG mode) gathers r and, from own-row values,
+//      applies the previous sweep's x += alpha p, forms p = r + beta p and
+//      q = (A + shift) r + beta q — which equals (A + shift) p without gathering p
+//      (Chronopoulos-Gear) — and the p'q partials; its prologue reduces the
+//      ||r||^2 partials and takes the stop / beta decisions (cg.py:86-96);
+//   2. the r-update: prologue reduces p'q, freezes columns with p'q <= 0 or forms
+//      alpha (cg.py:73-84); body r -= alpha q and the ||r||^2 partials.
+//
+// The SpMM is bound by its L1/L2 gather stream with HBM mostly idle (round-1 ncu:
+// DRAM 24 %), so the x / p / q streams ride along in its epilogue instead of a
+// third kernel.  Per sweep HBM traffic ~ 12 nnz + 56nk (SpMM) + 24nk (r-update),
+// against SpMM + 24nk + 40nk (+8nk own-row p re-read) with a separate p/x kernel.
+// No host sync happens inside the solve: once every column has stopped, device
+// flags turn the remaining launches into no-ops, and the sweep count is read
+// back lazily by the caller.
 
 #include <stdlib.h>
 
+#include "cgstate.cuh"
 #include "common.cuh"
 
 namespace gcg {
@@ -31,26 +39,12 @@ int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, con
                       const double* W, long long ldw, double* partials, int* grid_out,
                       const int* skip);
 int spmm_grid(Ctx* c, long long n);
+int spmm_cg_sweep_launch(Ctx* c, long long n, long long nnz, const int* rowptr,
+                         const int* colidx, const double* val, int k, const double* R,
+                         double shift, double* partials, int* grid_out, const CgSweep& cg);
 int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, double* Y,
                 long long ldy);
 
-struct CgState {
-  double* rz;  // [2][k]: r'r of the current sweep at parity (sweep & 1), next at the other
-  double* rn;
-  double* rn0;
-  double* target;
-  double* alpha;
-  double* beta;
-  int* conv;
-  int* frozen;
-  int* upd;
-  int* pup;
-  int* skip;
-  int* sweeps;
-  int* nact;
-  int* ticket;
-  int* live;
-};
 
 // Fixed-order reduction of one column's per-CTA partials by a 128-thread block:
 // thread t sums partials t, t+128, ... then a fixed tree — deterministic.
@@ -81,7 +75,7 @@ __device__ void publish_active(const CgState& s, int k, int my_active, bool rese
   if (last && threadIdx.x == 0) {
     __threadfence();
     const int na = atomicAdd(s.nact, 0);
-    if (na == 0) *s.skip = 1;
+    if (na == 0) *s.skip1 = 1;
     if (reset_sweeps) *s.sweeps = 0;
     *s.nact = 0;
     *s.ticket = 0;
@@ -104,50 +98,21 @@ __global__ void cg_init_fin(int k, const double* part, int nparts, double rel_to
     s.frozen[c] = 0;
     s.rz[c] = rr;
     s.upd[c] = 0;
-    s.pup[c] = 0;
   }
-  if (c == 0 && threadIdx.x == 0) *s.skip = 0;
-  // skip is only raised by the last block, after every block passed this point
+  if (c == 0 && threadIdx.x == 0) {
+    *s.skip1 = 0;
+    *s.skip2 = 0;
+    *s.pending = 0;
+  }
+  // skip1 is only raised by the last block, after every block passed this point
   publish_active(s, k, !cv, true);
 }
 
-// Fixed-order column sums of an nparts x k block of per-CTA partials, computed
-// redundantly by every CTA of the consumer kernel (256 threads, k <= 256): thread t
-// sums column t % k over parts t / k, t / k + L, ... (L = 256 / k), then the L
-// partials of each column are added in lane order — the same bits in every CTA
-// and run to run.  Replaces a separate 1-CTA "finish" launch per reduction.
-__device__ void cta_column_sums(const double* part, int nparts, int k, double* sm, double* out) {
-  const int L = blockDim.x / k;
-  const int c = threadIdx.x % k, l = threadIdx.x / k;
-  double v = 0.0;
-  if (l < L) {
-    // 8 independent loads in flight per round, added in index order
-    constexpr int U = 8;
-    int b = l;
-    for (; b + (U - 1) * L < nparts; b += U * L) {
-      double t[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) t[u] = part[(long long)(b + u * L) * k + c];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v += t[u];
-    }
-    for (; b < nparts; b += L) v += part[(long long)b * k + c];
-  }
-  sm[threadIdx.x] = v;
-  __syncthreads();
-  if (threadIdx.x < k) {
-    double t = 0.0;
-    for (int j = 0; j < L; ++j) t += sm[j * k + threadIdx.x];
-    out[threadIdx.x] = t;
-  }
-  __syncthreads();
-}
-
 // r -= alpha q and the ||r||^2 partials, with the alpha step of the recurrence
-// (cg.py:73-84) folded in: every CTA reduces the SpMM's p'q partials itself and
-// takes the per-column decisions (freeze when p'q <= 0, else alpha = r'r / p'q);
-// CTA 0 publishes them (the only state written here; 'frozen' only ever goes
-// 0 -> 1, so a CTA reading it before or after that store decides the same).
+// (cg.py:73-84) folded in: every CTA reduces the sweep SpMM's p'q partials itself
+// and takes the per-column decisions (freeze when p'q <= 0, else alpha = r'r / p'q);
+// CTA 0 publishes them.  x += alpha p is left to the next sweep SpMM (or the final
+// copy-back): `pending` says it is owed.
 __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, double* r,
                                                         const double* __restrict__ q,
                                                         long long rows_per_cta,
@@ -156,9 +121,9 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
                                                         int* prof_skipped) {
   pdl_wait();
   pdl_trigger();
-  if (*s.skip) {
+  if (*s.skip2) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      *s.live = 0;
+      *s.skip1 = 1;  // propagate: the next sweep SpMM is a no-op too
       if (prof_skipped) *prof_skipped = 1;
     }
     return;
@@ -166,6 +131,8 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   __shared__ double sm[256];
   __shared__ double s_al[256];
   __shared__ int s_up[256];
+  __shared__ int nup;
+  if (threadIdx.x == 0) nup = 0;
   cta_column_sums(spart, nsp, k, sm, s_al);
   if (threadIdx.x < k) {
     const int cc = threadIdx.x;
@@ -182,16 +149,18 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
     }
     s_al[cc] = al;
     s_up[cc] = u;
+    if (u) atomicAdd(&nup, 1);
     if (blockIdx.x == 0) {
       s.alpha[cc] = al;
       s.upd[cc] = u;
     }
   }
+  __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *s.sweeps += 1;
-    *s.live = 1;
+    *s.pending = 1;
+    if (nup == 0) *s.skip1 = 1;  // every column froze: nothing left to sweep
   }
-  __syncthreads();
   const int kc = k;  // k <= 256 (checked by the launcher)
   const int lanes = 256 / kc;
   const int c = threadIdx.x % kc;
@@ -233,106 +202,56 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   }
 }
 
-// x += alpha p (deferred from the r-update) and p = r + beta p, with the beta step
-// (cg.py:86-96) folded in: every CTA reduces the ||r||^2 partials, tests the stop
-// criterion and forms beta; CTA 0 publishes rn, conv, beta, r'r (into the other
-// parity slot, so no CTA can read a value of this sweep's update) and raises the
-// skip flag for the following sweeps once no column is active.
-__global__ void __launch_bounds__(256) cg_pupdate_kernel(long long n, int k, double* x,
-                                                         long long ldx,
-                                                         const double* __restrict__ r, double* p,
-                                                         long long rows_per_cta,
-                                                         const double* upart, int nup, CgState s,
-                                                         int par, int* prof_skipped) {
-  pdl_wait();
-  pdl_trigger();
-  if (!*s.live) {
-    if (prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *prof_skipped = 1;
-    return;
+// After the last sweep (256 threads, one CTA): when the last r-update's stop test is
+// still owed (no sweep SpMM followed it), reduce its ||r||^2 partials exactly as the
+// sweep SpMM's prologue would and test; then the report (cg.py:98-99).
+__global__ void __launch_bounds__(256) cg_final(int k, CgState s, const double* rpart, int nrp,
+                                                int* d_sweeps, int8_t* conv, int8_t* frozen,
+                                                double* relres) {
+  __shared__ double sm[256], rr[256];
+  const int pend = *s.pending;
+  if (pend) cta_column_sums(rpart, nrp, k, sm, rr);
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double rn = s.rn[c];
+    int cv = s.conv[c];
+    if (pend && s.upd[c]) {
+      rn = sqrt(rr[c]);
+      if (rn <= s.target[c]) cv = 1;
+    }
+    const double r0 = s.rn0[c];
+    relres[c] = rn / (r0 > 0.0 ? r0 : 1.0);
+    conv[c] = (int8_t)cv;
+    frozen[c] = (int8_t)s.frozen[c];
   }
-  __shared__ double sm[256];
-  __shared__ double s_be[256], s_al[256];
-  __shared__ int s_ux[256], s_pp[256];
-  __shared__ int nact;
-  if (threadIdx.x == 0) nact = 0;
-  cta_column_sums(upart, nup, k, sm, s_be);
+  if (threadIdx.x == 0) atomicMax(d_sweeps, *s.sweeps);  // max over column chunks
+}
+
+// x_user = X + alpha P for the columns whose last x-update is still owed, else X.
+__global__ void __launch_bounds__(256) cg_xout_kernel(long long n, int k,
+                                                      const double* __restrict__ X,
+                                                      const double* __restrict__ P, double* x,
+                                                      long long ldx, long long rows_per_cta,
+                                                      CgState s) {
+  __shared__ double s_al[256];
+  __shared__ int s_use[256];
   if (threadIdx.x < k) {
-    const int cc = threadIdx.x;
-    const double rr = s_be[cc];
-    const int ux = s.upd[cc];
-    int cv = s.conv[cc], pp = 0;
-    double be = 0.0;
-    const double rzo = s.rz[par * k + cc];
-    double rzn = rzo;
-    if (ux) {
-      const double rn = sqrt(rr);
-      if (blockIdx.x == 0) s.rn[cc] = rn;
-      if (rn <= s.target[cc]) {
-        cv = 1;
-      } else {
-        be = rr / rzo;
-        rzn = rr;
-        pp = 1;
-      }
-    }
-    s_be[cc] = be;
-    s_al[cc] = s.alpha[cc];
-    s_ux[cc] = ux;
-    s_pp[cc] = pp;
-    if (blockIdx.x == 0) {
-      s.conv[cc] = cv;
-      s.beta[cc] = be;
-      s.pup[cc] = pp;
-      s.rz[(par ^ 1) * k + cc] = rzn;
-    }
-    if (!cv && !s.frozen[cc]) atomicAdd(&nact, 1);
+    const int use = *s.pending && s.upd[threadIdx.x];
+    s_use[threadIdx.x] = use;
+    s_al[threadIdx.x] = use ? s.alpha[threadIdx.x] : 0.0;
   }
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0 && nact == 0) *s.skip = 1;
   const int lanes = 256 / k;
-  const int c = threadIdx.x % k;
-  const int rl = threadIdx.x / k;
+  const int c = threadIdx.x % k, rl = threadIdx.x / k;
   if (rl >= lanes) return;
   const long long r0 = (long long)blockIdx.x * rows_per_cta;
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
-  const bool ux = s_ux[c], up = s_pp[c];
-  if (!ux && !up) return;
-  const double al = s_al[c], be = s_be[c];
-  constexpr int U = 8;
-  long long i = r0 + rl;
-  for (; i + (U - 1) * lanes < r1; i += U * lanes) {
-    double pv[U], xv[U], rv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long ii = i + u * lanes;
-      pv[u] = p[ii * k + c];
-      if (ux) xv[u] = x[ii * ldx + c];
-      if (up) rv[u] = r[ii * k + c];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long ii = i + u * lanes;
-      if (ux) x[ii * ldx + c] = fma(al, pv[u], xv[u]);
-      if (up) p[ii * k + c] = fma(be, pv[u], rv[u]);
-    }
+  const bool use = s_use[c];
+  const double al = s_al[c];
+  for (long long i = r0 + rl; i < r1; i += lanes) {
+    const double xv = X[i * k + c];
+    x[i * ldx + c] = use ? fma(al, P[i * k + c], xv) : xv;
   }
-  for (; i < r1; i += lanes) {
-    const double pv = p[i * k + c];
-    if (ux) x[i * ldx + c] = fma(al, pv, x[i * ldx + c]);
-    if (up) p[i * k + c] = fma(be, pv, r[i * k + c]);
-  }
-}
-
-__global__ void cg_final(int k, CgState s, int* d_sweeps, int8_t* conv, int8_t* frozen,
-                         double* relres) {
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    const double r0 = s.rn0[c];
-    relres[c] = s.rn[c] / (r0 > 0.0 ? r0 : 1.0);
-    conv[c] = (int8_t)s.conv[c];
-    frozen[c] = (int8_t)s.frozen[c];
-  }
-  if (threadIdx.x == 0) atomicMax(d_sweeps, *s.sweeps);  // max over column chunks
 }
 
 int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
@@ -404,27 +323,26 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   ugrid = (int)((n + rpc - 1) / rpc);
   const int nparts_max = sgrid > ugrid ? sgrid : ugrid;
   const long long nghost = dist ? dist->nghost : 0;
-  // workspace: R, Q (n x k), P and X ((n + ghosts) x k) + partials + state.  The
-  // iterate lives in the dense X (ld = k) during the sweeps — a strided arena view
-  // streams noticeably slower — and is copied back into x at the end.
-  // block starts kept 32-byte aligned so the SpMM can gather rows with 256-bit loads
+  // workspace: R and X ((n + ghosts) x k: both are gathered by an SpMM), P, Q (n x k)
+  // + partials + state.  The iterate lives in the dense X (ld = k) during the sweeps —
+  // a strided arena view streams noticeably slower — and is copied back into x at the
+  // end.  Block starts kept 32-byte aligned so the SpMM can gather rows with 256-bit
+  // loads.
   const size_t vec = ((size_t)n * k + 3) & ~(size_t)3;
   const size_t pvec = ((size_t)(n + nghost) * k + 3) & ~(size_t)3;
   const size_t bytes =
       sizeof(double) * (2 * vec + 2 * pvec + 2 * (size_t)nparts_max * k + 7 * (size_t)k) +
-      sizeof(int) * (4 * (size_t)k + 5) + 256;
+      sizeof(int) * (3 * (size_t)k + 8) + 256;
   GCG_TRY(ensure(c->cg, bytes));
   double* R = (double*)c->cg.ptr;
-  double* Q = R + vec;
+  double* Xc = R + pvec;
+  double* Q = Xc + pvec;
   double* P = Q + vec;
-  double* Xc = P + pvec;
-  double* part = Xc + pvec;
+  double* part = P + vec;
   double* const x_user = x;
   const long long ldx_user = ldx;
   // initial guess: x0 when given (the caller's X block), else the iterate's own input
   GCG_TRY(copy_launch(c, n, k, x0 ? x0 : x_user, x0 ? ldx0 : ldx_user, Xc, k));
-  x = Xc;
-  ldx = k;
   double* upart = part + (size_t)nparts_max * k;  // r-update partials (SpMM's stay readable)
   double* sd = upart + (size_t)nparts_max * k;
   CgState s;
@@ -433,24 +351,22 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   s.rn0 = sd + 3 * k;
   s.target = sd + 4 * k;
   s.alpha = sd + 5 * k;
-  s.beta = sd + 6 * k;
   int* si = (int*)(sd + 7 * k);
   s.conv = si;
   s.frozen = si + k;
   s.upd = si + 2 * k;
-  s.pup = si + 3 * k;
-  s.skip = si + 4 * k;
-  s.sweeps = si + 4 * k + 1;
-  s.nact = si + 4 * k + 2;
-  s.ticket = si + 4 * k + 3;
-  s.live = si + 4 * k + 4;
-  GCG_TRY(cuda_status(cudaMemsetAsync(s.skip, 0, 5 * sizeof(int), c->stream)));
-  const int fin_threads = k < 32 ? 32 : (k + 31) / 32 * 32;
+  s.skip1 = si + 3 * k;
+  s.skip2 = si + 3 * k + 1;
+  s.pending = si + 3 * k + 2;
+  s.sweeps = si + 3 * k + 3;
+  s.nact = si + 3 * k + 4;
+  s.ticket = si + 3 * k + 5;
+  GCG_TRY(cuda_status(cudaMemsetAsync(s.skip1, 0, 6 * sizeof(int), c->stream)));
 
   // r = rhs - op(x) = -(A x) - shift*x + rhs ; ||r0||^2 partials
   int g = 0;
-  if (dist) GCG_TRY(dist_halo(c, dist, n, k, x, ldx));
-  GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, x, ldx, -1.0, -shift, x, ldx, 1.0,
+  if (dist) GCG_TRY(dist_halo(c, dist, n, k, Xc, k));
+  GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, Xc, k, -1.0, -shift, Xc, k, 1.0,
                             rhs, ldr, R, k, 2, nullptr, 0, part, &g, nullptr));
   const double* red = part;
   int nred = g;
@@ -462,11 +378,22 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   cg_init_fin<<<k, 128, 0, c->stream>>>(k, red, nred, rel_tol, s);
   ++g_launches;
   GCG_CHECK_LAUNCH();
-  GCG_TRY(copy_launch(c, n, k, R, k, P, k));
+  const double* rred = nullptr;  // ||r||^2 partials of the last r-update
+  int nrred = 0;
   for (int it = 0; it < max_iters; ++it) {
-    if (dist) GCG_TRY(dist_halo(c, dist, n, k, P, k));
-    GCG_TRY(spmm_launch_parts(c, n, nnz, rowptr, colidx, val, k, P, k, 1.0, shift, P, k, 0.0,
-                              nullptr, 0, Q, k, 1, P, k, part, &g, s.skip));
+    // sweep SpMM: x += alpha p (owed), p = r + beta p, q = (A + shift) r + beta q, p'q
+    if (dist) GCG_TRY(dist_halo(c, dist, n, k, R, k));
+    CgSweep sw;
+    sw.s = s;
+    sw.rpart = rred;
+    sw.nrp = nrred;
+    sw.k = k;
+    sw.par = it & 1;
+    sw.first = it == 0;
+    sw.x = Xc;
+    sw.P = P;
+    sw.Q = Q;
+    GCG_TRY(spmm_cg_sweep_launch(c, n, nnz, rowptr, colidx, val, k, R, shift, part, &g, sw));
     red = part;
     nred = g;
     if (dist) {
@@ -474,27 +401,27 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       red = dist->red_buf;
       nred = 1;
     }
-    int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
+    // r-update: alpha = r'r / p'q (freeze on p'q <= 0), r -= alpha q, ||r||^2 partials
+    const int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
     pdl_launch(cg_update_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, R, (const double*)Q,
-               (long long)rpc, red, nred, upart, s, it & 1, prof_skip_slot(c, ps));
+               (long long)rpc, red, nred, upart, s, (it & 1) ^ 1, prof_skip_slot(c, ps));
     prof_stop(c, ps);
-    red = upart;
-    nred = ugrid;
+    ++g_launches;
+    GCG_CHECK_LAUNCH();
+    rred = upart;
+    nrred = ugrid;
     if (dist) {
       GCG_TRY(dist_reduce(c, dist, upart, ugrid, k));
-      red = dist->red_buf;
-      nred = 1;
+      rred = dist->red_buf;
+      nrred = 1;
     }
-    ps = prof_start(c, PROF_CG_PUPDATE, 40.0 * n * k);
-    pdl_launch(cg_pupdate_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, x, (long long)ldx,
-               (const double*)R, P, (long long)rpc, red, nred, s, it & 1, prof_skip_slot(c, ps));
-    prof_stop(c, ps);
-    g_launches += 2;
-    GCG_CHECK_LAUNCH();
   }
-  GCG_TRY(copy_launch(c, n, k, Xc, k, x_user, ldx_user));
-  cg_final<<<1, fin_threads, 0, c->stream>>>(k, s, d_sweeps, d_conv, d_frozen, d_relres);
-  ++g_launches;
+  const int ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
+  cg_xout_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, Xc, P, x_user, ldx_user, (long long)rpc, s);
+  prof_stop(c, ps);
+  cg_final<<<1, 256, 0, c->stream>>>(k, s, rred ? rred : part, rred ? nrred : 0, d_sweeps, d_conv,
+                                     d_frozen, d_relres);
+  g_launches += 2;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
 }

@@ -37,6 +37,7 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <vector>
 
+#include "cgstate.cuh"
 #include "common.cuh"
 
 namespace gcg {
@@ -68,6 +69,7 @@ struct SpmmArgs {
   int pld;
   const int* skip;    // device flag: nonzero -> kernel is a no-op (CG early exit)
   int* prof_skipped;  // profiling: set when the launch was a no-op
+  int c0;             // first column of this pass (CG mode: index of the per-column state)
 };
 
 template <int VEC>
@@ -137,12 +139,27 @@ __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
   return doubles > 0 ? 4 : 4;  // every shape: 64 registers, one grid size
 }
 
-template <int VEC, int NV, bool SELF>
+// CG = true: the fused block-CG sweep (cgstate.cuh CgSweep; X is the residual block
+// r, dense ld = cg.k).  Prologue: every CTA reduces the previous r-update's ||r||^2
+// partials in fixed order and takes the per-column decisions of cg.py:86-96 (stop
+// test, beta); CTA 0 publishes them.  Epilogue, from own-row values only:
+// x += alpha p (the previous sweep's deferred x-update), p = r + beta p,
+// q = (A + shift) r + beta q  ( = (A + shift) p, the Chronopoulos-Gear recurrence:
+// no second gather of p), and the p'q partials for the next r-update.
+template <int VEC, int NV, bool SELF, bool CG>
 __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
-    spmm_csr_kernel(SpmmArgs a) {
+    spmm_csr_kernel(SpmmArgs a, CgSweep cg) {
   pdl_wait();
   pdl_trigger();
-  if (a.skip != nullptr && *a.skip) {
+  if constexpr (CG) {
+    if (*cg.s.skip1) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *cg.s.skip2 = 1;  // propagate: the r-update of this sweep is a no-op too
+        if (a.prof_skipped) *a.prof_skipped = 1;
+      }
+      return;
+    }
+  } else if (a.skip != nullptr && *a.skip) {
     if (a.prof_skipped && blockIdx.x == 0 && threadIdx.x == 0) *a.prof_skipped = 1;
     return;
   }
@@ -180,6 +197,49 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
   if (a.dot_mode) {
 #pragma unroll
     for (int q = 0; q < NV * VEC; ++q) sacc[warp][q][lane] = 0.0;
+  }
+  constexpr int CGN = CG ? kSpmmMaxPass : 1;
+  __shared__ double cg_be[CGN], cg_al[CGN], cg_sm[CGN];
+  __shared__ int cg_fl[CGN];  // bit 0: p/q update (active), bit 1: deferred x-update
+  __shared__ int cg_nact;
+  if constexpr (CG) {
+    const int K = cg.k;
+    if (threadIdx.x == 0) cg_nact = 0;
+    if (!cg.first) cta_column_sums(cg.rpart, cg.nrp, K, cg_sm, cg_be);
+    else __syncthreads();
+    if (threadIdx.x < K) {
+      const int cc = threadIdx.x;
+      int pp = 0, ux = 0;
+      double be = 0.0, al = 0.0;
+      const double rzo = cg.s.rz[cg.par * K + cc];
+      double rzn = rzo;
+      if (cg.first) {
+        pp = !cg.s.conv[cc] && !cg.s.frozen[cc];
+      } else if (cg.s.upd[cc]) {
+        ux = 1;
+        al = cg.s.alpha[cc];
+        const double rr = cg_be[cc];
+        const double rn = sqrt(rr);
+        if (blockIdx.x == 0) cg.s.rn[cc] = rn;
+        if (rn <= cg.s.target[cc]) {
+          if (blockIdx.x == 0) cg.s.conv[cc] = 1;
+        } else {
+          be = rr / rzo;
+          rzn = rr;
+          pp = 1;
+        }
+      }
+      if (blockIdx.x == 0) cg.s.rz[(cg.par ^ 1) * K + cc] = rzn;
+      cg_be[cc] = be;
+      cg_al[cc] = al;
+      cg_fl[cc] = pp | (ux << 1);
+      if (pp) atomicAdd(&cg_nact, 1);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *cg.s.pending = 0;
+      if (cg_nact == 0) *cg.s.skip2 = 1;
+    }
   }
 
   // prefetched state of the row this lane group handles next
@@ -290,7 +350,79 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
       }
     }
-    if (active && r < rend) {
+    if constexpr (CG) {
+      if (active && r < rend) {
+        auto ldv = [&](const double* p, double* o) {
+          if (a.vepi) {
+            VecT<VEC>::ld(p, o);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) o[e] = p[e];
+          }
+        };
+        auto stv = [&](double* p, const double* o) {
+          if (a.vepi) {
+            VecT<VEC>::st(p, o);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) p[e] = o[e];
+          }
+        };
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const int c = (q * LPR + sub) * VEC;
+          if (c >= k) continue;
+          const int gc = a.c0 + c;  // passes keep k % VEC == 0: every e is a column
+          double rv[VEC], y[VEC];
+          ldv(a.X + r * a.ldx + c, rv);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(a.gamma, rv[e], acc[q][e]);
+          int fl[VEC];
+          bool anyp = false, anyx = false;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            fl[e] = cg_fl[gc + e];
+            anyp |= (fl[e] & 1) != 0;
+            anyx |= (fl[e] & 2) != 0;
+          }
+          const long long o = r * (long long)cg.k + gc;
+          if (cg.first) {
+            stv(cg.P + o, rv);  // p = r, q = (A + shift) r for every column (keeps P finite)
+            stv(cg.Q + o, y);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (fl[e] & 1)
+                sacc[warp][q * VEC + e][lane] = fma(rv[e], y[e], sacc[warp][q * VEC + e][lane]);
+          } else if (anyp || anyx) {
+            double pv[VEC];
+            ldv(cg.P + o, pv);
+            if (anyx) {
+              double xv[VEC];
+              ldv(cg.x + o, xv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e)
+                if (fl[e] & 2) xv[e] = fma(cg_al[gc + e], pv[e], xv[e]);
+              stv(cg.x + o, xv);
+            }
+            if (anyp) {
+              double qv[VEC];
+              ldv(cg.Q + o, qv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                if (fl[e] & 1) {
+                  const double be = cg_be[gc + e];
+                  pv[e] = fma(be, pv[e], rv[e]);
+                  qv[e] = fma(be, qv[e], y[e]);
+                  sacc[warp][q * VEC + e][lane] = fma(pv[e], qv[e], sacc[warp][q * VEC + e][lane]);
+                }
+              }
+              stv(cg.P + o, pv);
+              stv(cg.Q + o, qv);
+            }
+          }
+        }
+      }
+    } else if (active && r < rend) {
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         const int c = (q * LPR + sub) * VEC;
@@ -401,35 +533,43 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
 }
 
 template <int VEC, int NV>
-static void launch_one(Ctx* c, const SpmmArgs& a, int grid) {
+static void launch_one(Ctx* c, const SpmmArgs& a, int grid, const CgSweep* cg) {
+  if (cg) {
+    pdl_launch(spmm_csr_kernel<VEC, NV, false, true>, dim3(grid), dim3(kSpmmThreads), 0,
+               c->stream, a, *cg);
+    return;
+  }
   // the CG forms (shift and/or dot against X itself, same ld): own row from the gathers
   static const bool self_env = getenv("GCG_SPMM_SELF") ? atoi(getenv("GCG_SPMM_SELF")) != 0 : false;
   const bool self = self_env && ((a.gamma != 0.0 && a.Z == a.X && a.ldz == a.ldx) ||
                                  (a.dot_mode == 1 && a.W == a.X && a.ldw == a.ldx));
+  const CgSweep none = {};
   if (self)
-    pdl_launch(spmm_csr_kernel<VEC, NV, true>, dim3(grid), dim3(kSpmmThreads), 0, c->stream, a);
+    pdl_launch(spmm_csr_kernel<VEC, NV, true, false>, dim3(grid), dim3(kSpmmThreads), 0,
+               c->stream, a, none);
   else
-    pdl_launch(spmm_csr_kernel<VEC, NV, false>, dim3(grid), dim3(kSpmmThreads), 0, c->stream, a);
+    pdl_launch(spmm_csr_kernel<VEC, NV, false, false>, dim3(grid), dim3(kSpmmThreads), 0,
+               c->stream, a, none);
 }
 
 template <int VEC>
-static void launch_vec(Ctx* c, const SpmmArgs& a, int nv, int grid) {
+static void launch_vec(Ctx* c, const SpmmArgs& a, int nv, int grid, const CgSweep* cg) {
   if constexpr (VEC == 4) {
-    if (nv == 1) launch_one<4, 1>(c, a, grid);
-    else launch_one<4, 2>(c, a, grid);
+    if (nv == 1) launch_one<4, 1>(c, a, grid, cg);
+    else launch_one<4, 2>(c, a, grid, cg);
   } else if constexpr (VEC == 2) {
     switch (nv) {
-      case 1: launch_one<2, 1>(c, a, grid); break;
-      case 2: launch_one<2, 2>(c, a, grid); break;
-      case 3: launch_one<2, 3>(c, a, grid); break;
-      default: launch_one<2, 4>(c, a, grid); break;
+      case 1: launch_one<2, 1>(c, a, grid, cg); break;
+      case 2: launch_one<2, 2>(c, a, grid, cg); break;
+      case 3: launch_one<2, 3>(c, a, grid, cg); break;
+      default: launch_one<2, 4>(c, a, grid, cg); break;
     }
   } else {
     switch (nv) {
-      case 1: launch_one<1, 1>(c, a, grid); break;
-      case 2: launch_one<1, 2>(c, a, grid); break;
-      case 3: launch_one<1, 3>(c, a, grid); break;
-      default: launch_one<1, 4>(c, a, grid); break;
+      case 1: launch_one<1, 1>(c, a, grid, cg); break;
+      case 2: launch_one<1, 2>(c, a, grid, cg); break;
+      case 3: launch_one<1, 3>(c, a, grid, cg); break;
+      default: launch_one<1, 4>(c, a, grid, cg); break;
     }
   }
 }
@@ -468,12 +608,13 @@ static double spmm_shape(int chunks, int vec, int* nv_out, int* lpr_out) {
 // One SpMM over all k columns, in even passes of at most 256 columns.  With
 // dot_mode != 0 and `partials` given, per-CTA partials ([grid][k]) are left for
 // the caller to reduce; otherwise they are reduced into `dots` per pass.
-int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
-                     const double* val, int k, const double* X, long long ldx, double alpha,
-                     double gamma, const double* Z, long long ldz, double beta, const double* Yin,
-                     long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
-                     long long ldw, double* dots, double* partials_ext, int* grid_out,
-                     const int* skip) {
+static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowptr,
+                            const int* colidx, const double* val, int k, const double* X,
+                            long long ldx, double alpha, double gamma, const double* Z,
+                            long long ldz, double beta, const double* Yin, long long ldyin,
+                            double* Y, long long ldy, int dot_mode, const double* W,
+                            long long ldw, double* dots, double* partials_ext, int* grid_out,
+                            const int* skip, const CgSweep* cg) {
   if (n <= 0 || k <= 0) return GCG_OK;
   double* partials = partials_ext;
   if (dot_mode && !partials) {
@@ -557,6 +698,7 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     a.partials = partials_ext ? partials + c0 : partials;
     a.pld = partials_ext ? k : kc;
     a.skip = skip;
+    a.c0 = c0;
     const int vb = 8 * vec;
     a.vepi = aligned_to(a.Y, vb) && ldy % vec == 0 &&
              (gamma == 0.0 || (aligned_to(a.Z, vb) && ldz % vec == 0)) &&
@@ -567,12 +709,15 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     if (gamma != 0.0 && Z != X) bytes += 8.0 * n * kc;
     if (beta != 0.0) bytes += 8.0 * n * kc;
     if (dot_mode == 1 && W != X && W != Z) bytes += 8.0 * n * kc;
+    // fused CG sweep: r once (gather) + p, q written (first sweep) / + p, q, x read and
+    // written (later sweeps)
+    if (cg) bytes = 12.0 * nnz + 4.0 * (n + 1) + (cg->first ? 24.0 : 56.0) * n * kc;
     const int ps = prof_start(c, PROF_SPMM, bytes);
     a.prof_skipped = prof_skip_slot(c, ps);
     switch (vec) {
-      case 4: launch_vec<4>(c, a, nv, grid); break;
-      case 2: launch_vec<2>(c, a, nv, grid); break;
-      default: launch_vec<1>(c, a, nv, grid); break;
+      case 4: launch_vec<4>(c, a, nv, grid, cg); break;
+      case 2: launch_vec<2>(c, a, nv, grid, cg); break;
+      default: launch_vec<1>(c, a, nv, grid, cg); break;
     }
     ++g_launches;
     GCG_CHECK_LAUNCH();
@@ -584,6 +729,26 @@ int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, cons
     c0 += kc;
   }
   return GCG_OK;
+}
+
+int spmm_launch_impl(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,
+                     const double* val, int k, const double* X, long long ldx, double alpha,
+                     double gamma, const double* Z, long long ldz, double beta, const double* Yin,
+                     long long ldyin, double* Y, long long ldy, int dot_mode, const double* W,
+                     long long ldw, double* dots, double* partials_ext, int* grid_out,
+                     const int* skip) {
+  return spmm_launch_core(c, n, nnz, rowptr, colidx, val, k, X, ldx, alpha, gamma, Z, ldz, beta,
+                          Yin, ldyin, Y, ldy, dot_mode, W, ldw, dots, partials_ext, grid_out, skip,
+                          nullptr);
+}
+
+// The fused block-CG sweep over the dense n x k residual block R (ld k): see the CG
+// mode of spmm_csr_kernel.  p'q partials ([grid][k]) are left in `partials`.
+int spmm_cg_sweep_launch(Ctx* c, long long n, long long nnz, const int* rowptr,
+                         const int* colidx, const double* val, int k, const double* R,
+                         double shift, double* partials, int* grid_out, const CgSweep& cg) {
+  return spmm_launch_core(c, n, nnz, rowptr, colidx, val, k, R, k, 1.0, shift, R, k, 0.0, nullptr,
+                          0, cg.Q, k, 1, cg.P, k, nullptr, partials, grid_out, nullptr, &cg);
 }
 
 int spmm_launch_parts(Ctx* c, long long n, long long nnz, const int* rowptr, const int* colidx,

@@ -40,6 +40,33 @@ def _gram_defect(x, b=None):
     return float(np.abs(x.T @ bx - np.eye(x.shape[1])).max())
 
 
+def _span_sin(got, want, b=None):
+    """sin of the largest principal angle between span(got) and span(want), both
+    B-orthonormal: ||(I - W W'B) G||_B."""
+    bg = got if b is None else b @ got
+    y = got - want @ (want.T @ bg)
+    by = y if b is None else b @ y
+    return float(np.sqrt(max(0.0, np.linalg.eigvalsh(y.T @ by).max())))
+
+
+def _blocks_match(got, want, b=None, tol=1e-12, leaf=16):
+    """Equal blocks where the SVQB output is determined; equal spans where it is not.
+
+    A repeat SVQB pass (orth.py:168-175) factors a Gram matrix that is already I to
+    ~1e-15: its eigenvectors — hence the output basis of that leaf — are an arbitrary
+    rotation inside the (numerically) degenerate eigenspace, so two correct
+    implementations agree on the leaf's span (and on everything the solver uses: the
+    iteration depends only on span(V)), not on its columns.  Leaf by
+    leaf, spans of the nested prefixes must agree."""
+    k = got.shape[1]
+    if np.abs(got - want).max() <= tol:
+        return True
+    for j in sorted(set(list(range(leaf, k, leaf)) + [k])):
+        if _span_sin(got[:, :j], want[:, :j], b) > 1e3 * tol:
+            return False
+    return True
+
+
 @pytest.fixture(params=["native", "python"])
 def driver(request):
     saved = OR._NATIVE
@@ -57,7 +84,10 @@ def test_recursive_orth_matches_reference(dev, golden, driver, tag, tol):
     assert (out.num_kept, out.reduction_count) == (kept, red) == (32, 7 if tag == "strict" else 5)
     assert out.replaced_indices == []
     got = x.cpu().numpy()
-    assert np.abs(got - golden[f"orth_{tag}_out"]).max() <= 1e-12
+    want = golden[f"orth_{tag}_out"]
+    if tag == "default":  # every leaf stops after its second Gram check: columns determined
+        assert np.abs(got - want).max() <= 1e-12
+    assert _blocks_match(got, want)
     assert _gram_defect(got) <= 1e-12 if tag == "strict" else _gram_defect(got) <= 1e-10
 
 
@@ -118,7 +148,7 @@ def test_recursive_orth_dependent_and_b(dev, driver, use_b):
         (rr.num_kept, rr.reduction_count, list(rr.replaced_indices))
     k = out.num_kept
     got = x.cpu().numpy()[:, :k]
-    assert np.abs(got - ref[:, :k]).max() <= 1e-10
+    assert _blocks_match(got, ref[:, :k], bs, tol=1e-12)
     assert _gram_defect(got, bs) <= 1e-9
 
 
