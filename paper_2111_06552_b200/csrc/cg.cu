@@ -108,6 +108,9 @@ __global__ void cg_init_fin(int k, const double* part, int nparts, double rel_to
   publish_active(s, k, !cv, true);
 }
 
+__constant__ int c_prefetch_upd = 0;
+__device__ __forceinline__ bool prefetch_upd() { return c_prefetch_upd != 0; }
+
 // r -= alpha q and the ||r||^2 partials, with the alpha step of the recurrence
 // (cg.py:73-84) folded in: every CTA reduces the sweep SpMM's p'q partials itself
 // and takes the per-column decisions (freeze when p'q <= 0, else alpha = r'r / p'q);
@@ -119,6 +122,18 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
                                                         const double* spart, int nsp,
                                                         double* part, CgState s, int par,
                                                         int* prof_skipped) {
+  // Pull this CTA's r and q rows into L2 while the sweep SpMM drains and the p'q
+  // partials are reduced (L2 is the point of coherence, so prefetching lines the
+  // predecessor is still writing is safe).
+  if (prefetch_upd()) {
+    const long long b0 = (long long)blockIdx.x * rows_per_cta * k;
+    long long b1 = b0 + rows_per_cta * k;
+    if (b1 > n * k) b1 = n * k;
+    for (long long e = b0 + threadIdx.x * 16; e < b1; e += 256 * 16) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(r + e));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(q + e));
+    }
+  }
   pdl_wait();
   pdl_trigger();
   if (*s.skip2) {
@@ -272,6 +287,11 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
                     double rel_tol, int* d_sweeps, int8_t* d_conv, int8_t* d_frozen,
                     double* d_relres, const gcg_cg_dist* dist) {
   if (k <= 0 || n <= 0) return GCG_ERR_ARG;
+  static const bool pf_set = [] {
+    const int v = getenv("GCG_CG_UPD_PREFETCH") ? atoi(getenv("GCG_CG_UPD_PREFETCH")) : 0;
+    return cudaMemcpyToSymbol(c_prefetch_upd, &v, sizeof(int)) == cudaSuccess;
+  }();
+  (void)pf_set;
   GCG_TRY(cuda_status(cudaMemsetAsync(d_sweeps, 0, sizeof(int), c->stream)));
   static const char* env = getenv("GCG_CG_CHUNK");
   int kc = env ? atoi(env) : k;
@@ -416,7 +436,7 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       nrred = 1;
     }
   }
-  const int ps = prof_start(c, PROF_CG_PUPDATE, 24.0 * n * k);
+  const int ps = prof_start(c, PROF_CG_XOUT, 24.0 * n * k);
   cg_xout_kernel<<<ugrid, 256, 0, c->stream>>>(n, k, Xc, P, x_user, ldx_user, (long long)rpc, s);
   prof_stop(c, ps);
   cg_final<<<1, 256, 0, c->stream>>>(k, s, rred ? rred : part, rred ? nrred : 0, d_sweeps, d_conv,

@@ -70,18 +70,33 @@ struct SpmmArgs {
   const int* skip;    // device flag: nonzero -> kernel is a no-op (CG early exit)
   int* prof_skipped;  // profiling: set when the launch was a no-op
   int c0;             // first column of this pass (CG mode: index of the per-column state)
+  int cg_prefetch;    // CG mode: L2-prefetch the next row step's p, q, x
 };
 
 template <int VEC>
 struct VecT;
 template <>
 struct VecT<1> {
+  static __device__ __forceinline__ void ld_stream(const double* p, double* o) {
+    long long a;
+    asm volatile("ld.global.L1::no_allocate.b64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");
+    o[0] = __longlong_as_double(a);
+  }
   static __device__ __forceinline__ void load(const double* p, double* o) { o[0] = __ldg(p); }
   static __device__ __forceinline__ void ld(const double* p, double* o) { o[0] = *p; }
   static __device__ __forceinline__ void st(double* p, const double* o) { *p = o[0]; }
 };
 template <>
 struct VecT<2> {
+  static __device__ __forceinline__ void ld_stream(const double* p, double* o) {
+    long long a, b;
+    asm volatile("ld.global.L1::no_allocate.v2.b64 {%0,%1}, [%2];"
+                 : "=l"(a), "=l"(b)
+                 : "l"(p)
+                 : "memory");
+    o[0] = __longlong_as_double(a);
+    o[1] = __longlong_as_double(b);
+  }
   static __device__ __forceinline__ void load(const double* p, double* o) {
     const double2 v = __ldg(reinterpret_cast<const double2*>(p));
     o[0] = v.x;
@@ -123,6 +138,18 @@ struct VecT<4> {
     o[2] = __longlong_as_double(c);
     o[3] = __longlong_as_double(d);
   }
+  // streaming own-row load that does not allocate in L1 (keeps L1 for the gathers)
+  static __device__ __forceinline__ void ld_stream(const double* p, double* o) {
+    long long a, b, c, d;
+    asm volatile("ld.global.L1::no_allocate.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p)
+                 : "memory");
+    o[0] = __longlong_as_double(a);
+    o[1] = __longlong_as_double(b);
+    o[2] = __longlong_as_double(c);
+    o[3] = __longlong_as_double(d);
+  }
   static __device__ __forceinline__ void st(double* p, const double* o) {
     asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(__double_as_longlong(o[0])),
                  "l"(__double_as_longlong(o[1])), "l"(__double_as_longlong(o[2])),
@@ -146,9 +173,13 @@ __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
 // x += alpha p (the previous sweep's deferred x-update), p = r + beta p,
 // q = (A + shift) r + beta q  ( = (A + shift) p, the Chronopoulos-Gear recurrence:
 // no second gather of p), and the p'q partials for the next r-update.
-template <int VEC, int NV, bool SELF, bool CG>
-__global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
+// CGM: 0 = plain SpMM, 1 = CG sweep at 4 CTAs / SM (64 registers), 2 = CG sweep at
+// 3 CTAs / SM (80 registers: the fused epilogue's values no longer spill the gather
+// pipeline's state)
+template <int VEC, int NV, bool SELF, int CGM>
+__global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(VEC* NV))
     spmm_csr_kernel(SpmmArgs a, CgSweep cg) {
+  constexpr bool CG = CGM != 0;
   pdl_wait();
   pdl_trigger();
   if constexpr (CG) {
@@ -198,6 +229,13 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
 #pragma unroll
     for (int q = 0; q < NV * VEC; ++q) sacc[warp][q][lane] = 0.0;
   }
+  // CG mode: the p'q accumulators stay in registers (one shared-memory store at the
+  // end) — per-row shared read-modify-writes doubled the L1 wavefronts of the sweep
+  double dacc[CG ? NV : 1][CG ? VEC : 1];
+#pragma unroll
+  for (int q = 0; q < (CG ? NV : 1); ++q)
+#pragma unroll
+    for (int e = 0; e < (CG ? VEC : 1); ++e) dacc[q][e] = 0.0;
   constexpr int CGN = CG ? kSpmmMaxPass : 1;
   __shared__ double cg_be[CGN], cg_al[CGN], cg_sm[CGN];
   __shared__ int cg_fl[CGN];  // bit 0: p/q update (active), bit 1: deferred x-update
@@ -288,6 +326,30 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
     nlen = plen;
     if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
     if (rbn + stride < rend) fetch_rowptr(rbn + stride, pstart, plen);
+    if constexpr (CG) {
+      // the next step's own-row streams (p, q, x) into L2 while this step gathers, so
+      // the epilogue's loads are L2 hits instead of exposed HBM latency
+      static_assert(CGM >= 0, "");
+      const long long rp = rb + (a.cg_prefetch == 2 ? 2 : 1) * stride + g;
+      if (a.cg_prefetch && !cg.first && active && rp < rend) {
+        const long long o = rp * (long long)cg.k + a.c0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const int c = (q * LPR + sub) * VEC;
+          if (c < k) {
+            if (a.cg_prefetch == 3) {
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(cg.P + o + c));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(cg.Q + o + c));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(cg.x + o + c));
+            } else {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(cg.P + o + c));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(cg.Q + o + c));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(cg.x + o + c));
+            }
+          }
+        }
+      }
+    }
     const int maxlen = __reduce_max_sync(FULL, len);
     // SELF (Z and/or W are X itself): keep the row's own X values from the
     // diagonal gather instead of re-reading them in the epilogue
@@ -360,6 +422,14 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             for (int e = 0; e < VEC; ++e) o[e] = p[e];
           }
         };
+        auto lds = [&](const double* p, double* o) {  // p, q, x: read once, bypass L1
+          if (a.vepi) {
+            VecT<VEC>::ld_stream(p, o);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) o[e] = p[e];
+          }
+        };
         auto stv = [&](double* p, const double* o) {
           if (a.vepi) {
             VecT<VEC>::st(p, o);
@@ -391,14 +461,13 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             stv(cg.Q + o, y);
 #pragma unroll
             for (int e = 0; e < VEC; ++e)
-              if (fl[e] & 1)
-                sacc[warp][q * VEC + e][lane] = fma(rv[e], y[e], sacc[warp][q * VEC + e][lane]);
+              if (fl[e] & 1) dacc[CG ? q : 0][CG ? e : 0] = fma(rv[e], y[e], dacc[CG ? q : 0][CG ? e : 0]);
           } else if (anyp || anyx) {
             double pv[VEC];
-            ldv(cg.P + o, pv);
+            lds(cg.P + o, pv);
             if (anyx) {
               double xv[VEC];
-              ldv(cg.x + o, xv);
+              lds(cg.x + o, xv);
 #pragma unroll
               for (int e = 0; e < VEC; ++e)
                 if (fl[e] & 2) xv[e] = fma(cg_al[gc + e], pv[e], xv[e]);
@@ -406,14 +475,14 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
             }
             if (anyp) {
               double qv[VEC];
-              ldv(cg.Q + o, qv);
+              lds(cg.Q + o, qv);
 #pragma unroll
               for (int e = 0; e < VEC; ++e) {
                 if (fl[e] & 1) {
                   const double be = cg_be[gc + e];
                   pv[e] = fma(be, pv[e], rv[e]);
                   qv[e] = fma(be, qv[e], y[e]);
-                  sacc[warp][q * VEC + e][lane] = fma(pv[e], qv[e], sacc[warp][q * VEC + e][lane]);
+                  dacc[CG ? q : 0][CG ? e : 0] = fma(pv[e], qv[e], dacc[CG ? q : 0][CG ? e : 0]);
                 }
               }
               stv(cg.P + o, pv);
@@ -483,6 +552,12 @@ __global__ void __launch_bounds__(kSpmmThreads, spmm_min_blocks(VEC* NV))
   }
 
   if (a.dot_mode == 0) return;
+  if constexpr (CG) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) sacc[warp][q * VEC + e][lane] = dacc[q][e];
+  }
   // reduce over the row groups of the warp (fixed order g = 0..G-1), then warps
   __syncwarp();
   if (g0 == 0) {
@@ -532,11 +607,21 @@ int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* o
   return GCG_OK;
 }
 
+// resident CTAs per SM of the fused CG sweep (GCG_CG_MINB=4: the 64-register build)
+static int cg_minb() {
+  static const int v = getenv("GCG_CG_MINB") ? atoi(getenv("GCG_CG_MINB")) : 3;
+  return v == 4 ? 4 : 3;
+}
+
 template <int VEC, int NV>
 static void launch_one(Ctx* c, const SpmmArgs& a, int grid, const CgSweep* cg) {
   if (cg) {
-    pdl_launch(spmm_csr_kernel<VEC, NV, false, true>, dim3(grid), dim3(kSpmmThreads), 0,
-               c->stream, a, *cg);
+    if (cg_minb() == 4)
+      pdl_launch(spmm_csr_kernel<VEC, NV, false, 1>, dim3(grid), dim3(kSpmmThreads), 0,
+                 c->stream, a, *cg);
+    else
+      pdl_launch(spmm_csr_kernel<VEC, NV, false, 2>, dim3(grid), dim3(kSpmmThreads), 0,
+                 c->stream, a, *cg);
     return;
   }
   // the CG forms (shift and/or dot against X itself, same ld): own row from the gathers
@@ -545,10 +630,10 @@ static void launch_one(Ctx* c, const SpmmArgs& a, int grid, const CgSweep* cg) {
                                  (a.dot_mode == 1 && a.W == a.X && a.ldw == a.ldx));
   const CgSweep none = {};
   if (self)
-    pdl_launch(spmm_csr_kernel<VEC, NV, true, false>, dim3(grid), dim3(kSpmmThreads), 0,
+    pdl_launch(spmm_csr_kernel<VEC, NV, true, 0>, dim3(grid), dim3(kSpmmThreads), 0,
                c->stream, a, none);
   else
-    pdl_launch(spmm_csr_kernel<VEC, NV, false, false>, dim3(grid), dim3(kSpmmThreads), 0,
+    pdl_launch(spmm_csr_kernel<VEC, NV, false, 0>, dim3(grid), dim3(kSpmmThreads), 0,
                c->stream, a, none);
 }
 
@@ -663,7 +748,9 @@ static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowpt
       }
     }
     // caller-reduced partials ([grid][k]) need one grid for every pass
-    int grid = grid_fixed ? grid_fixed : spmm_grid_for(c, n, nv * vec);
+    int grid = grid_fixed ? grid_fixed
+                          : (cg ? grid_for(n, 64, cg_minb(), c->num_sms)
+                                : spmm_grid_for(c, n, nv * vec));
     if (partials_ext) grid_fixed = grid;
     long long rpc = 0;
     if (contig) {
@@ -699,6 +786,8 @@ static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowpt
     a.pld = partials_ext ? k : kc;
     a.skip = skip;
     a.c0 = c0;
+    static const int cg_pf = getenv("GCG_CG_PREFETCH") ? atoi(getenv("GCG_CG_PREFETCH")) : 1;
+    a.cg_prefetch = cg_pf;
     const int vb = 8 * vec;
     a.vepi = aligned_to(a.Y, vb) && ldy % vec == 0 &&
              (gamma == 0.0 || (aligned_to(a.Z, vb) && ldz % vec == 0)) &&
