@@ -53,6 +53,9 @@ BACKEND_NAME = "sm100"
 _TIMING_KEYS = ("t_step2", "t_step3", "t_step4", "t_step5", "t_step6")
 _RESIDUAL_MODES = {"reference": None, "relative": 2}
 _RNG_CHUNK_ROWS = 1 << 16
+_PANEL_BYTES = 512 << 20      # row-panel scratch of the wide in-place LinComb
+_PANEL_MIN_ROWS = 1 << 16
+_AB_CHUNK_BYTES = 4 << 30     # A*basis of the full projection in column chunks above this
 
 
 @dataclass
@@ -328,25 +331,34 @@ class _Solve:
 
     def update_in_place(self, basis, cm, dst):
         """dst <- basis @ cm where dst = the leading columns of basis (the reference's
-        v[:, locked:sx] = x_new; v[:, sx:sx+np] = p_new, solver.py:378-384).  One
-        in-place lincomb when all columns fit one tile (<= 256), else via a temporary."""
-        if cm.shape[1] <= 256:
+        v[:, locked:sx] = x_new; v[:, sx:sx+np] = p_new, solver.py:378-384, and the
+        moving window's x_all = basis @ full.vectors, :333).  One in-place lincomb when
+        all columns fit one CTA tile (<= 256); wider products go through row panels: each
+        output row depends only on the same input row, so a panel scratch of
+        _PANEL_BYTES replaces the n x d temporary (cfg5: 33.5 GB per rank at 4 GPUs)."""
+        d = cm.shape[1]
+        if d <= 256:
             D.lincomb(self.dev, basis, cm, dst)
-        else:
-            tmp = self.ops.vec(cm.shape[1])
-            D.lincomb(self.dev, basis, cm, tmp)
-            D.copy(self.dev, tmp, dst)
+            return
+        nloc = basis.shape[0]
+        rows = int(min(nloc, max(_PANEL_MIN_ROWS, _PANEL_BYTES // (8 * d))))
+        tmp = self.dev.empty(rows, d)
+        for r in range(0, nloc, rows):
+            e = min(r + rows, nloc)
+            D.lincomb(self.dev, basis[r:e], cm, tmp[:e - r])
+            D.copy(self.dev, tmp[:e - r], dst[r:e])
 
-    def hstack(self, parts):
-        """Contiguous copy of column blocks (the reference's np.hstack, solver.py:337,356,401,450)."""
-        parts = [p for p in parts if p.shape[1] > 0]
-        width = sum(p.shape[1] for p in parts)
-        out = self.ops.vec(width)
-        c = 0
-        for p in parts:
-            D.copy(self.dev, p, out[:, c:c + p.shape[1]])
-            c += p.shape[1]
-        return out
+    def projected(self, basis, abar):
+        """abar = basis' A basis (solver.py:279); A basis in column chunks when the n x m
+        product would be large (one chunk below _AB_CHUNK_BYTES: the round-1 path)."""
+        m = basis.shape[1]
+        step = m if basis.shape[0] * m * 8 <= _AB_CHUNK_BYTES else 256
+        for c0 in range(0, m, step):
+            c1 = min(m, c0 + step)
+            ab = self.apply_a(basis[:, c0:c1])
+            self.ops.gram(basis, ab, abar if step == m else abar[:, c0:c1])
+            del ab
+        D.symmetrize(self.dev, abar)
 
 
 def gcg_solve(a, b=None, config=None, *, x0=None):
@@ -388,7 +400,15 @@ def gcg_solve_ops(ops, cfg, x0=None):
     det = cfg.deterministic
     Bop = prob.B
 
-    v = ops.vec(sx + 2 * bs, zero=True)
+    # One arena for the converged store and the window (SURVEY §7 "Memory"):
+    # columns [0, S) hold the pairs the moving window has emitted, the window
+    # [X | P | W] starts at S.  [store, X, P] — the deflation basis of STEP 2 — is
+    # then a contiguous column range, the window slide is an in-place LinComb plus
+    # S += c, and nothing is copied (the reference hstacks, solver.py:337,356,401,450).
+    width = (ne if cfg.moving else 0) + sx + 2 * bs
+    arena = ops.vec(width, zero=True)
+    S_off = 0
+    v = arena
     lam = np.zeros(sx + 2 * bs)
     # host eigenvector buffer, page-faulted in the background during the solve
     host_out = None if cfg.return_device else PrefaultedHost(nloc, ne)
@@ -414,7 +434,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
     np_, nw = 0, 0
     abar_prev = None
     p_coupling = None
-    store_x, store_vals = [], []
+    store_vals = []
     history = []
     pending_cg = []
     timers = []
@@ -434,9 +454,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
         # STEP 3: projected matrix (solver.py:277-294)
         abar = dev.empty(m, m)
         if abar_prev is None:
-            ab = S.apply_a(basis)
-            ops.gram(basis, ab, abar)
-            D.symmetrize(dev, abar)
+            S.projected(basis, abar)
         else:
             cross = None
             if nw:
@@ -497,19 +515,16 @@ def gcg_solve_ops(ops, cfg, x0=None):
                 ops.broadcast(full.values)
                 ops.broadcast(full.vectors)
             lam_all = full.values.cpu().numpy()
-            x_all = dev.empty(nloc, m)
-            D.lincomb(dev, basis, full.vectors, x_all)
-            blk = dev.empty(nloc, locked + newly)
-            if locked:
-                D.copy(dev, v[:, :locked], blk[:, :locked])
-            if newly:
-                D.copy(dev, x_all[:, :newly], blk[:, locked:])
-            store_x.append(blk)
+            # x_all = basis @ full.vectors, in place over the basis (v[:, locked:locked+m]):
+            # the emitted pairs [X_locked | x_all[:, :newly]] then already sit right after
+            # the store, and the new window x_all[:, newly:] right after them
+            S.update_in_place(basis, full.vectors, basis)
             store_vals.append(np.concatenate([lam[:locked], lam_all[:newly]]))
             stored += c
+            S_off += c
+            v = arena[:, S_off:]
             sx = m - newly
             if sx:
-                D.copy(dev, x_all[:, newly:], v[:, :sx])
                 lam[:sx] = lam_all[newly:]
             locked = 0
             np_, nw = 0, 0
@@ -520,7 +535,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
                 add = min(3 * bs, n - stored) - sx
                 if add > 0:
                     S.set_random(v[:, sx:sx + add], cfg.seed + 104729 * it)
-                    defl = S.hstack(store_x + [v[:, :sx]])
+                    defl = arena[:, :S_off + sx]   # [store, X]: contiguous
                     ro = orth_against(ops, v[:, sx:sx + add], defl, b=Bop, cfg=ocfg)
                     iter_red += ro.reduction_count
                     sx += ro.num_kept
@@ -571,11 +586,8 @@ def gcg_solve_ops(ops, cfg, x0=None):
                                   x0=x_act)
             timer.lap("t_step6")
 
-            # STEP 2: W against [store, X, P] (solver.py:398-420)
-            if store_x:
-                defl = S.hstack(store_x + [v[:, :sx + np_]])
-            else:
-                defl = v[:, :sx + np_]
+            # STEP 2: W against [store, X, P] (solver.py:398-420): one contiguous range
+            defl = arena[:, :S_off + sx + np_]
             try:
                 w_out = orth_against(ops, w_region, defl, b=Bop, cfg=ocfg)
                 nw = w_out.num_kept
@@ -615,18 +627,17 @@ def gcg_solve_ops(ops, cfg, x0=None):
     for tm in timers:             # per-step GPU times (the records hold tm.marks)
         tm.resolve()
 
-    # result assembly (solver.py:447-472)
-    if store_x:
-        parts = store_x + [v[:, :locked]]
+    # result assembly (solver.py:447-472): store, locked window columns and (when the
+    # iterations ran out) Ritz padding are consecutive arena columns
+    if store_vals:
         all_vals = np.concatenate(store_vals + [lam[:locked]])
         n_conv = all_vals.shape[0]
         if n_conv < ne:
             extra = min(ne - n_conv, sx - locked)
-            parts.append(v[:, locked:locked + extra])
             all_vals = np.concatenate([all_vals, lam[locked:locked + extra]])
         take = min(ne, all_vals.shape[0])
         values = all_vals[:take].copy()
-        vectors = S.hstack(parts)[:, :take]
+        vectors = arena[:, :take]
     else:
         n_conv = locked
         values = lam[:ne].copy()
