@@ -322,6 +322,27 @@ int gcg_stencil_csr(void* ctx, int64_t n0, int64_t n1, int64_t n2, int32_t noff,
  * from the N^3 cell field kc (device): out = [diag | -face(ax, s) for (ax, s) in
  * (0,-1),(0,+1),(1,-1),(1,+1),(2,-1),(2,+1)], 7 arrays of N^3. */
 int gcg_varcoef7_weights(void* ctx, int64_t N, const double* kc, double* out);
+/* One rank's z-slab of the same stencil for a row-partitioned run:
+ * rows [row0, row1) with columns in the local layout of distributed.local_part —
+ * owned rows 0..nloc-1, then the ghost plane below (global [row0 - nprev, row0)),
+ * then the one above ([row1, row1 + nnext)); a plane is n1*n2 rows (n2 for n0 = 1).
+ * Pass 1 (colidx == NULL): fills rowptr (nloc + 1) and *nnz_out = the slab's nnz.
+ * Pass 2: fills colidx/val; *nnz_out = nprev + nnext (ghost rows); GCG_ERR_ARG if
+ * the stencil reaches beyond one ghost plane.  wrow (per-row weights) are indexed by
+ * GLOBAL row. */
+int gcg_stencil_slab(void* ctx, int64_t n0, int64_t n1, int64_t n2, int32_t noff,
+                     const int32_t* offs, const double* w, const double* const* wrow, int64_t row0,
+                     int64_t row1, int32_t* rowptr, int32_t* colidx, double* val,
+                     int64_t* nnz_out);
+/* Device validation of a square CSR operator (operators.py:56-66, 79-87; rows sorted):
+ * out[4] (host) = {max |a_ij|, max |a_ij - a_ji| (missing = 0), #non-finite values,
+ * #column indices outside [0, n)}.  Synchronous. */
+int gcg_csr_check(void* ctx, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                  const double* val, double* out);
+/* X[i, c] = N(0,1) from Philox4x32-10 keyed by seed at counter (row0 + i, c / 2)
+ * (Box-Muller): a seeded block that every row partition draws identically. */
+int gcg_fill_normal(void* ctx, int64_t n, int64_t k, int64_t row0, uint64_t seed, double* X,
+                    int64_t ldx);
 
 /* ---- MatrixMarket ingestion (host; io.py:108-216 read_matrix_market) ------
  * gcg_mm_open parses the whole file (coordinate entries tokenised by

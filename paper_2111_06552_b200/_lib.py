@@ -80,6 +80,10 @@ _SIGS = {
     "gcg_stencil_nnz": [_i64, _i64, _i64, _i32, _ptr, _ptr],
     "gcg_stencil_csr": [_ptr, _i64, _i64, _i64, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
     "gcg_varcoef7_weights": [_ptr, _i64, _ptr, _ptr],
+    "gcg_stencil_slab": [_ptr, _i64, _i64, _i64, _i32, _ptr, _ptr, _ptr, _i64, _i64, _ptr, _ptr,
+                         _ptr, C.POINTER(_i64)],
+    "gcg_csr_check": [_ptr, _i64, _ptr, _ptr, _ptr, _ptr],
+    "gcg_fill_normal": [_ptr, _i64, _i64, _i64, C.c_uint64, _ptr, _i64],
     "gcg_mm_open": [C.c_char_p, _int, C.POINTER(_ptr), _ptr],
     "gcg_mm_fetch": [_ptr, _ptr, _ptr, _ptr],
     "gcg_mm_close": [_ptr],

@@ -24,8 +24,9 @@ from . import problems as P
 from .errors import InvalidShape
 from .operators import DeviceCsr, DeviceProblem
 
-__all__ = ["stencil_device", "laplacian_2d_device", "laplacian_3d_device", "stencil27_device",
-           "varcoef_diffusion_3d_device", "device_baseline_problem"]
+__all__ = ["stencil_device", "stencil_slab_device", "baseline_stencil_spec", "laplacian_2d_device",
+           "laplacian_3d_device", "stencil27_device", "varcoef_diffusion_3d_device",
+           "device_baseline_problem"]
 
 
 def _grid3(shape, offsets):
@@ -45,29 +46,85 @@ def stencil_device(ctx, shape, offsets, weights):
     flat = (C.c_int32 * (3 * noff))(*[v for o in offs for v in o])
     nnz = C.c_int64()
     _lib.check(_lib.load().gcg_stencil_nnz(n0, n1, n2, noff, flat, C.byref(nnz)), "gcg_stencil_nnz")
-    per_row = any(isinstance(w, torch.Tensor) for w in weights)
     keep = []  # temporaries that must outlive the launch
-    wc = (C.c_double * noff)(*[0.0 if isinstance(w, torch.Tensor) else float(w) for w in weights])
-    wr = None
-    if per_row:
-        ptrs = []
-        for w in weights:
-            if isinstance(w, torch.Tensor):
-                if w.shape != (n,) or w.dtype != torch.float64 or not w.is_cuda:
-                    raise InvalidShape("per-row stencil weights must be (n,) float64 device arrays")
-                ptrs.append(w.data_ptr())
-            else:  # a constant next to per-row weights: broadcast as a device array
-                t = ctx.empty(n)
-                D.fill(ctx, t.view(n, 1), float(w))
-                keep.append(t)
-                ptrs.append(t.data_ptr())
-        wr = (C.c_void_p * noff)(*ptrs)
+    wc, wr = _weight_args(ctx, weights, n, keep)
     rowptr = ctx.empty(n + 1, dtype=torch.int32)
     colidx = ctx.empty(int(nnz.value), dtype=torch.int32)
     val = ctx.empty(int(nnz.value))
     _lib.call("gcg_stencil_csr", ctx.h, n0, n1, n2, noff, flat, wc, wr, D._p(rowptr),
               D._p(colidx), D._p(val))
     return DeviceCsr(ctx, rowptr, colidx, val, n)
+
+
+def _weight_args(ctx, weights, n, keep):
+    """(constant weights, per-row pointer array or None) for the stencil generators."""
+    noff = len(weights)
+    per_row = any(isinstance(w, torch.Tensor) for w in weights)
+    wc = (C.c_double * noff)(*[0.0 if isinstance(w, torch.Tensor) else float(w) for w in weights])
+    if not per_row:
+        return wc, None
+    ptrs = []
+    for w in weights:
+        if isinstance(w, torch.Tensor):
+            if w.shape != (n,) or w.dtype != torch.float64 or not w.is_cuda:
+                raise InvalidShape("per-row stencil weights must be (n,) float64 device arrays")
+            ptrs.append(w.data_ptr())
+        else:
+            t = ctx.empty(n)
+            D.fill(ctx, t.view(n, 1), float(w))
+            keep.append(t)
+            ptrs.append(t.data_ptr())
+    return wc, (C.c_void_p * noff)(*ptrs)
+
+
+def stencil_slab_device(ctx, shape, offsets, weights, row0, row1):
+    """This rank's z-slab [row0, row1) of the stencil in the local layout of a
+    row-partitioned run (gcg_stencil_slab): a DeviceCsr with n = row1 - row0 owned rows
+    whose columns index owned rows, then the ghost plane below, then the one above —
+    the matrix distributed.local_part cuts from the global CSR, without ever building
+    it.  Returns (csr, nprev, nnext)."""
+    (n0, n1, n2), offs = _grid3(shape, offsets)
+    noff = len(offs)
+    n = n0 * n1 * n2
+    flat = (C.c_int32 * (3 * noff))(*[v for o in offs for v in o])
+    keep = []
+    wc, wr = _weight_args(ctx, weights, n, keep)
+    nloc = int(row1 - row0)
+    rowptr = ctx.empty(nloc + 1, dtype=torch.int32)
+    nnz = C.c_int64()
+    _lib.call("gcg_stencil_slab", ctx.h, n0, n1, n2, noff, flat, wc, wr, int(row0), int(row1),
+              D._p(rowptr), None, None, C.byref(nnz))
+    colidx = ctx.empty(int(nnz.value), dtype=torch.int32)
+    val = ctx.empty(int(nnz.value))
+    ng = C.c_int64()
+    _lib.call("gcg_stencil_slab", ctx.h, n0, n1, n2, noff, flat, wc, wr, int(row0), int(row1),
+              D._p(rowptr), D._p(colidx), D._p(val), C.byref(ng))
+    plane = n1 * n2 if n0 > 1 else n2
+    nprev = min(plane, int(row0)) if row0 > 0 else 0
+    nnext = min(plane, n - int(row1)) if row1 < n else 0
+    assert nprev + nnext == int(ng.value)
+    return DeviceCsr(ctx, rowptr, colidx, val, nloc), nprev, nnext
+
+
+def baseline_stencil_spec(ctx, cfg, scale=None):
+    """(grid shape, offsets, weights) of BASELINE config 1, 2, 4 or 5 (weights of config 4
+    are per-row device arrays of the global grid)."""
+    meta = P.baseline_problem(cfg, scale=scale, build=False)
+    N = meta.grid[0]
+    if cfg == 1:
+        return (N, N), [(0, 0)] + _axis_offsets(2), [4.0] + [-1.0] * 4, meta
+    if cfg == 2:
+        return (N, N, N), [(0, 0, 0)] + _axis_offsets(3), [6.0] + [-1.0] * 6, meta
+    if cfg == 4:
+        rng = np.random.default_rng(0)
+        kc = torch.from_numpy(np.exp(rng.standard_normal((N, N, N))).reshape(-1)).to(ctx.device)
+        w = ctx.empty(7, N ** 3)
+        _lib.call("gcg_varcoef7_weights", ctx.h, N, D._p(kc), D._p(w))
+        return (N, N, N), [(0, 0, 0)] + _axis_offsets(3), [w[t] for t in range(7)], meta
+    if cfg == 5:
+        offs = list(itertools.product((-1, 0, 1), repeat=3))
+        return (N, N, N), offs, [26.0 if o == (0, 0, 0) else -1.0 for o in offs], meta
+    raise InvalidShape(f"config {cfg} is not a structured-grid stencil")
 
 
 def _axis_offsets(nd):

@@ -355,3 +355,17 @@ def col_scale_copy(ctx, s, X, Y):
     n, k = X.shape
     _lib.call("gcg_col_scale_copy", ctx.h, n, k, _p(s), _p(X), _ld(X), _p(Y), _ld(Y))
     return Y
+
+
+def fill_normal(ctx, X, row0, seed):
+    """X[i, c] = seeded N(0,1) of global row row0 + i (Philox, gcg_fill_normal)."""
+    n, k = X.shape
+    _lib.call("gcg_fill_normal", ctx.h, n, k, int(row0), int(seed) & (2**64 - 1), _p(X), _ld(X))
+    return X
+
+
+def csr_check(ctx, A):
+    """(max |a|, max |a - a'|, #non-finite, #bad columns) of a square DeviceCsr (gcg_csr_check)."""
+    out = (C.c_double * 4)()
+    _lib.call("gcg_csr_check", ctx.h, A.n, _p(A.rowptr), _p(A.colidx), _p(A.val), out)
+    return float(out[0]), float(out[1]), int(out[2]), int(out[3])

@@ -37,7 +37,8 @@ from . import device as D
 from .mvops import LocalOps
 from .operators import DeviceCsr, DeviceProblem, _shared_pattern
 
-__all__ = ["row_bounds", "LocalPart", "local_part", "Comm", "DistProblem", "DistOps"]
+__all__ = ["row_bounds", "LocalPart", "local_part", "SlabPart", "slab_problem", "Comm",
+           "DistProblem", "DistOps", "gcg_solve_distributed"]
 
 
 def row_bounds(n, nranks, plane=1):
@@ -111,6 +112,65 @@ def local_part(a, b, bounds, rank):
         lb = scipy.sparse.csr_matrix((bsub.data, newcols.astype(np.int32), bsub.indptr),
                                      shape=la.shape)
     return LocalPart(rank, np.asarray(bounds), la, lb, ghost, recv_counts, send_rows)
+
+
+@dataclass
+class SlabPart:
+    """LocalPart of a z-slab assembled on the device (devgen.stencil_slab_device): the same
+    halo bookkeeping without host matrices — ghosts are the plane below (from rank - 1)
+    and the plane above (from rank + 1); the rows sent are the slab's first / last plane."""
+
+    rank: int
+    bounds: np.ndarray
+    nprev: int
+    nnext: int
+    a = None
+    b = None
+
+    @property
+    def r0(self):
+        return int(self.bounds[self.rank])
+
+    @property
+    def nloc(self):
+        return int(self.bounds[self.rank + 1] - self.bounds[self.rank])
+
+    @property
+    def nghost(self):
+        return self.nprev + self.nnext
+
+    @property
+    def recv_counts(self):
+        c = np.zeros(len(self.bounds) - 1, dtype=np.int64)
+        if self.nprev:
+            c[self.rank - 1] = self.nprev
+        if self.nnext:
+            c[self.rank + 1] = self.nnext
+        return c
+
+    @property
+    def send_rows(self):
+        out = [np.zeros(0, dtype=np.int64) for _ in range(len(self.bounds) - 1)]
+        if self.nprev:   # my first plane is the lower neighbour's upper ghost plane
+            out[self.rank - 1] = np.arange(self.nprev, dtype=np.int64)
+        if self.nnext:   # my last plane is the upper neighbour's lower ghost plane
+            out[self.rank + 1] = np.arange(self.nloc - self.nnext, self.nloc, dtype=np.int64)
+        return out
+
+
+def slab_problem(dev, comm, cfg, scale=None, plane_align=True):
+    """This rank's DistProblem of BASELINE config 1/2/4/5 assembled on the device: the
+    global operator is never built on any host (config 5: 449 M nonzeros)."""
+    from .devgen import baseline_stencil_spec, stencil_slab_device
+
+    shape, offs, weights, meta = baseline_stencil_spec(dev, cfg, scale)
+    n = int(np.prod(shape))
+    plane = int(np.prod(shape[1:])) if plane_align else 1
+    bounds = row_bounds(n, comm.size, plane)
+    r0, r1 = int(bounds[comm.rank]), int(bounds[comm.rank + 1])
+    A, nprev, nnext = stencil_slab_device(dev, shape, offs, weights, r0, r1)
+    part = SlabPart(comm.rank, bounds, nprev, nnext)
+    return DistProblem(dev, part, comm, n, A=A), meta
 
 
 class Comm:
@@ -200,18 +260,20 @@ class Comm:
 class DistProblem:
     """This rank's share of A (and B) in HBM plus the halo plan."""
 
-    def __init__(self, dev, part, comm, n_global):
+    def __init__(self, dev, part, comm, n_global, A=None, B=None):
         self.dev = self.ctx = dev
         self.part = part
         self.comm = comm
         self.n = part.nloc                      # rows owned (the solver's local n)
         self.n_global = n_global
         self.nghost = part.nghost
-        self.A = DeviceCsr.from_scipy(dev, part.a)
+        if A is None:
+            A = DeviceCsr.from_scipy(dev, part.a)
+            if part.b is not None:
+                B = A.with_values(dev.upload(part.b.data.astype(np.float64)))
+        self.A = A
         self.A.n = part.nloc
-        self.B = None
-        if part.b is not None:
-            self.B = self.A.with_values(dev.upload(part.b.data.astype(np.float64)))
+        self.B = B
         self._shift_vals = None
         self._shift_theta = None
         send = [np.asarray(s, dtype=np.int32) for s in part.send_rows]

@@ -20,7 +20,8 @@ from . import _lib
 from . import device as D
 from .errors import InvalidMatrix, InvalidShape
 
-__all__ = ["DeviceCsr", "DeviceSell", "DeviceProblem", "as_device_problem", "validate_symmetric"]
+__all__ = ["DeviceCsr", "DeviceSell", "DeviceProblem", "as_device_problem", "validate_symmetric",
+           "validate_device"]
 
 _SYM_RTOL = 1e-12  # operators.py:26
 
@@ -56,9 +57,11 @@ class DeviceCsr:
         sp = scipy.sparse.csr_matrix(sp)
         if sp.nnz >= 2**31 or sp.shape[0] >= 2**31:
             raise InvalidShape("CSR too large for int32 indices")
-        rp = ctx.upload(sp.indptr.astype(np.int32))
-        ci = ctx.upload(sp.indices.astype(np.int32))
-        v = ctx.upload((sp.data if values is None else values).astype(np.float64))
+        # np.asarray: no host copy when the arrays already have the device dtypes (so
+        # arrays in page-locked memory go straight to a DMA)
+        rp = ctx.upload(np.asarray(sp.indptr, dtype=np.int32))
+        ci = ctx.upload(np.asarray(sp.indices, dtype=np.int32))
+        v = ctx.upload(np.asarray(sp.data if values is None else values, dtype=np.float64))
         return cls(ctx, rp, ci, v, sp.shape[0])
 
     def with_values(self, val):
@@ -204,12 +207,30 @@ def as_device_problem(ctx, a, b=None, validate=True):
             else:
                 raise InvalidShape(f"cannot build an operator from shape {arr.shape}")
         sp.sum_duplicates()
-        if validate:
-            validate_symmetric(sp, name)
+        if sp.shape[0] != sp.shape[1]:
+            raise InvalidShape(f"sparse {name} must be square, got {sp.shape}")
         return sp
 
     sa = coerce(a, "A")
     sb = coerce(b, "B") if b is not None else None
     if sb is not None and sb.shape[0] != sa.shape[0]:
         raise InvalidShape(f"B dim {sb.shape[0]} != A dim {sa.shape[0]}")
-    return DeviceProblem(ctx, sa, sb)
+    prob = DeviceProblem(ctx, sa, sb)
+    if validate:
+        # the reference's operator checks (operators.py:79-87) on the device copy
+        for name, op in (("A", prob.A), ("B", prob.B)):
+            if op is not None:
+                validate_device(ctx, op, name)
+    return prob
+
+
+def validate_device(ctx, op, name="operator"):
+    """Finite and symmetric to 1e-12 * max(1, max |a|) (operators.py:79-87), checked by
+    gcg_csr_check on the matrix in HBM."""
+    amax, defect, nonfinite, badcol = D.csr_check(ctx, op)
+    if badcol:
+        raise InvalidShape(f"sparse {name} has column indices outside 0..{op.n - 1}")
+    if nonfinite:
+        raise InvalidMatrix(f"sparse {name} has non-finite entries")
+    if defect > _SYM_RTOL * max(1.0, amax):
+        raise InvalidMatrix(f"sparse {name} is not symmetric")

@@ -79,7 +79,8 @@ class SolverConfig:
     instrument_orth: bool = False
     cross_check_abar: bool = False
     # B200 drop-in extensions
-    init: str = "uniform"          # "uniform" (reference) | "normal" (BASELINE)
+    init: str = "uniform"          # "uniform" (reference) | "normal" (BASELINE, host PCG64)
+    #                                | "philox" (seeded N(0,1) drawn on the device per global row)
     residual: str = "reference"    # "reference" | "relative" (north-star)
     validate: bool = True          # host symmetry/finiteness check of the input matrices
     return_device: bool = False    # keep eigenvectors as a device tensor (row-major n x nev)
@@ -197,6 +198,8 @@ class _Solve:
         self.prob = ops.prob
         self.cfg = cfg
         self.generalized = self.prob.B is not None
+        if cfg.init not in ("uniform", "normal", "philox"):
+            raise InvalidShape(f"unknown init {cfg.init!r}")
         mode = _RESIDUAL_MODES.get(cfg.residual, "bad")
         if mode == "bad":
             raise InvalidShape(f"unknown residual kind {cfg.residual!r}")
@@ -211,6 +214,9 @@ class _Solve:
         PCG64 stream exactly like one call); each rank keeps its own rows.
         """
         ops = self.ops
+        if self.cfg.init == "philox":  # device draw: same global block for any row partition
+            D.fill_normal(self.dev, block, ops.row0, seed)
+            return
         rng = np.random.Generator(np.random.PCG64(seed))
         k = block.shape[1]
         r0, r1 = ops.row0, ops.row0 + ops.nloc
