@@ -60,13 +60,30 @@ def solver_kwargs(pr):
                 seed=0)
 
 
+def problem_size(pr):
+    """(n, nnz(A)) — from the matrix, or from the generator for device-assembled configs."""
+    if pr.a is not None:
+        return pr.a.shape[0], int(pr.a.nnz)
+    from paper_2111_06552_b200 import _lib
+    import ctypes as C
+    import itertools
+
+    N = pr.grid[0]
+    offs = list(itertools.product((-1, 0, 1), repeat=3))
+    flat = (C.c_int32 * (3 * len(offs)))(*[v for o in offs for v in o])
+    nnz = C.c_int64()
+    _lib.call("gcg_stencil_nnz", N, N, N, len(offs), flat, C.byref(nnz))
+    return N ** 3, int(nnz.value)
+
+
 def bench_config(pr, world):
     """The `config` dict both arms print (identical keys, so the driver's same_config holds)."""
-    return {"workload": pr.name, "n": pr.a.shape[0], "nnz": int(pr.a.nnz),
+    n, nnz = problem_size(pr)
+    return {"workload": pr.name, "n": n, "nnz": nnz,
             "nev": pr.num_eigen, "tol": pr.tol, "criterion": "north-star relative",
             "parallelism": f"row-partition x{world} (z-slabs, halo + reductions)"
             if world > 1 else "single",
-            "l2": "working set > 126 MB L2 (V arena 0.42 GB + CG blocks), no flush"}
+            "l2": "working set (arena + CG blocks) > 126 MB L2, no flush"}
 
 
 def initial_block(pr):
@@ -247,8 +264,17 @@ def main():
     rank, world, local = dist_env()
     from paper_2111_06552_b200 import problems as P
 
-    pr = P.baseline_problem(args.config)
+    # config 5 (449 M nonzeros, nev = 1000) is only ever assembled on the devices, one
+    # z-slab per rank; it needs >= 4 GPUs (device_memory_plan)
+    device_built = args.config == 5
+    pr = P.baseline_problem(args.config, build=not device_built)
     if args.impl == "reference":
+        if device_built:
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable":
+                                  "config 5 needs > 300 GB of host memory for the reference "
+                                  "(SURVEY §8(d)); not runnable on this host"}), flush=True)
+            return
         run_reference_arm(args, pr, rank, world)
         return
 
@@ -271,26 +297,56 @@ def main():
 
     ctx = D.default_context()
     kw = solver_kwargs(pr)
-    x0_host = initial_block(pr)
-    cfg = SolverConfig(**kw, init="normal", residual="relative", validate=False, return_device=True,
-                       collect_history=True)
+    n_glob, nnz_glob = problem_size(pr)
+    if device_built:
+        from paper_2111_06552_b200.solver import device_memory_plan
+
+        plane = pr.grid[1] * pr.grid[2]
+        plan = device_memory_plan(n_glob // world, nnz_glob // world + 1, pr.num_eigen,
+                                  moving=pr.moving, nghost=0 if world == 1 else 2 * plane)
+        cap = torch.cuda.get_device_properties(dev_index).total_memory
+        if plan["total"] > 0.95 * cap:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                                  "config": bench_config(pr, world), "unavailable":
+                                  f"per-rank HBM plan {plan['total'] / 1e9:.0f} GB > device "
+                                  f"{cap / 1e9:.0f} GB at {world} GPU(s); config 5 runs at >= 4"}),
+                      flush=True)
+            if world > 1:
+                dist.destroy_process_group()
+            return
+    # the seeded N(0,1) initial block: host PCG64 (the reference's stream) where a host
+    # draw is affordable, the partition-invariant device draw for config 5
+    x0_host = None if device_built else initial_block(pr)
+    cfg = SolverConfig(**kw, init="philox" if device_built else "normal", residual="relative",
+                       validate=False, return_device=True, collect_history=True)
     plane = int(np.prod(pr.grid[1:])) if len(pr.grid) > 1 else 1
     if world > 1:
-        # row-partitioned solve: z-slab row blocks, halo exchange + NCCL reductions
+        # row-partitioned solve: z-slab row blocks, halo exchange + NCCL reductions; the
+        # structured-grid operators are assembled per rank on the device (no global host CSR)
         from paper_2111_06552_b200.distributed import (Comm, DistOps, DistProblem, local_part,
-                                                       row_bounds)
+                                                       row_bounds, slab_problem)
 
         comm = Comm()
-        bounds = row_bounds(pr.a.shape[0], world, plane)
-        part = local_part(pr.a, pr.b, bounds, rank)
-        ops = DistOps(ctx, DistProblem(ctx, part, comm, pr.a.shape[0]))
-        x0_local = x0_host[part.r0:part.r0 + part.nloc]
+        if args.config in (1, 2, 4, 5):
+            dprob, _ = slab_problem(ctx, comm, args.config)
+        else:
+            bounds = row_bounds(n_glob, world, plane)
+            dprob = DistProblem(ctx, local_part(pr.a, pr.b, bounds, rank), comm, n_glob)
+        ops = DistOps(ctx, dprob)
+        x0_local = None if x0_host is None else x0_host[ops.row0:ops.row0 + ops.nloc]
     else:
         from paper_2111_06552_b200.mvops import LocalOps
 
-        ops = LocalOps(ctx, as_device_problem(ctx, pr.a, pr.b, validate=False))
+        if device_built:
+            from paper_2111_06552_b200.devgen import device_baseline_problem
+
+            ops = LocalOps(ctx, device_baseline_problem(ctx, args.config)[0])
+        else:
+            ops = LocalOps(ctx, as_device_problem(ctx, pr.a, pr.b, validate=False))
         x0_local = x0_host
-    x0_dev = torch.from_numpy(np.ascontiguousarray(x0_local)).to(ctx.device)
+    x0_dev = None if x0_local is None else \
+        torch.from_numpy(np.ascontiguousarray(x0_local)).to(ctx.device)
 
     def step():
         return gcg_solve_ops(ops, cfg, x0=x0_dev)
@@ -324,7 +380,7 @@ def main():
 
     # end-to-end through the public call with host buffers (pinned CSR + x0 in, eigenpairs out)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not device_built:
         import scipy.sparse
 
         # inputs in pinned host memory: the CSR arrays (int32 indices, as the device stores

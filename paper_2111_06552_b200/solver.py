@@ -47,6 +47,7 @@ __all__ = [
     "gcg_solve_ops",
     "select_shift",
     "moving_memory_budget",
+    "device_memory_plan",
 ]
 
 BACKEND_NAME = "sm100"
@@ -121,6 +122,33 @@ def moving_memory_budget(size_x, block_size):
     """solver.moving_memory_budget (solver.py:106-110)."""
     mpd = size_x + 2 * block_size
     return (size_x + 2 * block_size) + 2 * mpd * mpd + 10 * mpd + size_x * block_size
+
+
+def device_memory_plan(n_local, nnz_local, num_eigen, block_size=None, size_x=None,
+                       moving=False, nghost=0, generalized=False):
+    """Peak HBM bytes of one rank's solve (this implementation's allocations).
+
+    The arena [store | X | P | W] (moving: nev + sx + 2bs columns, else sx + 2bs) and the
+    block-CG workspace (r and x with ghost rows, p and q) are live for the whole solve;
+    on top of them at most three n_local x max(bs, 256) temporaries (residual chunk,
+    its A*x, the CG right-hand side / Ritz chunk) and the 512 MB panel scratch of the
+    wide in-place LinComb.  Returns a dict of the terms and their sum."""
+    bs = block_size if block_size is not None else max(1, math.ceil(num_eigen / 5))
+    if moving:
+        sx = 3 * bs
+    else:
+        sx = size_x if size_x is not None else num_eigen + 3 * bs
+    rows = n_local + nghost
+    arena = 8 * rows * ((num_eigen if moving else 0) + sx + 2 * bs)
+    csr = 4 * (n_local + 1) + 12 * nnz_local + (8 * nnz_local if generalized else 0)
+    cg = 8 * bs * (2 * rows + 2 * n_local)
+    temps = 3 * 8 * n_local * max(bs, 256)
+    if generalized:
+        temps += 8 * n_local * bs  # B * block in the orthogonalisation
+    plan = {"csr": csr, "arena": arena, "cg": cg, "temporaries": temps,
+            "panel": _PANEL_BYTES}
+    plan["total"] = sum(plan.values())
+    return plan
 
 
 def select_shift(mode, lam, num_locked, store_vals=()):

@@ -127,3 +127,20 @@ def test_comm_gloo_world2():
     assert res[0][1] == [1e16 + 1.0, 1.0 + 1e16, -1e16 + 1.0]
     assert res[0][2] == res[1][2] == 8.0
     assert res[0][3] == res[1][3] == [1.5, 6.0, -9.0]
+
+
+def test_cfg5_memory_plan_fits_at_4_and_8_gpus():
+    """BASELINE config 5 (27-pt 256^3, nev = 1000, moving): the per-rank HBM plan of the
+    single-arena solver fits a 180 GB B200 with headroom at 4 and 8 ranks
+    and does not at 1 or 2 — the SURVEY §8(d) memory analysis."""
+    from paper_2111_06552_b200.solver import device_memory_plan
+
+    n, nnz, plane = 256 ** 3, 449_455_096, 256 * 256
+    gb = {}
+    for ranks in (1, 2, 4, 8):
+        nloc = n // ranks
+        nghost = 0 if ranks == 1 else 2 * plane
+        plan = device_memory_plan(nloc, nnz // ranks + 1, 1000, moving=True, nghost=nghost)
+        gb[ranks] = plan["total"] / 1e9
+    assert gb[4] < 170.0 and gb[8] < 90.0
+    assert gb[2] > 180.0 and gb[1] > 180.0
