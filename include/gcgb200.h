@@ -63,6 +63,8 @@ int gcg_ctx_set_stream(void* ctx, void* cuda_stream);
 int gcg_ctx_sync(void* ctx);
 /* number of kernels this library has launched since load (instrumentation) */
 int64_t gcg_launch_count(void);
+/* number of cuSOLVER eigensolver calls since load (0 for every order <= 1024) */
+int64_t gcg_cusolver_calls(void);
 /* Live kernel timing: between begin and end every SpMM / Gram / LinComb / CG-update /
  * CG-p-update launch on this ctx is bracketed by CUDA events on the ctx stream.
  * end() synchronises and writes out[3*cls + {0,1,2}] = {total ms, launches,

@@ -21,6 +21,7 @@ _SIGS = {
     "gcg_abi_version": [],
     "gcg_status_string": [_int],
     "gcg_launch_count": [],
+    "gcg_cusolver_calls": [],
     "gcg_ctx_create": [C.POINTER(_ptr), _ptr],
     "gcg_ctx_destroy": [_ptr],
     "gcg_ctx_set_stream": [_ptr, _ptr],
@@ -88,7 +89,7 @@ _SIGS = {
     "gcg_mm_fetch": [_ptr, _ptr, _ptr, _ptr],
     "gcg_mm_close": [_ptr],
 }
-_RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64, "gcg_mm_close": None}
+_RESTYPE = {"gcg_status_string": C.c_char_p, "gcg_launch_count": _i64, "gcg_cusolver_calls": _i64, "gcg_mm_close": None}
 
 
 class OrthOpts(C.Structure):
@@ -185,3 +186,8 @@ def call(name, *args):
 
 def launch_count():
     return int(load().gcg_launch_count())
+
+
+def cusolver_calls():
+    """cuSOLVER eigensolver calls since load (none for Rayleigh-Ritz orders <= 1024)."""
+    return int(load().gcg_cusolver_calls())

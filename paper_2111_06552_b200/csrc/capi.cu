@@ -17,6 +17,7 @@
 namespace gcg {
 
 extern int64_t g_launches;
+extern int64_t g_cusolver_calls;
 
 int sell_size(Ctx* c, long long n, const int* rowptr, int sigma, long long* nslices,
               long long* nnz_padded);
@@ -239,6 +240,7 @@ const char* gcg_status_string(int status) {
 }
 
 int64_t gcg_launch_count(void) { return g_launches; }
+int64_t gcg_cusolver_calls(void) { return g_cusolver_calls; }
 
 int gcg_ctx_create(void** out, void* stream) {
   if (!out) return GCG_ERR_ARG;

@@ -396,12 +396,18 @@ __global__ void vec_fix_kernel(int m, const double* Vcm, double* V, long long ld
 bool dense_syev_tridiag_ok(int m);
 int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, double* w,
                        double* V, long long ldv);
+int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int sym, int il,
+                             int iu, double* w, double* V, long long ldv);
+
+int64_t g_cusolver_calls = 0;
 
 int dense_syev_cusolver_sym(Ctx* c, int m, const double* A, long long lda, int symmetrize,
                             double* w, double* V, long long ldv) {
   if (m <= 0) return GCG_ERR_ARG;
-  // orders up to 232: the one-CTA tridiagonalisation path (eig.cu), no cuSOLVER
+  // orders 3..1024 (every BASELINE Rayleigh-Ritz order): eig.cu, no cuSOLVER; cuSOLVER
+  // syevd only beyond (or with GCG_SYEV=cusolver for A/B)
   if (dense_syev_tridiag_ok(m)) return dense_syev_tridiag(c, m, A, lda, symmetrize, w, V, ldv);
+  ++g_cusolver_calls;
   cusolverDnSetStream(c->solver, c->stream);
   int lwork = 0;
   const size_t mat = (size_t)m * m;
@@ -468,13 +474,16 @@ int dense_syev_cusolver(Ctx* c, int m, const double* A, long long lda, double* w
   return dense_syev_cusolver_sym(c, m, A, lda, 0, w, V, ldv);
 }
 
-// Eigenpairs il..iu (1-based inclusive) — sym_eig_range (dense.py:86-117) — by
-// cuSOLVER syevdx with an index range: the same tridiagonalisation, then only the
-// requested pairs (bisection + inverse iteration) and their back-transformation.
+// Eigenpairs il..iu (1-based inclusive) — sym_eig_range (dense.py:86-117): for orders
+// 3..1024 eig.cu's tridiagonalisation, bisection of the requested indices only,
+// inverse iteration and back-transformation of those columns (the split-range RR of
+// each slice is independent); cuSOLVER syevdx beyond.
 // w receives iu - il + 1 values, V (m x (iu - il + 1), row-major) the sign-fixed vectors.
 int dense_syev_range(Ctx* c, int m, const double* A, long long lda, int il, int iu, double* w,
                      double* V, long long ldv) {
   if (m <= 0 || il < 1 || iu < il || iu > m) return GCG_ERR_ARG;
+  if (dense_syev_tridiag_ok(m)) return dense_syev_tridiag_range(c, m, A, lda, 0, il, iu, w, V, ldv);
+  ++g_cusolver_calls;
   cusolverDnSetStream(c->solver, c->stream);
   const size_t mat = (size_t)m * m;
   GCG_TRY(ensure(c->dense, sizeof(double) * (mat + (size_t)m) + 64));

@@ -43,7 +43,8 @@ namespace gcg {
 extern int64_t g_launches;
 
 constexpr int kTriThreads = 1024;
-constexpr int kEigMaxM = 224;
+constexpr int kEigMaxM = 224;    // one-CTA tridiagonalisation (packed triangle in smem)
+constexpr int kEigMaxBig = 1024; // multi-CTA path (tridiag_grid_kernel)
 
 __host__ __device__ inline int tri_off(int m, int j) { return j * m - (j * (j - 1)) / 2; }
 
@@ -274,8 +275,10 @@ __device__ __forceinline__ int sturm_count(int m, const double* d, const double*
 // 2. Eigenvalue idx (0-based, ascending) by 33-way multisection, one warp each.
 __global__ void __launch_bounds__(256) bisect_kernel(int m, const double* __restrict__ d,
                                                      const double* __restrict__ e, double* lam,
-                                                     double* norms) {
-  __shared__ double sd[kEigMaxM], se2[kEigMaxM];
+                                                     double* norms, int i0, int K) {
+  extern __shared__ double bsd[];  // d, e^2 of the scaled T (2m doubles)
+  double* sd = bsd;
+  double* se2 = bsd + m;
   __shared__ double rlo[8], rhi[8], rone[8];
   __shared__ double sgl, sgu, sscale;
   // Gershgorin interval and ||T||_1 (= ||T||_inf), block-parallel
@@ -320,8 +323,9 @@ __global__ void __launch_bounds__(256) bisect_kernel(int m, const double* __rest
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (idx >= m) return;
+  const int jl = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (jl >= K) return;
+  const int idx = i0 + jl;  // eigenvalue index (0-based, ascending) of this warp
   const double eps = 1.1102230246251565e-16;  // 2^-53
   const double tn = fmax(fabs(sgl), fabs(sgu));
   const double pad = 2.0 * eps * tn * m + 0x1p-900;
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(256) bisect_kernel(int m, const double* __rest
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) lam[idx] = 0.5 * (lo + hi) / sc;
+  if (lane == 0) lam[jl] = 0.5 * (lo + hi) / sc;
 }
 
 // deterministic pseudo-random start vector entry (dstein starts from uniform(-1, 1))
@@ -355,17 +359,32 @@ __device__ __forceinline__ double start_entry(int j, int k) {
 
 // 3. Inverse iteration for eigenvector j of T: solve (T - lam_j I) z = b by LU with
 // partial pivoting (dlagtf), b = start vector (pass 0) or the current column of Z
-// (pass 1); writes z (unnormalised) into column j of Z (column-major, ld m).
-// Per-thread factors interleaved [k][m] in W (coalesced across threads).  Pass 0
+// (pass 1); writes z (unnormalised) into column j of Z.
+// Per-thread factors interleaved [k][K] in W (coalesced across threads).  Pass 0
 // factors (one reciprocal per step on the dependent chain) and keeps the
 // multipliers and row swaps; pass 1 only re-runs the substitutions (one FMA per
 // step on the chain).  The backward pass multiplies by stored reciprocal pivots.
-__global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const double* e,
-                                                   const double* __restrict__ lam,
-                                                   double* __restrict__ Z, double* __restrict__ W,
-                                                   int pass,
-                                                   const double* __restrict__ norms) {
-  __shared__ double sdv[kEigMaxM], sev[kEigMaxM];
+// K vectors (eigenvalues lam[0..K-1], global indices j0..j0+K-1: the start vector
+// depends on the global index, so a slice equals the same columns of the full
+// solve).  Z layout: ldz == 0 -> column-major m x K (vector j at Z + j*m), else
+// row-major (element (k, j) at Z[k*ldz + j]).  The forward-substituted rhs lives
+// in dynamic shared memory ([m][blockDim]) when ys_shared, else in W (after the
+// six factor arrays, [m][K]).
+struct InvitZ {
+  double* Z;
+  long long ldz;
+  int m;
+  __device__ __forceinline__ double& at(int k, int j) const {
+    return ldz ? Z[(long long)k * ldz + j] : Z[(long long)j * m + k];
+  }
+};
+__global__ void __launch_bounds__(32) invit_kernel(int m, int K, int j0, const double* d,
+                                                   const double* e,
+                                                   const double* __restrict__ lam, InvitZ zz,
+                                                   double* __restrict__ W, int pass,
+                                                   const double* __restrict__ norms,
+                                                   int ys_shared) {
+  __shared__ double sdv[kEigMaxBig], sev[kEigMaxBig];
   extern __shared__ double ysm[];  // [m][32]: this thread's forward-substituted rhs
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
     sdv[k] = d[k];
@@ -375,31 +394,33 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
   d = sdv;
   e = sev;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  const size_t mm = (size_t)m * m;
+  if (j >= K) return;
+  const size_t mk = (size_t)m * K;
   double* R1 = W;            // 1 / U(k, k)
-  double* U2 = W + mm;
-  double* U3 = W + 2 * mm;
-  double* const Yb = ysm + threadIdx.x;  // Yb[k * 32]
-#define YS(k) Yb[(size_t)(k) * 32]
-  double* ML = W + 4 * mm;   // multipliers; negative zero-bias flag in SW
-  double* SW = W + 5 * mm;   // 1.0 where rows k, k+1 were swapped
-  double* z = Z + (size_t)j * m;
+  double* U2 = W + mk;
+  double* U3 = W + 2 * mk;
+  double* const Yb = ys_shared ? ysm + threadIdx.x : W + 6 * mk + j;
+  const size_t ysd = ys_shared ? blockDim.x : (size_t)K;
+#define YS(k) Yb[(size_t)(k) * ysd]
+  double* ML = W + 4 * mk;   // multipliers; negative zero-bias flag in SW
+  double* SW = W + 5 * mk;   // 1.0 where rows k, k+1 were swapped
+#define ZV(k) zz.at((k), j)
   if (pass == 0) {
     const double lj = lam[j];
     const double tnorm = norms[0];
     const double tiny = fmax(tnorm, 1e-300) * 2.220446049250313e-16;
     auto fixp = [&](double u) { return fabs(u) < tiny ? (u < 0.0 ? -tiny : tiny) : u; };
+    const int jg = j0 + j;
     double dg = d[0] - lj;            // current pivot-row diagonal
     double sp = m > 1 ? e[0] : 0.0;   // current pivot-row superdiagonal
-    double yk = start_entry(j, 0);
+    double yk = start_entry(jg, 0);
 #pragma unroll 4
     for (int k = 0; k + 1 < m; ++k) {
       const double sub = e[k];                        // T(k+1, k)
       const double a1 = d[k + 1] - lj;                // T(k+1, k+1)
       const double s1 = k + 2 < m ? e[k + 1] : 0.0;   // T(k+1, k+2)
-      const double bk1 = start_entry(j, k + 1);
-      const size_t o = (size_t)k * m + j;
+      const double bk1 = start_entry(jg, k + 1);
+      const size_t o = (size_t)k * K + j;
       // partial pivoting without divergence: swap rows k, k+1 when |sub| > |dg|
       const bool sw = fabs(sub) > fabs(dg);
       const double rp = __drcp_rn(sw ? sub : fixp(dg));
@@ -414,23 +435,23 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
       dg = fma(-mult, sw ? a1 : sp, sw ? sp : a1);
       sp = sw ? -mult * s1 : s1;
     }
-    R1[(size_t)(m - 1) * m + j] = __drcp_rn(fixp(dg));
+    R1[(size_t)(m - 1) * K + j] = __drcp_rn(fixp(dg));
     YS(m - 1) = yk;
   } else {
     // forward substitution of the new right-hand side with the stored factors
     // loads are batched 8 steps ahead of the chain: the stores to Y would otherwise
     // keep the compiler from hoisting the ML / SW / z loads (same base pointer)
-    double yk = z[0];
+    double yk = ZV(0);
     constexpr int B = 8;
     int k = 0;
     for (; k + B < m; k += B) {
       double mlb[B], swb[B], bb[B];
 #pragma unroll
       for (int u = 0; u < B; ++u) {
-        const size_t o = (size_t)(k + u) * m + j;
+        const size_t o = (size_t)(k + u) * K + j;
         mlb[u] = ML[o];
         swb[u] = SW[o];
-        bb[u] = z[k + u + 1];
+        bb[u] = ZV(k + u + 1);
       }
 #pragma unroll
       for (int u = 0; u < B; ++u) {
@@ -440,16 +461,16 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
       }
     }
     for (; k + 1 < m; ++k) {
-      const size_t o = (size_t)k * m + j;
-      const double bk1 = z[k + 1];
+      const size_t o = (size_t)k * K + j;
+      const double bk1 = ZV(k + 1);
       const bool sw = SW[o] != 0.0;
       YS(k) = sw ? bk1 : yk;
       yk = fma(-ML[o], sw ? bk1 : yk, sw ? yk : bk1);
     }
     YS(m - 1) = yk;
   }
-  double x2 = 0.0, x1 = YS(m - 1) * R1[(size_t)(m - 1) * m + j];
-  z[m - 1] = x1;
+  double x2 = 0.0, x1 = YS(m - 1) * R1[(size_t)(m - 1) * K + j];
+  ZV(m - 1) = x1;
   {
     constexpr int B = 8;
     int k = m - 2;
@@ -457,7 +478,7 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
       double yb[B], u2[B], u3[B], r1[B];
 #pragma unroll
       for (int u = 0; u < B; ++u) {
-        const size_t o = (size_t)(k - u) * m + j;
+        const size_t o = (size_t)(k - u) * K + j;
         yb[u] = YS(k - u);
         u2[u] = U2[o];
         u3[u] = U3[o];
@@ -466,20 +487,21 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, const double* d, const
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const double x0 = (yb[u] - u2[u] * x1 - u3[u] * x2) * r1[u];
-        z[k - u] = x0;
+        ZV(k - u) = x0;
         x2 = x1;
         x1 = x0;
       }
     }
     for (; k >= 0; --k) {
-      const size_t o = (size_t)k * m + j;
+      const size_t o = (size_t)k * K + j;
       const double x0 = (YS(k) - U2[o] * x1 - U3[o] * x2) * R1[o];
-      z[k] = x0;
+      ZV(k) = x0;
       x2 = x1;
       x1 = x0;
     }
   }
 #undef YS
+#undef ZV
   // no normalisation here: the cluster kernel normalises every column (2-norm);
   // the unnormalised solution is at most ~1/eps times the start vector
 }
@@ -497,87 +519,88 @@ constexpr double kTightGap = 1e-7;
 // 4. Orthonormalise each tight cluster (consecutive eigenvalues, gaps <= ortol):
 // one CTA per potential cluster start; classical Gram-Schmidt twice per vector
 // against the earlier members, then 2-norm normalisation (fixed-order sums).
-__global__ void __launch_bounds__(256) cluster_kernel(int m, const double* __restrict__ lam,
-                                                      double* Z, const double* __restrict__ norms) {
+// K vectors of length m in the InvitZ layout.
+__global__ void __launch_bounds__(256) cluster_kernel(int m, int K, const double* __restrict__ lam,
+                                                      InvitZ zz, const double* __restrict__ norms) {
   __shared__ double red[8][33];
-  __shared__ double coef[kEigMaxM];
+  __shared__ double coef[kEigMaxBig];
   const int b = blockIdx.x;
   const double ortol = kTightGap * norms[0];
   if (b > 0 && lam[b] - lam[b - 1] <= ortol) return;  // not a cluster start
   int end = b + 1;
-  while (end < m && lam[end] - lam[end - 1] <= ortol) ++end;
+  while (end < K && lam[end] - lam[end - 1] <= ortol) ++end;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int jj = b; jj < end; ++jj) {
-    double* zj = Z + (size_t)jj * m;
     for (int pass = 0; pass < 2 && jj > b; ++pass) {
       // coefficients c_i = z_i' z_j, one warp per earlier member (fixed order)
       for (int i = b + warp; i < jj; i += 8) {
-        const double* zi = Z + (size_t)i * m;
         double s = 0.0;
-        for (int k = lane; k < m; k += 32) s = fma(zi[k], zj[k], s);
+        for (int k = lane; k < m; k += 32) s = fma(zz.at(k, i), zz.at(k, jj), s);
         s = warp_sum(s);
         if (lane == 0) coef[i - b] = s;
       }
       __syncthreads();
       for (int k = tid; k < m; k += 256) {
-        double x = zj[k];
-        for (int i = b; i < jj; ++i) x = fma(-coef[i - b], Z[(size_t)i * m + k], x);
-        zj[k] = x;
+        double x = zz.at(k, jj);
+        for (int i = b; i < jj; ++i) x = fma(-coef[i - b], zz.at(k, i), x);
+        zz.at(k, jj) = x;
       }
       __syncthreads();
     }
     double s = 0.0;
-    for (int k = tid; k < m; k += 256) s = fma(zj[k], zj[k], s);
+    for (int k = tid; k < m; k += 256) s = fma(zz.at(k, jj), zz.at(k, jj), s);
     s = warp_sum(s);
     if (lane == 0) red[warp][0] = s;
     __syncthreads();
     double nrm2 = 0.0;
     for (int w2 = 0; w2 < 8; ++w2) nrm2 += red[w2][0];
     const double inv = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
-    for (int k = tid; k < m; k += 256) zj[k] *= inv;
+    for (int k = tid; k < m; k += 256) zz.at(k, jj) *= inv;
     __syncthreads();
   }
 }
 
-// 5. Z <- Q Z with Q = H_0 H_1 ... H_{m-3}: each warp owns kBtCols columns of Z in
-// registers (lane holds rows lane + 32 s) and applies all reflectors last-first,
-// with the next reflector's loads issued before the current one's reductions; no
-// block barriers.
+// 5. Z <- Q Z with Q = H_0 H_1 ... H_{m-3}: each warp owns COLS columns of Z in
+// registers (lane holds rows lane + 32 s, s < ROWS) and applies all reflectors
+// last-first, with the next reflector's loads issued before the current one's
+// reductions; no block barriers inside a chunk of CHUNK reflectors (staged in shared
+// memory, double-buffered).  K columns of Z in the InvitZ layout.
+// m <= 224: 4 columns x 7 rows per lane; m <= 1024: 1 column x 32 rows.
 constexpr int kBtWarps = 8;
-constexpr int kBtCols = 4;
-constexpr int kBtRows = (kEigMaxM + 31) / 32;
-constexpr int kBtChunk = 16;  // reflectors per shared-memory stage
-static size_t backtr_smem(int m) { return sizeof(double) * 2 * kBtChunk * ((size_t)m + 1); }
-__global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, const double* __restrict__ Vr,
+template <int CHUNK>
+static size_t backtr_smem(int m) { return sizeof(double) * 2 * CHUNK * ((size_t)m + 1); }
+template <int COLS, int ROWS, int CHUNK>
+__global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, int K,
+                                                               const double* __restrict__ Vr,
                                                                const double* __restrict__ tau,
-                                                               double* Z) {
-  extern __shared__ __align__(16) double bsm[];  // [2][kBtChunk][m] reflectors + [2][kBtChunk] tau
+                                                               InvitZ zz) {
+  extern __shared__ __align__(16) double bsm[];  // [2][CHUNK][m] reflectors + [2][CHUNK] tau
   double* vbuf = bsm;
-  double* tbuf = bsm + 2 * kBtChunk * (size_t)m;
+  double* tbuf = bsm + 2 * CHUNK * (size_t)m;
   const int lane = threadIdx.x & 31;
-  const int col0 = (blockIdx.x * kBtWarps + (threadIdx.x >> 5)) * kBtCols;
-  const bool live = col0 < m;
-  double r[kBtCols][kBtRows];
+  const int col0 = (blockIdx.x * kBtWarps + (threadIdx.x >> 5)) * COLS;
+  const bool live = col0 < K;
+  double r[COLS][ROWS];
 #pragma unroll
-  for (int cc = 0; cc < kBtCols; ++cc)
+  for (int cc = 0; cc < COLS; ++cc)
 #pragma unroll
-    for (int s = 0; s < kBtRows; ++s) {
+    for (int s = 0; s < ROWS; ++s) {
       const int k = lane + 32 * s;
-      r[cc][s] = (live && k < m && col0 + cc < m) ? Z[(size_t)(col0 + cc) * m + k] : 0.0;
+      r[cc][s] = (live && k < m && col0 + cc < K) ? zz.at(k, col0 + cc) : 0.0;
     }
-  // reflectors are applied last-first: chunk c covers j = jtop - c*kBtChunk down to ..-kBtChunk+1
+  // reflectors are applied last-first: chunk c covers j = jtop - c*CHUNK down to ..-CHUNK+1
   const int jtop = m - 3;
-  const int nchunks = jtop >= 0 ? jtop / kBtChunk + 1 : 0;
+  const int nchunks = jtop >= 0 ? jtop / CHUNK + 1 : 0;
   auto stage = [&](int cidx, int buf) {
-    const int jhi = jtop - cidx * kBtChunk;
-    const int cnt = min(kBtChunk, jhi + 1);
-    double* dst = vbuf + (size_t)buf * kBtChunk * m;
+    const int jhi = jtop - cidx * CHUNK;
+    const int cnt = min(CHUNK, jhi + 1);
+    double* dst = vbuf + (size_t)buf * CHUNK * m;
     for (int e = threadIdx.x; e < cnt * m; e += blockDim.x) {
       const int q = e / m, k = e - q * m;
       const int j = jhi - q;
       cp_async8(dst + (size_t)q * m + k, Vr + (size_t)j * m + k, k > j);
     }
-    if (threadIdx.x < cnt) cp_async8(tbuf + buf * kBtChunk + threadIdx.x, tau + jhi - threadIdx.x, true);
+    if (threadIdx.x < cnt) cp_async8(tbuf + buf * CHUNK + threadIdx.x, tau + jhi - threadIdx.x, true);
     cp_commit();
   };
   if (nchunks > 0) stage(0, 0);
@@ -590,36 +613,39 @@ __global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, const doub
       cp_wait<0>();
     }
     __syncthreads();
-    const int jhi = jtop - cidx * kBtChunk;
-    const int cnt = min(kBtChunk, jhi + 1);
-    const double* vb = vbuf + (size_t)buf * kBtChunk * m;
+    const int jhi = jtop - cidx * CHUNK;
+    const int cnt = min(CHUNK, jhi + 1);
+    const double* vb = vbuf + (size_t)buf * CHUNK * m;
     if (live) {
       for (int q = 0; q < cnt; ++q) {
-        const double t = tbuf[buf * kBtChunk + q];
+        const double t = tbuf[buf * CHUNK + q];
         if (t == 0.0) continue;
         const double* vj = vb + (size_t)q * m;
-        double vv[kBtRows];
+        // rows above the reflector's first row (k <= j) are zero-filled: skip whole
+        // register rows below the first nonzero 32-row block
+        const int s0 = (jhi - q + 1) >> 5;
+        double vv[ROWS];
 #pragma unroll
-        for (int s = 0; s < kBtRows; ++s) {
+        for (int s = 0; s < ROWS; ++s) {
           const int k = lane + 32 * s;
-          vv[s] = k < m ? vj[k] : 0.0;  // zero-filled above the reflector's first row
+          vv[s] = (s >= s0 && k < m) ? vj[k] : 0.0;
         }
-        double dot[kBtCols];
+        double dot[COLS];
 #pragma unroll
-        for (int cc = 0; cc < kBtCols; ++cc) {
+        for (int cc = 0; cc < COLS; ++cc) {
           dot[cc] = 0.0;
 #pragma unroll
-          for (int s = 0; s < kBtRows; ++s) dot[cc] = fma(vv[s], r[cc][s], dot[cc]);
+          for (int s = 0; s < ROWS; ++s) dot[cc] = fma(vv[s], r[cc][s], dot[cc]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-          for (int cc = 0; cc < kBtCols; ++cc) dot[cc] += __shfl_xor_sync(0xffffffffu, dot[cc], o);
+          for (int cc = 0; cc < COLS; ++cc) dot[cc] += __shfl_xor_sync(0xffffffffu, dot[cc], o);
 #pragma unroll
-        for (int cc = 0; cc < kBtCols; ++cc) {
+        for (int cc = 0; cc < COLS; ++cc) {
           const double f = t * dot[cc];
 #pragma unroll
-          for (int s = 0; s < kBtRows; ++s) r[cc][s] = fma(-f, vv[s], r[cc][s]);
+          for (int s = 0; s < ROWS; ++s) r[cc][s] = fma(-f, vv[s], r[cc][s]);
         }
       }
     }
@@ -627,11 +653,11 @@ __global__ void __launch_bounds__(32 * kBtWarps) backtr_kernel(int m, const doub
   }
   if (!live) return;
 #pragma unroll
-  for (int cc = 0; cc < kBtCols; ++cc)
+  for (int cc = 0; cc < COLS; ++cc)
 #pragma unroll
-    for (int s = 0; s < kBtRows; ++s) {
+    for (int s = 0; s < ROWS; ++s) {
       const int k = lane + 32 * s;
-      if (k < m && col0 + cc < m) Z[(size_t)(col0 + cc) * m + k] = r[cc][s];
+      if (k < m && col0 + cc < K) zz.at(k, col0 + cc) = r[cc][s];
     }
 }
 
@@ -665,51 +691,395 @@ __global__ void __launch_bounds__(256) loewdin_apply_kernel(int m, const double*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Orders 224 < m <= 1024 (cfg3 / cfg4 / cfg5 Rayleigh-Ritz: m = 400 / 500 / 1000):
+// the packed triangle (up to 4 MB) no longer fits one SM, so the Householder
+// reduction runs on G co-resident CTAs (cooperative launch, G ~ m / 8 <= #SMs).
+//
+// 1'. tridiag_grid_kernel  Row i of the full symmetric matrix lives in the shared
+//     memory of CTA i mod G (cyclic: the trailing block stays balanced), one warp
+//     per row.  Step j:
+//       A  each CTA applies the deferred rank-2 update of step j-1 to its trailing
+//          rows (x -= v_i w_c + w_i v_c, the product sum commutative, so the stored
+//          matrix stays bitwise symmetric), forms p_i = tau_j sum_c A(i, c) v_c and
+//          publishes p_i, its partial sum of p_i v_i and — the owner of row j+1 —
+//          that row (= column j+1 by symmetry) to global memory (L2, double
+//          buffered by step parity);
+//       one grid barrier (monotone counter, release / acquire);
+//       B  every CTA redundantly reduces the G partials in a fixed order, forms
+//          w_j = p - (tau/2)(p'v) v, applies step j's update to column j+1 and
+//          computes reflector v_{j+1} (dlarfg) — identical bits in every CTA.
+//     One barrier and a few L2 round trips per step; every element is read and
+//     written once per step from shared memory.  Same outputs as tridiag_kernel.
+constexpr int kTgThreads = 256;
+constexpr int kTgWarps = kTgThreads / 32;
+constexpr int kTgRows = 8;  // rows per CTA (one per warp); G = ceil(m / kTgRows)
+
+struct TgArgs {
+  int m;
+  const double* A;
+  long long lda;
+  int sym;
+  double* d;
+  double* e;
+  double* tau;
+  double* Vr;
+  double* pbuf;    // [2][m]  p of the current step (by parity)
+  double* rowbuf;  // [2][m]  row j+1 of A^(j)
+  double* part;    // [2][G]  per-CTA partial p'v
+  double* dlast;   // A^(m-3)(m-1, m-1)
+  unsigned* bar;   // grid barrier counter (zeroed before the launch)
+  int G;
+  int R;           // rows per CTA = ceil(m / G)
+};
+
+__device__ __forceinline__ double tg_sym_at(const TgArgs& a, int i, int c) {
+  const int r = i >= c ? i : c, s = i >= c ? c : i;  // the lower triangle of row-major A
+  double x = a.A[(long long)r * a.lda + s];
+  if (a.sym) x = 0.5 * (x + a.A[(long long)s * a.lda + r]);
+  return x;
+}
+// x - (v_i w_c + w_i v_c), symmetric in (i, c) bit for bit
+__device__ __forceinline__ double tg_upd(double x, double vi, double wc, double wi, double vc) {
+  return x - __dadd_rn(__dmul_rn(vi, wc), __dmul_rn(wi, vc));
+}
+__device__ __forceinline__ void tg_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+// fixed-order block sum (every thread gets the same value); red: 8 slots
+__device__ __forceinline__ double tg_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kTgWarps; ++w) s += red[w];
+  return s;
+}
+// reflector of column j (x[j..m-1] in shared memory) into vout; CTA 0 records d, e,
+// tau and the reflector column of Vr.  Returns tau.
+__device__ double tg_reflector(const TgArgs& a, int j, const double* x, double* vout,
+                               double* red) {
+  const int m = a.m;
+  double sq = 0.0;
+  for (int i = j + 2 + (int)threadIdx.x; i < m; i += kTgThreads) sq = fma(x[i], x[i], sq);
+  const double s = tg_block_sum(sq, red);
+  const double alpha = x[j + 1], djj = x[j];
+  double t = 0.0, beta = alpha, scal = 0.0;
+  if (s > 0.0) {
+    const double nrm2 = fma(alpha, alpha, s);
+    const double rn = rsqrt(nrm2);  // beta = -sign(alpha) ||x||
+    beta = alpha >= 0.0 ? -nrm2 * rn : nrm2 * rn;
+    t = (beta - alpha) * __drcp_rn(beta);
+    scal = __drcp_rn(alpha - beta);
+  }
+  for (int i = threadIdx.x; i < m; i += kTgThreads) {
+    const double vi = i <= j ? 0.0 : (i == j + 1 ? 1.0 : x[i] * scal);
+    vout[i] = t != 0.0 ? vi : 0.0;
+    if (blockIdx.x == 0 && i > j) a.Vr[(long long)j * m + i] = vi;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.d[j] = djj;
+    a.e[j] = beta;
+    a.tau[j] = t;
+  }
+  __syncthreads();
+  return t;
+}
+
+static size_t tg_smem(int m, int R) { return sizeof(double) * ((size_t)R * m + 4 * (size_t)m + 32); }
+
+__global__ void __launch_bounds__(kTgThreads, 1) tridiag_grid_kernel(TgArgs a) {
+  extern __shared__ double gsm[];
+  const int m = a.m, G = a.G, R = a.R, cta = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* S = gsm;  // [R][m]: local row r = global row cta + G r
+  double* vb[4];
+  for (int q = 0; q < 4; ++q) vb[q] = S + (size_t)R * m + (size_t)q * m;
+  double* red = vb[3] + m;  // [0,8) norm, [8,16) p'v warps, [16] p'v
+  for (int r = 0; r < R; ++r) {
+    const int i = cta + G * r;
+    if (i >= m) break;
+    for (int c = tid; c < m; c += kTgThreads) S[(size_t)r * m + c] = tg_sym_at(a, i, c);
+  }
+  for (int c = tid; c < m; c += kTgThreads) {
+    vb[0][c] = 0.0;  // v_{-1}
+    vb[1][c] = 0.0;  // w_{-1}
+    vb[3][c] = tg_sym_at(a, c, 0);  // column 0
+  }
+  __syncthreads();
+  double* vprev = vb[0];
+  double* wprev = vb[1];
+  double* vcur = vb[2];
+  double* wnew = vb[3];
+  double t = tg_reflector(a, 0, wnew, vcur, red);
+  for (int j = 0; j + 2 < m; ++j) {
+    const int par = j & 1;
+    double* pb = a.pbuf + (size_t)par * m;
+    double* rb = a.rowbuf + (size_t)par * m;
+    // A: deferred update + p on this CTA's trailing rows
+    double mypv = 0.0;
+    for (int r = warp; r < R; r += kTgWarps) {
+      const int i = cta + G * r;
+      if (i <= j || i >= m) continue;
+      double* Si = S + (size_t)r * m;
+      const double vpi = vprev[i], wpi = wprev[i];
+      const bool pub = i == j + 1;
+      double acc = 0.0;
+      for (int c = j + 1 + lane; c < m; c += 32) {
+        const double x = tg_upd(Si[c], vpi, wprev[c], wpi, vprev[c]);
+        Si[c] = x;
+        acc = fma(x, vcur[c], acc);
+        if (pub) __stcg(rb + c, x);
+      }
+      acc = warp_sum(acc);
+      __syncwarp();
+      const double p = t * acc;
+      if (lane == 0) {
+        __stcg(pb + i, p);
+        mypv = fma(p, vcur[i], mypv);
+        if (i == m - 1 && j == m - 3) __stcg(a.dlast, Si[m - 1]);
+      }
+    }
+    if (lane == 0) red[8 + warp] = mypv;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kTgWarps; ++w) s += red[8 + w];
+      __stcg(a.part + (size_t)par * G + cta, s);
+    }
+    tg_barrier(a.bar, (unsigned)G * (unsigned)(j + 1));
+    // B (redundant in every CTA): p'v in fixed order, w_j, column j+1, reflector j+1
+    if (warp == 0) {
+      double s = 0.0;
+      for (int q = lane; q < G; q += 32) s += __ldcg(a.part + (size_t)par * G + q);
+      s = warp_sum(s);
+      if (lane == 0) red[16] = s;
+    }
+    __syncthreads();
+    const double a2 = -0.5 * t * red[16];
+    for (int i = j + 1 + tid; i < m; i += kTgThreads) wnew[i] = fma(a2, vcur[i], __ldcg(pb + i));
+    __syncthreads();
+    double* xb = wprev;  // dead after A: column j+1 of A^(j+1)
+    double* vn = vprev;  // dead after A: v_{j+1}
+    const double wj1 = wnew[j + 1], vj1 = vcur[j + 1];
+    for (int i = j + 1 + tid; i < m; i += kTgThreads)
+      xb[i] = tg_upd(__ldcg(rb + i), vcur[i], wj1, wnew[i], vj1);
+    __syncthreads();
+    if (j + 3 < m) {
+      t = tg_reflector(a, j + 1, xb, vn, red);
+    } else if (cta == 0 && tid == 0) {  // last 2 x 2 block
+      a.d[m - 2] = xb[m - 2];
+      a.e[m - 2] = xb[m - 1];
+      a.tau[m - 2] = 0.0;
+      a.d[m - 1] = tg_upd(__ldcg(a.dlast), vcur[m - 1], wnew[m - 1], wnew[m - 1], vcur[m - 1]);
+    }
+    // rotate: (v_j, w_j) become the deferred update, v_{j+1} the current reflector
+    vprev = vcur;
+    wprev = wnew;
+    vcur = vn;
+    wnew = xb;
+    __syncthreads();
+  }
+}
+
+// V[i*ldv + j] = sign_j * Z[i*ldz + j] (row-major Z, column j) with the sign rule
+__global__ void vec_fix_rm_kernel(int m, const double* Z, long long ldz, double* V, long long ldv) {
+  const int j = blockIdx.x;
+  double best = -1.0;
+  int lead = 0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = fabs(Z[(long long)i * ldz + j]);
+    if (x > best) {
+      best = x;
+      lead = i;
+    }
+  }
+  __shared__ double bv[256];
+  __shared__ int bi[256];
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = lead;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double o = bv[threadIdx.x + w];
+      const int oi = bi[threadIdx.x + w];
+      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = o;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  const double sg = Z[(long long)bi[0] * ldz + j] < 0.0 ? -1.0 : 1.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) V[(long long)i * ldv + j] = sg * Z[(long long)i * ldz + j];
+}
+
+int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                const double* Y, long long ldy, double alpha, double beta, double* G,
+                long long grs, long long gcs);
+int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
+                   long long ldx, const double* C, long long ldc, double beta, double* Y,
+                   long long ldy);
+int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, double* Y,
+                long long ldy);
+
 __global__ void vec_fix_kernel(int m, const double* Vcm, double* V, long long ldv);
 
 bool dense_syev_tridiag_ok(int m) {
   static const char* impl = getenv("GCG_SYEV");
   if (impl && impl[0] == 'c') return false;  // GCG_SYEV=cusolver: A/B switch
-  return m >= 3 && m <= kEigMaxM;
+  return m >= 3 && m <= kEigMaxBig;
+}
+
+static bool use_grid_tridiag(int m) {
+  // GCG_TRIGRID=1: the multi-CTA reduction for m <= 224 too (A/B)
+  static const bool force = getenv("GCG_TRIGRID") && getenv("GCG_TRIGRID")[0] == '1';
+  return m > kEigMaxM || force;
+}
+
+static int tridiag_grid_launch(Ctx* c, int m, const double* A, long long lda, int sym, double* dd,
+                               double* ee, double* tt, double* Vr, double* gw) {
+  int G = (m + kTgRows - 1) / kTgRows;
+  if (G > c->num_sms) G = c->num_sms;
+  const int R = (m + G - 1) / G;
+  if (R > 2 * kTgRows) return GCG_ERR_ARG;
+  TgArgs a;
+  a.m = m;
+  a.A = A;
+  a.lda = lda;
+  a.sym = sym;
+  a.d = dd;
+  a.e = ee;
+  a.tau = tt;
+  a.Vr = Vr;
+  a.pbuf = gw;
+  a.rowbuf = gw + 2 * (size_t)m;
+  a.part = gw + 4 * (size_t)m;
+  a.dlast = a.part + 2 * (size_t)G;
+  a.bar = (unsigned*)(a.dlast + 2);
+  a.G = G;
+  a.R = R;
+  GCG_TRY(cuda_status(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), c->stream)));
+  const size_t smem = tg_smem(m, R);
+  kernel_smem((const void*)tridiag_grid_kernel, smem);
+  void* args[] = {&a};
+  GCG_TRY(cuda_status(cudaLaunchCooperativeKernel((const void*)tridiag_grid_kernel, dim3(G),
+                                                  dim3(kTgThreads), args, smem, c->stream)));
+  ++g_launches;
+  return GCG_OK;
+}
+
+// Eigenpairs il..iu (1-based inclusive; K = iu - il + 1) of the symmetric m x m
+// row-major A (symmetrised first when sym != 0): w (K values, ascending) and V
+// (row-major m x K, ldv; the sign rule applied).  No cuSOLVER:
+//   tridiagonalisation (one CTA for m <= 224, tridiag_grid_kernel above), bisection
+//   of the requested indices only, inverse iteration + tight-cluster Gram-Schmidt
+//   (twice), Loewdin, back-transform, sign rule.
+// The full spectrum of an order <= 224 keeps the column-major one-CTA kernels; every
+// other case (larger orders, index slices) works on a row-major Z (m x K) whose
+// Loewdin step is one DMMA Gram Z'Z and one LinComb Z (3/2 I - 1/2 G).
+int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int sym, int il,
+                             int iu, double* w, double* V, long long ldv) {
+  if (m < 3 || m > kEigMaxBig || il < 1 || iu < il || iu > m) return GCG_ERR_ARG;
+  const int K = iu - il + 1;
+  const bool grid = use_grid_tridiag(m);
+  const bool small = !grid && K == m;  // the original one-CTA pipeline
+  const size_t mm = (size_t)m * m, mk = (size_t)m * K;
+  const bool ys_shared = 32 * (size_t)m * sizeof(double) <= 64 * 1024;
+  // workspace: d, e, tau (3m) | Vr (m^2) | Z (mK) | inverse-iteration factors (6 mK)
+  // [+ rhs (mK)] | Z2 (mK) | G (K^2) | grid scratch (6m + 2G + 8) | norms
+  const size_t words = 3 * (size_t)m + mm + mk + 6 * mk + (ys_shared ? 0 : mk) + mk +
+                       (size_t)K * K + 6 * (size_t)m + 2 * kNumSMs + 16 + 8;
+  GCG_TRY(ensure(c->dense, sizeof(double) * words + 512));
+  double* dd = (double*)c->dense.ptr;
+  double* ee = dd + m;
+  double* tt = ee + m;
+  double* Vr = tt + m;
+  double* Z = Vr + mm;
+  double* W = Z + mk;
+  double* Z2 = W + 6 * mk + (ys_shared ? 0 : mk);
+  double* Gm = Z2 + mk;
+  double* gw = Gm + (size_t)K * K;
+  double* norms = gw + 6 * (size_t)m + 2 * kNumSMs + 16;
+  if (grid) {
+    GCG_TRY(tridiag_grid_launch(c, m, A, lda, sym, dd, ee, tt, Vr, gw));
+  } else {
+    const size_t smem = tri_smem(m);
+    kernel_smem((const void*)tridiag_kernel, smem);
+    tridiag_kernel<<<1, kTriThreads, smem, c->stream>>>(m, A, lda, sym, dd, ee, tt, Vr);
+    ++g_launches;
+  }
+  bisect_kernel<<<(K + 7) / 8, 256, 2 * sizeof(double) * m, c->stream>>>(m, dd, ee, w, norms,
+                                                                          il - 1, K);
+  InvitZ zz;
+  zz.Z = Z;
+  zz.ldz = small ? 0 : K;
+  zz.m = m;
+  const size_t ysm = ys_shared ? sizeof(double) * 32 * (size_t)m : 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    kernel_smem((const void*)invit_kernel, ysm);
+    invit_kernel<<<(K + 31) / 32, 32, ysm, c->stream>>>(m, K, il - 1, dd, ee, w, zz, W, pass,
+                                                        norms, ys_shared ? 1 : 0);
+    cluster_kernel<<<K, 256, 0, c->stream>>>(m, K, w, zz, norms);
+  }
+  g_launches += 5;
+  GCG_CHECK_LAUNCH();
+  if (small) {
+    double* G = W;  // the inverse-iteration factors are dead now
+    double* Zs = W + mm;
+    loewdin_gram_kernel<<<m, 256, 0, c->stream>>>(m, Z, G);
+    loewdin_apply_kernel<<<m, 256, 0, c->stream>>>(m, Z, G, Zs);
+    zz.Z = Zs;
+    auto bt = backtr_kernel<4, (kEigMaxM + 31) / 32, 16>;
+    kernel_smem((const void*)bt, backtr_smem<16>(m));
+    bt<<<(m + kBtWarps * 4 - 1) / (kBtWarps * 4), 32 * kBtWarps, backtr_smem<16>(m), c->stream>>>(
+        m, K, Vr, tt, zz);
+    vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, Zs, V, ldv);
+    g_launches += 4;
+    GCG_CHECK_LAUNCH();
+    return GCG_OK;
+  }
+  // Loewdin on the row-major Z: G = Z'Z, Z2 = 3/2 Z - 1/2 Z G (LinComb in <= 256-column panels)
+  GCG_TRY(gram_launch(c, m, K, K, Z, K, Z, K, 1.0, 0.0, Gm, K, 1));
+  GCG_TRY(copy_launch(c, m, K, Z, K, Z2, K));
+  for (int c0 = 0; c0 < K; c0 += 256) {
+    const int dk = K - c0 < 256 ? K - c0 : 256;
+    GCG_TRY(lincomb_launch(c, m, K, dk, -0.5, Z, K, Gm + c0, K, 1.5, Z2 + c0, K));
+  }
+  zz.Z = Z2;
+  if (m <= kEigMaxM) {
+    auto bt = backtr_kernel<4, (kEigMaxM + 31) / 32, 16>;
+    kernel_smem((const void*)bt, backtr_smem<16>(m));
+    bt<<<(K + kBtWarps * 4 - 1) / (kBtWarps * 4), 32 * kBtWarps, backtr_smem<16>(m), c->stream>>>(
+        m, K, Vr, tt, zz);
+  } else {
+    auto bt = backtr_kernel<1, kEigMaxBig / 32, 8>;
+    kernel_smem((const void*)bt, backtr_smem<8>(m));
+    bt<<<(K + kBtWarps - 1) / kBtWarps, 32 * kBtWarps, backtr_smem<8>(m), c->stream>>>(m, K, Vr,
+                                                                                      tt, zz);
+  }
+  vec_fix_rm_kernel<<<K, 256, 0, c->stream>>>(m, Z2, K, V, ldv);
+  g_launches += 2;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
 }
 
 // w (m, ascending) and V (row-major, ldv; eigenvector j in column j, sign rule
 // applied) of the symmetric m x m row-major A (symmetrised first when sym != 0).
 int dense_syev_tridiag(Ctx* c, int m, const double* A, long long lda, int sym, double* w,
                        double* V, long long ldv) {
-  if (m < 3 || m > kEigMaxM) return GCG_ERR_ARG;
-  const size_t mm = (size_t)m * m;
-  // workspace: d, e, tau (3m) | Vr (m^2) | Z (m^2) | inverse-iteration factors (6 m^2) | norms
-  GCG_TRY(ensure(c->dense, sizeof(double) * (3 * (size_t)m + 8 * mm + 8) + 256));
-  double* dd = (double*)c->dense.ptr;
-  double* ee = dd + m;
-  double* tt = ee + m;
-  double* Vr = tt + m;
-  double* Z = Vr + mm;
-  double* W = Z + mm;
-  double* norms = W + 6 * mm;
-  const size_t smem = tri_smem(m);
-  kernel_smem((const void*)tridiag_kernel, smem);
-  tridiag_kernel<<<1, kTriThreads, smem, c->stream>>>(m, A, lda, sym, dd, ee, tt, Vr);
-  bisect_kernel<<<(m + 7) / 8, 256, 0, c->stream>>>(m, dd, ee, w, norms);
-  for (int pass = 0; pass < 2; ++pass) {
-    const size_t ysm = sizeof(double) * 32 * (size_t)m;
-    kernel_smem((const void*)invit_kernel, ysm);
-    invit_kernel<<<(m + 31) / 32, 32, ysm, c->stream>>>(m, dd, ee, w, Z, W, pass, norms);
-    cluster_kernel<<<m, 256, 0, c->stream>>>(m, w, Z, norms);
-  }
-  double* G = W;            // the inverse-iteration factors are dead now
-  double* Z2 = W + mm;
-  loewdin_gram_kernel<<<m, 256, 0, c->stream>>>(m, Z, G);
-  loewdin_apply_kernel<<<m, 256, 0, c->stream>>>(m, Z, G, Z2);
-  Z = Z2;
-  kernel_smem((const void*)backtr_kernel, backtr_smem(m));
-  backtr_kernel<<<(m + kBtWarps * kBtCols - 1) / (kBtWarps * kBtCols), 32 * kBtWarps,
-                  backtr_smem(m), c->stream>>>(m, Vr, tt, Z);
-  vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, Z, V, ldv);
-  g_launches += 10;
-  GCG_CHECK_LAUNCH();
-  return GCG_OK;
+  return dense_syev_tridiag_range(c, m, A, lda, sym, 1, m, w, V, ldv);
 }
 
 }  // namespace gcg

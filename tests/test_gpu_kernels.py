@@ -241,7 +241,8 @@ def test_axpby_copy_scale_dots(dev):
     assert rel_err(host(out), (x * y).sum(0)) <= 1e-12
 
 
-@pytest.mark.parametrize("m", [1, 2, 5, 16, 33, 64, 65, 120, 200, 231, 232, 233])
+@pytest.mark.parametrize("m", [1, 2, 5, 16, 33, 64, 65, 120, 200, 224, 225, 231, 232, 233, 300,
+                               400, 500, 777, 1000, 1024, 1025])
 def test_syev_vs_lapack(dev, m):
     rng = np.random.default_rng(m)
     a = rng.standard_normal((m, m))
@@ -273,7 +274,7 @@ def _degenerate(m, seed, kind):
         a = (q * w) @ q.T
         return (a + a.T) / 2
     if kind == "rr":             # Rayleigh-Ritz shape: diag(Ritz values) coupled to a P/W block
-        d = 160 if m > 160 else m - 10
+        d = (3 * m) // 5 if m > 224 else (160 if m > 160 else m - 10)
         a = np.zeros((m, m))
         a[:d, :d] = np.diag(np.sort(rng.uniform(0.006, 0.3, d)))
         b = 1e-3 * rng.standard_normal((m - d, d))
@@ -288,7 +289,10 @@ def _degenerate(m, seed, kind):
 
 
 @pytest.mark.parametrize("m,kind", [(216, "lap3d"), (125, "lap3d"), (200, "clusters"),
-                                    (96, "clusters"), (200, "rr"), (120, "rr"), (100, "diag")])
+                                    (96, "clusters"), (200, "rr"), (120, "rr"), (100, "diag"),
+                                    (343, "lap3d"), (729, "lap3d"), (1000, "lap3d"),
+                                    (400, "clusters"), (1000, "clusters"), (400, "rr"),
+                                    (500, "rr"), (1000, "rr"), (500, "diag")])
 def test_syev_degenerate_spectra(dev, m, kind):
     """Eigensolver on the structures RR matrices have: exact multiplicities (grid
     symmetries), near-degenerate clusters, an exact zero, the diag + coupling shape.
@@ -320,9 +324,12 @@ def test_syev_degenerate_spectra(dev, m, kind):
 
 @pytest.mark.parametrize("m,lo,hi,workers", [(30, 1, 30, 1), (80, 1, 64, 1), (80, 5, 17, 1),
                                              (200, 1, 160, 1), (200, 1, 160, 4), (120, 3, 77, 3),
-                                             (16, 2, 9, 1)])
+                                             (16, 2, 9, 1), (400, 1, 320, 1), (500, 1, 300, 1),
+                                             (500, 1, 300, 4), (1000, 1, 600, 1),
+                                             (1000, 1, 600, 8), (400, 50, 77, 1), (1000, 990, 1000, 1)])
 def test_sym_eig_range_vs_lapack(dev, m, lo, hi, workers):
-    """sym_eig_range (dense.py:93-117): syevdx index ranges, optionally sliced."""
+    """sym_eig_range (dense.py:93-117): index ranges (eig.cu bisection + inverse
+    iteration of the requested indices), optionally sliced."""
     from paper_2111_06552_b200.dense import split_ranges, sym_eig_range
 
     rng = np.random.default_rng(m + lo)
@@ -338,6 +345,57 @@ def test_sym_eig_range_vs_lapack(dev, m, lo, hi, workers):
     assert np.abs(V - vv).max() <= 1e-9  # sign rule, non-degenerate random spectrum
     if workers > 1:
         assert len(split_ranges(lo, hi, workers)) > 1
+
+
+def test_eigensolver_never_calls_cusolver_up_to_1024(dev):
+    """Every BASELINE Rayleigh-Ritz order (m <= 1000, full spectrum and index ranges)
+    runs on the library's own kernels: the cuSOLVER call counter does not move."""
+    from paper_2111_06552_b200 import _lib
+    from paper_2111_06552_b200.dense import sym_eig_full, sym_eig_range
+
+    rng = np.random.default_rng(7)
+    n0 = _lib.cusolver_calls()
+    for m in (120, 400, 500, 1000):
+        a = rng.standard_normal((m, m))
+        a = (a + a.T) / 2
+        sym_eig_full(dev, rm(dev, a))
+        sym_eig_range(dev, rm(dev, a), 1, (3 * m) // 5)
+    torch.cuda.synchronize()
+    assert _lib.cusolver_calls() == n0
+    a = rng.standard_normal((1025, 1025))
+    sym_eig_full(dev, rm(dev, (a + a.T) / 2))  # beyond 1024: cuSOLVER syevd
+    assert _lib.cusolver_calls() == n0 + 1
+
+
+_GRID_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2111_06552_b200 import device as D
+dev = D.default_context()
+for m in (3, 4, 9, 65, 120, 200, 224):
+    rng = np.random.default_rng(m)
+    a = rng.standard_normal((m, m)); a = (a + a.T) / 2
+    w = dev.empty(m); v = dev.empty(m, m)
+    D.syev(dev, torch.from_numpy(a).to(dev.device), w, v)
+    ww = np.linalg.eigvalsh(a); lam = w.cpu().numpy(); V = v.cpu().numpy()
+    s = max(1.0, np.abs(ww).max())
+    assert np.abs(lam - ww).max() <= 1e-12 * s, m
+    assert np.abs(a @ V - V * lam).max() <= 1e-12 * s, m
+    assert np.abs(V.T @ V - np.eye(m)).max() <= 1e-12, m
+print("grid-ok")
+"""
+
+
+def test_grid_tridiagonalisation_small_orders():
+    """The multi-CTA tridiagonalisation (GCG_TRIGRID=1 forces it below 225, including
+    the one- and two-row-per-CTA edge cases m = 3, 4, 9) agrees with LAPACK."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, GCG_TRIGRID="1", GCG_SYEV="tri")
+    r = subprocess.run([sys.executable, "-c", _GRID_SCRIPT], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "grid-ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_syev_golden_m8(dev, golden):

@@ -133,8 +133,13 @@ def test_cfg3_baseline_against_reference_run():
         pytest.skip("golden_cfg3.json not generated")
     ref = json.load(open(path))
     pr = P.baseline_problem(3)
+    from paper_2111_06552_b200 import _lib
+
+    n_cusolver = _lib.cusolver_calls()
     rep = gcg_solve(pr.a, pr.b, SolverConfig(num_eigen=200, tol=1e-8, seed=0, init="normal",
                                              residual="relative", validate=False))
+    # every Rayleigh-Ritz solve (order up to 400) ran on eig.cu, none on cuSOLVER
+    assert _lib.cusolver_calls() == n_cusolver
     want = np.array(ref["eigenvalues"])
     assert rep.status == "converged"
     assert np.abs(rep.eigenvalues - want).max() / np.abs(want).max() <= 1e-9
