@@ -35,6 +35,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "async.cuh"
 #include "common.cuh"
 
@@ -44,7 +46,7 @@ extern int64_t g_launches;
 
 constexpr int kTriThreads = 1024;
 constexpr int kEigMaxM = 224;    // one-CTA tridiagonalisation (packed triangle in smem)
-constexpr int kEigMaxBig = 1024; // multi-CTA path (tridiag_grid_kernel)
+constexpr int kEigMaxBig = 1024; // multi-CTA path (tridiag_multi_kernel)
 
 __host__ __device__ inline int tri_off(int m, int j) { return j * m - (j * (j - 1)) / 2; }
 
@@ -506,6 +508,76 @@ __global__ void __launch_bounds__(32) invit_kernel(int m, int K, int j0, const d
   // the unnormalised solution is at most ~1/eps times the start vector
 }
 
+// 3'. Inverse iteration with the factors in shared memory: each pass factors
+// T - lambda_j I again (the same operations, so the same factors as a stored copy)
+// while eliminating the right-hand side — start vector (pass 0) or the current
+// column of Z (pass 1, preloaded into the rhs array) — then back-substitutes from
+// shared memory.  T threads per block (one eigenvalue each), [k][T] interleaved
+// arrays: R1 (1/pivot), U2, U3, Y.  Bitwise the same result as invit_kernel.
+static int invit_threads(int m) {
+  int t = 32;
+  while (t > 1 && 4 * sizeof(double) * (size_t)m * t > 160 * 1024) t >>= 1;
+  return t;
+}
+__global__ void invit_smem_kernel(int m, int K, int j0, const double* __restrict__ d,
+                                  const double* __restrict__ e, const double* __restrict__ lam,
+                                  InvitZ zz, int pass, const double* __restrict__ norms) {
+  __shared__ double sdv[kEigMaxBig], sev[kEigMaxBig];
+  extern __shared__ double fsm[];
+  const int T = blockDim.x;
+  for (int k = threadIdx.x; k < m; k += T) {
+    sdv[k] = d[k];
+    sev[k] = k + 1 < m ? e[k] : 0.0;
+  }
+  const int j = blockIdx.x * T + threadIdx.x;
+  double* R1 = fsm + threadIdx.x;
+  double* U2 = R1 + (size_t)m * T;
+  double* U3 = U2 + (size_t)m * T;
+  double* Y = U3 + (size_t)m * T;
+#define FS(arr, k) arr[(size_t)(k) * T]
+  if (pass == 1 && j < K)
+    for (int k = 0; k < m; ++k) FS(Y, k) = zz.at(k, j);
+  __syncthreads();
+  if (j >= K) return;
+  const double lj = lam[j];
+  const double tnorm = norms[0];
+  const double tiny = fmax(tnorm, 1e-300) * 2.220446049250313e-16;
+  auto fixp = [&](double u) { return fabs(u) < tiny ? (u < 0.0 ? -tiny : tiny) : u; };
+  const int jg = j0 + j;
+  double dg = sdv[0] - lj;
+  double sp = m > 1 ? sev[0] : 0.0;
+  double yk = pass == 0 ? start_entry(jg, 0) : FS(Y, 0);
+#pragma unroll 4
+  for (int k = 0; k + 1 < m; ++k) {
+    const double sub = sev[k];
+    const double a1 = sdv[k + 1] - lj;
+    const double s1 = k + 2 < m ? sev[k + 1] : 0.0;
+    const double bk1 = pass == 0 ? start_entry(jg, k + 1) : FS(Y, k + 1);
+    const bool sw = fabs(sub) > fabs(dg);
+    const double rp = __drcp_rn(sw ? sub : fixp(dg));
+    const double mult = (sw ? dg : sub) * rp;
+    FS(R1, k) = rp;
+    FS(U2, k) = sw ? a1 : sp;
+    FS(U3, k) = sw ? s1 : 0.0;
+    FS(Y, k) = sw ? bk1 : yk;
+    yk = fma(-mult, sw ? bk1 : yk, sw ? yk : bk1);
+    dg = fma(-mult, sw ? a1 : sp, sw ? sp : a1);
+    sp = sw ? -mult * s1 : s1;
+  }
+  FS(R1, m - 1) = __drcp_rn(fixp(dg));
+  FS(Y, m - 1) = yk;
+  double x2 = 0.0, x1 = FS(Y, m - 1) * FS(R1, m - 1);
+  zz.at(m - 1, j) = x1;
+#pragma unroll 4
+  for (int k = m - 2; k >= 0; --k) {
+    const double x0 = (FS(Y, k) - FS(U2, k) * x1 - FS(U3, k) * x2) * FS(R1, k);
+    zz.at(k, j) = x0;
+    x2 = x1;
+    x1 = x0;
+  }
+#undef FS
+}
+
 // Eigenvalues closer than kTightGap ||T|| form a tight cluster: inverse iteration
 // gives them vectors that are arbitrary inside the (near-)invariant subspace, so
 // they are Gram-Schmidt orthogonalised.  Every other pair is already orthogonal to
@@ -711,9 +783,7 @@ __global__ void __launch_bounds__(256) loewdin_apply_kernel(int m, const double*
 //          computes reflector v_{j+1} (dlarfg) — identical bits in every CTA.
 //     One barrier and a few L2 round trips per step; every element is read and
 //     written once per step from shared memory.  Same outputs as tridiag_kernel.
-constexpr int kTgThreads = 256;
-constexpr int kTgWarps = kTgThreads / 32;
-constexpr int kTgRows = 8;  // rows per CTA (one per warp); G = ceil(m / kTgRows)
+constexpr int kTgRows = 8;  // rows per CTA of the grid variant; G = ceil(m / kTgRows)
 
 struct TgArgs {
   int m;
@@ -724,12 +794,12 @@ struct TgArgs {
   double* e;
   double* tau;
   double* Vr;
-  double* pbuf;    // [2][m]  p of the current step (by parity)
-  double* rowbuf;  // [2][m]  row j+1 of A^(j)
-  double* part;    // [2][G]  per-CTA partial p'v
-  double* dlast;   // A^(m-3)(m-1, m-1)
-  unsigned* bar;   // grid barrier counter (zeroed before the launch)
-  int G;
+  double* pbuf;    // grid: [2][m]  p of the current step (by parity)
+  double* rowbuf;  // grid: [2][m]  row j+1 of A^(j)
+  double* part;    // grid: [2][G]  per-CTA partial p'v
+  double* dlast;   // grid: A^(m-3)(m-1, m-1)
+  unsigned* bar;   // grid: barrier counter (zeroed before the launch)
+  int G;           // CTAs (grid size / cluster size)
   int R;           // rows per CTA = ceil(m / G)
 };
 
@@ -743,36 +813,26 @@ __device__ __forceinline__ double tg_sym_at(const TgArgs& a, int i, int c) {
 __device__ __forceinline__ double tg_upd(double x, double vi, double wc, double wi, double vc) {
   return x - __dadd_rn(__dmul_rn(vi, wc), __dmul_rn(wi, vc));
 }
-__device__ __forceinline__ void tg_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-// fixed-order block sum (every thread gets the same value); red: 8 slots
+// fixed-order block sum (every thread gets the same value); red: NT/32 slots
+template <int NT>
 __device__ __forceinline__ double tg_block_sum(double v, double* red) {
   v = warp_sum(v);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < kTgWarps; ++w) s += red[w];
+  for (int w = 0; w < NT / 32; ++w) s += red[w];
   return s;
 }
-// reflector of column j (x[j..m-1] in shared memory) into vout; CTA 0 records d, e,
+// reflector of column j (x[j..m-1] in shared memory) into vout; block 0 records d, e,
 // tau and the reflector column of Vr.  Returns tau.
+template <int NT>
 __device__ double tg_reflector(const TgArgs& a, int j, const double* x, double* vout,
                                double* red) {
   const int m = a.m;
   double sq = 0.0;
-  for (int i = j + 2 + (int)threadIdx.x; i < m; i += kTgThreads) sq = fma(x[i], x[i], sq);
-  const double s = tg_block_sum(sq, red);
+  for (int i = j + 2 + (int)threadIdx.x; i < m; i += NT) sq = fma(x[i], x[i], sq);
+  const double s = tg_block_sum<NT>(sq, red);
   const double alpha = x[j + 1], djj = x[j];
   double t = 0.0, beta = alpha, scal = 0.0;
   if (s > 0.0) {
@@ -782,7 +842,7 @@ __device__ double tg_reflector(const TgArgs& a, int j, const double* x, double* 
     t = (beta - alpha) * __drcp_rn(beta);
     scal = __drcp_rn(alpha - beta);
   }
-  for (int i = threadIdx.x; i < m; i += kTgThreads) {
+  for (int i = threadIdx.x; i < m; i += NT) {
     const double vi = i <= j ? 0.0 : (i == j + 1 ? 1.0 : x[i] * scal);
     vout[i] = t != 0.0 ? vi : 0.0;
     if (blockIdx.x == 0 && i > j) a.Vr[(long long)j * m + i] = vi;
@@ -796,22 +856,43 @@ __device__ double tg_reflector(const TgArgs& a, int j, const double* x, double* 
   return t;
 }
 
-static size_t tg_smem(int m, int R) { return sizeof(double) * ((size_t)R * m + 4 * (size_t)m + 32); }
+template <int NT>
+static size_t tg_smem(int m, int R) {
+  return sizeof(double) * ((size_t)R * m + 4 * (size_t)m + 4 * (NT / 32) + 16);
+}
 
-__global__ void __launch_bounds__(kTgThreads, 1) tridiag_grid_kernel(TgArgs a) {
+// The multi-CTA Householder reduction; CLUSTER = false: G co-resident CTAs exchanging
+// through L2 with a grid barrier (1'), true: one thread-block cluster exchanging
+// through distributed shared memory with the cluster barrier (1'').  Per step: phase
+// A (no block barrier) processes a warp's rows in pairs — the shared vector loads
+// serve both, two independent reduction chains — and leaves per-warp partials of
+// p'v; one cluster / grid barrier; phase B issues every remote load first, each warp
+// reduces p'v itself (fixed order, identical everywhere), each thread forms w_i, the
+// updated column entry x_i and its share of ||x||^2 in registers; one block barrier
+// for the norm, the reflector is formed redundantly by every thread, a second block
+// barrier publishes it.  Entries are owned by thread i - (j + 1) mod NT; their (owner
+// CTA, slot) pairs advance incrementally with j (no divisions on the step path).
+constexpr int kTbSlots = 4;  // phase-B entries per thread: m <= NT * kTbSlots
+template <int NT, bool CLUSTER>
+__global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
+  namespace cgx = cooperative_groups;
+  constexpr int NW = NT / 32;
+  constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ double gsm[];
-  const int m = a.m, G = a.G, R = a.R, cta = blockIdx.x;
+  const int m = a.m, G = a.G, R = a.R;
+  const int cta = CLUSTER ? (int)cgx::this_cluster().block_rank() : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* S = gsm;  // [R][m]: local row r = global row cta + G r
   double* vb[4];
   for (int q = 0; q < 4; ++q) vb[q] = S + (size_t)R * m + (size_t)q * m;
-  double* red = vb[3] + m;  // [0,8) norm, [8,16) p'v warps, [16] p'v
+  double* part = vb[3] + m;  // cluster: [2][NW] per-warp partials of p'v, by step parity
+  double* red = part + 2 * NW;  // [0, NW) ||x||^2 warps, [NW, 2 NW) p'v warps (grid), [2 NW, +2) d, alpha
   for (int r = 0; r < R; ++r) {
     const int i = cta + G * r;
     if (i >= m) break;
-    for (int c = tid; c < m; c += kTgThreads) S[(size_t)r * m + c] = tg_sym_at(a, i, c);
+    for (int c = tid; c < m; c += NT) S[(size_t)r * m + c] = tg_sym_at(a, i, c);
   }
-  for (int c = tid; c < m; c += kTgThreads) {
+  for (int c = tid; c < m; c += NT) {
     vb[0][c] = 0.0;  // v_{-1}
     vb[1][c] = 0.0;  // w_{-1}
     vb[3][c] = tg_sym_at(a, c, 0);  // column 0
@@ -821,77 +902,207 @@ __global__ void __launch_bounds__(kTgThreads, 1) tridiag_grid_kernel(TgArgs a) {
   double* wprev = vb[1];
   double* vcur = vb[2];
   double* wnew = vb[3];
-  double t = tg_reflector(a, 0, wnew, vcur, red);
+  double t = tg_reflector<NT>(a, 0, wnew, vcur, red);
+  // phase-B entries i_q = j + 1 + tid + q NT: owner CTA and local slot, advanced per step
+  int own[kTbSlots], slt[kTbSlots];
+#pragma unroll
+  for (int q = 0; q < kTbSlots; ++q) {
+    const int i = 1 + tid + q * NT;
+    own[q] = i % G;
+    slt[q] = i / G;
+  }
+  int own1 = 1 % G, slt1 = 1 / G;  // row j + 1
+  if constexpr (CLUSTER) cgx::this_cluster().sync();  // rows loaded before remote reads
   for (int j = 0; j + 2 < m; ++j) {
     const int par = j & 1;
-    double* pb = a.pbuf + (size_t)par * m;
-    double* rb = a.rowbuf + (size_t)par * m;
-    // A: deferred update + p on this CTA's trailing rows
+    // A: deferred update + p on this CTA's trailing rows, two rows per pass
     double mypv = 0.0;
-    for (int r = warp; r < R; r += kTgWarps) {
-      const int i = cta + G * r;
-      if (i <= j || i >= m) continue;
-      double* Si = S + (size_t)r * m;
-      const double vpi = vprev[i], wpi = wprev[i];
-      const bool pub = i == j + 1;
-      double acc = 0.0;
+    const int rfirst = (j + 1 - cta + G - 1) / G > 0 ? (j + 1 - cta + G - 1) / G : 0;
+    for (int r0 = rfirst + warp; r0 < R; r0 += 2 * NW) {
+      const int r1 = r0 + NW;
+      const int i0 = cta + G * r0, i1 = cta + G * r1;
+      const bool ok0 = i0 < m, ok1 = r1 < R && i1 < m;
+      if (!ok0) break;
+      double* S0 = S + (size_t)r0 * m;
+      double* S1 = S + (size_t)(ok1 ? r1 : r0) * m;
+      const double vp0 = vprev[i0], wp0 = wprev[i0];
+      const double vp1 = ok1 ? vprev[i1] : 0.0, wp1 = ok1 ? wprev[i1] : 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
       for (int c = j + 1 + lane; c < m; c += 32) {
-        const double x = tg_upd(Si[c], vpi, wprev[c], wpi, vprev[c]);
-        Si[c] = x;
-        acc = fma(x, vcur[c], acc);
-        if (pub) __stcg(rb + c, x);
+        const double wc = wprev[c], vc = vprev[c], uc = vcur[c];
+        const double x0 = tg_upd(S0[c], vp0, wc, wp0, vc);
+        S0[c] = x0;
+        acc0 = fma(x0, uc, acc0);
+        double x1 = 0.0;
+        if (ok1) {
+          x1 = tg_upd(S1[c], vp1, wc, wp1, vc);
+          S1[c] = x1;
+          acc1 = fma(x1, uc, acc1);
+        }
+        if constexpr (!CLUSTER) {
+          if (i0 == j + 1) __stcg(a.rowbuf + (size_t)par * m + c, x0);
+          if (ok1 && i1 == j + 1) __stcg(a.rowbuf + (size_t)par * m + c, x1);
+        }
       }
-      acc = warp_sum(acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc0 += __shfl_xor_sync(FULL, acc0, o);
+        acc1 += __shfl_xor_sync(FULL, acc1, o);
+      }
       __syncwarp();
-      const double p = t * acc;
       if (lane == 0) {
-        __stcg(pb + i, p);
-        mypv = fma(p, vcur[i], mypv);
-        if (i == m - 1 && j == m - 3) __stcg(a.dlast, Si[m - 1]);
+        const double p0 = t * acc0, p1 = t * acc1;
+        if constexpr (CLUSTER) {
+          // p_i lives in column j of row i's own storage: dead since step j-1
+          S0[j] = p0;
+          if (ok1) S1[j] = p1;
+        } else {
+          __stcg(a.pbuf + (size_t)par * m + i0, p0);
+          if (ok1) __stcg(a.pbuf + (size_t)par * m + i1, p1);
+          if (j == m - 3) {
+            if (i0 == m - 1) __stcg(a.dlast, S0[m - 1]);
+            if (ok1 && i1 == m - 1) __stcg(a.dlast, S1[m - 1]);
+          }
+        }
+        mypv = fma(p0, vcur[i0], mypv);
+        if (ok1) mypv = fma(p1, vcur[i1], mypv);
       }
     }
-    if (lane == 0) red[8 + warp] = mypv;
+    if constexpr (CLUSTER) {
+      if (lane == 0) part[par * NW + warp] = mypv;
+      cgx::this_cluster().sync();
+    } else {
+      if (lane == 0) red[NW + warp] = mypv;
+      __syncthreads();
+      if (tid == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += red[NW + w];
+        __stcg(a.part + (size_t)par * G + cta, s);
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+        const unsigned target = (unsigned)G * (unsigned)(j + 1);
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+        } while (v < target);
+      }
+      __syncthreads();
+    }
+    // B: remote loads first
+    double pv = 0.0, p1 = 0.0;
+    double pr[kTbSlots], rw[kTbSlots];
+    if constexpr (CLUSTER) {
+      cgx::cluster_group cl = cgx::this_cluster();
+      for (int idx = lane; idx < G * NW; idx += 32)
+        pv += *cl.map_shared_rank(part + par * NW + (idx % NW), idx / NW);
+      p1 = *cl.map_shared_rank(S + (size_t)slt1 * m + j, own1);
+      const double* rowj1 = cl.map_shared_rank(S + (size_t)slt1 * m, own1);
+#pragma unroll
+      for (int q = 0; q < kTbSlots; ++q) {
+        const int i = j + 1 + tid + q * NT;
+        pr[q] = i < m ? *cl.map_shared_rank(S + (size_t)slt[q] * m + j, own[q]) : 0.0;
+        rw[q] = i < m ? rowj1[i] : 0.0;
+      }
+    } else {
+      for (int q = lane; q < G; q += 32) pv += __ldcg(a.part + (size_t)par * G + q);
+      p1 = __ldcg(a.pbuf + (size_t)par * m + j + 1);
+#pragma unroll
+      for (int q = 0; q < kTbSlots; ++q) {
+        const int i = j + 1 + tid + q * NT;
+        pr[q] = i < m ? __ldcg(a.pbuf + (size_t)par * m + i) : 0.0;
+        rw[q] = i < m ? __ldcg(a.rowbuf + (size_t)par * m + i) : 0.0;
+      }
+    }
+    pv = warp_sum(pv);  // every warp, same order
+    const double a2 = -0.5 * t * pv;
+    const double vj1 = vcur[j + 1];
+    const double wj1 = fma(a2, vj1, p1);
+    double xq[kTbSlots];
+    double sq = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTbSlots; ++q) {
+      const int i = j + 1 + tid + q * NT;
+      xq[q] = 0.0;
+      if (i < m) {
+        const double vi = vcur[i];
+        const double wi = fma(a2, vi, pr[q]);
+        wnew[i] = wi;
+        const double x = tg_upd(rw[q], vi, wj1, wi, vj1);
+        xq[q] = x;
+        if (i >= j + 3) sq = fma(x, x, sq);
+        if (i == j + 1) red[2 * NW] = x;
+        if (i == j + 2) red[2 * NW + 1] = x;
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) red[warp] = sq;
     __syncthreads();
-    if (tid == 0) {
+    const double djj = red[2 * NW], alpha = red[2 * NW + 1];
+    if (j + 3 < m) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < kTgWarps; ++w) s += red[8 + w];
-      __stcg(a.part + (size_t)par * G + cta, s);
-    }
-    tg_barrier(a.bar, (unsigned)G * (unsigned)(j + 1));
-    // B (redundant in every CTA): p'v in fixed order, w_j, column j+1, reflector j+1
-    if (warp == 0) {
-      double s = 0.0;
-      for (int q = lane; q < G; q += 32) s += __ldcg(a.part + (size_t)par * G + q);
-      s = warp_sum(s);
-      if (lane == 0) red[16] = s;
-    }
-    __syncthreads();
-    const double a2 = -0.5 * t * red[16];
-    for (int i = j + 1 + tid; i < m; i += kTgThreads) wnew[i] = fma(a2, vcur[i], __ldcg(pb + i));
-    __syncthreads();
-    double* xb = wprev;  // dead after A: column j+1 of A^(j+1)
-    double* vn = vprev;  // dead after A: v_{j+1}
-    const double wj1 = wnew[j + 1], vj1 = vcur[j + 1];
-    for (int i = j + 1 + tid; i < m; i += kTgThreads)
-      xb[i] = tg_upd(__ldcg(rb + i), vcur[i], wj1, wnew[i], vj1);
-    __syncthreads();
-    if (j + 3 < m) {
-      t = tg_reflector(a, j + 1, xb, vn, red);
-    } else if (cta == 0 && tid == 0) {  // last 2 x 2 block
-      a.d[m - 2] = xb[m - 2];
-      a.e[m - 2] = xb[m - 1];
+      for (int w = 0; w < NW; ++w) s += red[w];
+      double tn = 0.0, beta = alpha, scal = 0.0;
+      if (s > 0.0) {
+        const double nrm2 = fma(alpha, alpha, s);
+        const double rn = rsqrt(nrm2);  // beta = -sign(alpha) ||x||
+        beta = alpha >= 0.0 ? -nrm2 * rn : nrm2 * rn;
+        tn = (beta - alpha) * __drcp_rn(beta);
+        scal = __drcp_rn(alpha - beta);
+      }
+      double* vn = vprev;  // dead after A: v_{j+1}
+#pragma unroll
+      for (int q = 0; q < kTbSlots; ++q) {
+        const int i = j + 1 + tid + q * NT;
+        if (i < m) {
+          const double vi = i == j + 1 ? 0.0 : (i == j + 2 ? 1.0 : xq[q] * scal);
+          vn[i] = tn != 0.0 ? vi : 0.0;
+          if (blockIdx.x == 0 && i > j + 1) a.Vr[(long long)(j + 1) * m + i] = vi;
+        }
+      }
+      if (blockIdx.x == 0 && tid == 0) {
+        a.d[j + 1] = djj;
+        a.e[j + 1] = beta;
+        a.tau[j + 1] = tn;
+      }
+      t = tn;
+    } else if (blockIdx.x == 0 && tid == 0) {  // last 2 x 2 block
+      double dl;
+      if constexpr (CLUSTER)
+        dl = *cgx::this_cluster().map_shared_rank(S + (size_t)((m - 1) / G) * m + (m - 1),
+                                                  (m - 1) % G);
+      else
+        dl = __ldcg(a.dlast);
+      a.d[m - 2] = djj;
+      a.e[m - 2] = alpha;
       a.tau[m - 2] = 0.0;
-      a.d[m - 1] = tg_upd(__ldcg(a.dlast), vcur[m - 1], wnew[m - 1], wnew[m - 1], vcur[m - 1]);
+      a.d[m - 1] = tg_upd(dl, vcur[m - 1], wnew[m - 1], wnew[m - 1], vcur[m - 1]);
     }
+    __syncthreads();
     // rotate: (v_j, w_j) become the deferred update, v_{j+1} the current reflector
+    double* old_w = wprev;
+    double* old_v = vprev;
     vprev = vcur;
     wprev = wnew;
-    vcur = vn;
-    wnew = xb;
-    __syncthreads();
+    vcur = old_v;
+    wnew = old_w;
+#pragma unroll
+    for (int q = 0; q < kTbSlots; ++q)
+      if (++own[q] == G) {
+        own[q] = 0;
+        ++slt[q];
+      }
+    if (++own1 == G) {
+      own1 = 0;
+      ++slt1;
+    }
   }
+  if constexpr (CLUSTER) cgx::this_cluster().sync();  // nobody leaves while read remotely
 }
+
+constexpr int kTgThreads = 256;  // grid variant
+constexpr int kTcThreads = 512;  // cluster variant
 
 // V[i*ldv + j] = sign_j * Z[i*ldz + j] (row-major Z, column j) with the sign rule
 __global__ void vec_fix_rm_kernel(int m, const double* Z, long long ldz, double* V, long long ldv) {
@@ -942,10 +1153,63 @@ bool dense_syev_tridiag_ok(int m) {
   return m >= 3 && m <= kEigMaxBig;
 }
 
-static bool use_grid_tridiag(int m) {
-  // GCG_TRIGRID=1: the multi-CTA reduction for m <= 224 too (A/B)
-  static const bool force = getenv("GCG_TRIGRID") && getenv("GCG_TRIGRID")[0] == '1';
-  return m > kEigMaxM || force;
+// Tridiagonalisation variant by order: 'o' one CTA (m <= 224), 'c' one cluster
+// (m <= 600), 'g' co-resident grid.  GCG_TRIMODE=o|c|g forces one where it applies (A/B).
+constexpr int kTcMaxM = 600;
+static char tridiag_mode(int m) {
+  static const char* env = getenv("GCG_TRIMODE");
+  static const char force = env ? env[0] : 0;
+  static const bool legacy_grid = getenv("GCG_TRIGRID") && getenv("GCG_TRIGRID")[0] == '1';
+  if (legacy_grid) return 'g';
+  if (force == 'o' && m <= kEigMaxM) return 'o';
+  if (force == 'g') return 'g';
+  if (force == 'c' && m <= kTcMaxM) return 'c';
+  // measured (scripts/eig_bench.py, profiles/r02_eig_modes.txt): one CTA up to 128, the
+  // cluster to 256, the co-resident grid above (the cluster's 16 CTAs run out of
+  // parallelism in phase A past ~300)
+  if (m <= 128) return 'o';
+  return m <= 256 ? 'c' : 'g';
+}
+static bool use_grid_tridiag(int m) { return tridiag_mode(m) != 'o'; }
+
+static int tridiag_cluster_launch(Ctx* c, int m, const double* A, long long lda, int sym,
+                                  double* dd, double* ee, double* tt, double* Vr) {
+  const int C = m <= 256 ? 8 : 16;
+  const int R = (m + C - 1) / C;
+  TgArgs a = {};
+  a.m = m;
+  a.A = A;
+  a.lda = lda;
+  a.sym = sym;
+  a.d = dd;
+  a.e = ee;
+  a.tau = tt;
+  a.Vr = Vr;
+  a.G = C;
+  a.R = R;
+  const size_t smem = tg_smem<kTcThreads>(m, R);
+  auto kern = tridiag_multi_kernel<kTcThreads, true>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_done = true;
+  }
+  kernel_smem((const void*)kern, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GCG_TRY(cuda_status(cudaLaunchKernelEx(&cfg, kern, a)));
+  ++g_launches;
+  return GCG_OK;
 }
 
 static int tridiag_grid_launch(Ctx* c, int m, const double* A, long long lda, int sym, double* dd,
@@ -971,19 +1235,41 @@ static int tridiag_grid_launch(Ctx* c, int m, const double* A, long long lda, in
   a.G = G;
   a.R = R;
   GCG_TRY(cuda_status(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), c->stream)));
-  const size_t smem = tg_smem(m, R);
-  kernel_smem((const void*)tridiag_grid_kernel, smem);
+  const size_t smem = tg_smem<kTgThreads>(m, R);
+  auto kern = tridiag_multi_kernel<kTgThreads, false>;
+  kernel_smem((const void*)kern, smem);
   void* args[] = {&a};
-  GCG_TRY(cuda_status(cudaLaunchCooperativeKernel((const void*)tridiag_grid_kernel, dim3(G),
-                                                  dim3(kTgThreads), args, smem, c->stream)));
+  GCG_TRY(cuda_status(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kTgThreads),
+                                                  args, smem, c->stream)));
   ++g_launches;
+  return GCG_OK;
+}
+
+// back-transform for m <= 224: COLS columns per warp (GCG_BTCOLS=1|2|4, default 2):
+// fewer columns per warp = more CTAs and a shorter per-reflector chain
+static int backtr_small(Ctx* c, int m, int K, const double* Vr, const double* tt, InvitZ zz) {
+  static const int cols = getenv("GCG_BTCOLS") ? atoi(getenv("GCG_BTCOLS")) : 2;
+  constexpr int RW = (kEigMaxM + 31) / 32;
+#define BT(C)                                                                               \
+  do {                                                                                      \
+    auto bt = backtr_kernel<C, RW, 16>;                                                     \
+    kernel_smem((const void*)bt, backtr_smem<16>(m));                                       \
+    bt<<<(K + kBtWarps * C - 1) / (kBtWarps * C), 32 * kBtWarps, backtr_smem<16>(m),        \
+         c->stream>>>(m, K, Vr, tt, zz);                                                    \
+  } while (0)
+  if (cols == 1) BT(1);
+  else if (cols == 4) BT(4);
+  else BT(2);
+#undef BT
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
   return GCG_OK;
 }
 
 // Eigenpairs il..iu (1-based inclusive; K = iu - il + 1) of the symmetric m x m
 // row-major A (symmetrised first when sym != 0): w (K values, ascending) and V
 // (row-major m x K, ldv; the sign rule applied).  No cuSOLVER:
-//   tridiagonalisation (one CTA for m <= 224, tridiag_grid_kernel above), bisection
+//   tridiagonalisation (one CTA, one cluster or a co-resident grid: tridiag_mode), bisection
 //   of the requested indices only, inverse iteration + tight-cluster Gram-Schmidt
 //   (twice), Loewdin, back-transform, sign rule.
 // The full spectrum of an order <= 224 keeps the column-major one-CTA kernels; every
@@ -994,7 +1280,7 @@ int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int 
   if (m < 3 || m > kEigMaxBig || il < 1 || iu < il || iu > m) return GCG_ERR_ARG;
   const int K = iu - il + 1;
   const bool grid = use_grid_tridiag(m);
-  const bool small = !grid && K == m;  // the original one-CTA pipeline
+  const bool small = m <= kEigMaxM && K == m;  // column-major Z, one-CTA Loewdin kernels
   const size_t mm = (size_t)m * m, mk = (size_t)m * K;
   const bool ys_shared = 32 * (size_t)m * sizeof(double) <= 64 * 1024;
   // workspace: d, e, tau (3m) | Vr (m^2) | Z (mK) | inverse-iteration factors (6 mK)
@@ -1012,7 +1298,9 @@ int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int 
   double* Gm = Z2 + mk;
   double* gw = Gm + (size_t)K * K;
   double* norms = gw + 6 * (size_t)m + 2 * kNumSMs + 16;
-  if (grid) {
+  if (grid && tridiag_mode(m) == 'c') {
+    GCG_TRY(tridiag_cluster_launch(c, m, A, lda, sym, dd, ee, tt, Vr));
+  } else if (grid) {
     GCG_TRY(tridiag_grid_launch(c, m, A, lda, sym, dd, ee, tt, Vr, gw));
   } else {
     const size_t smem = tri_smem(m);
@@ -1026,11 +1314,20 @@ int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int 
   zz.Z = Z;
   zz.ldz = small ? 0 : K;
   zz.m = m;
+  static const bool invit_global = getenv("GCG_INVIT") && getenv("GCG_INVIT")[0] == 'g';
   const size_t ysm = ys_shared ? sizeof(double) * 32 * (size_t)m : 0;
+  const int it = invit_threads(m);
+  const size_t fsm = 4 * sizeof(double) * (size_t)m * it;
   for (int pass = 0; pass < 2; ++pass) {
-    kernel_smem((const void*)invit_kernel, ysm);
-    invit_kernel<<<(K + 31) / 32, 32, ysm, c->stream>>>(m, K, il - 1, dd, ee, w, zz, W, pass,
-                                                        norms, ys_shared ? 1 : 0);
+    if (invit_global) {  // A/B: factors stored in global memory by pass 0, reused by pass 1
+      kernel_smem((const void*)invit_kernel, ysm);
+      invit_kernel<<<(K + 31) / 32, 32, ysm, c->stream>>>(m, K, il - 1, dd, ee, w, zz, W, pass,
+                                                          norms, ys_shared ? 1 : 0);
+    } else {
+      kernel_smem((const void*)invit_smem_kernel, fsm);
+      invit_smem_kernel<<<(K + it - 1) / it, it, fsm, c->stream>>>(m, K, il - 1, dd, ee, w, zz,
+                                                                   pass, norms);
+    }
     cluster_kernel<<<K, 256, 0, c->stream>>>(m, K, w, zz, norms);
   }
   g_launches += 5;
@@ -1041,10 +1338,7 @@ int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int 
     loewdin_gram_kernel<<<m, 256, 0, c->stream>>>(m, Z, G);
     loewdin_apply_kernel<<<m, 256, 0, c->stream>>>(m, Z, G, Zs);
     zz.Z = Zs;
-    auto bt = backtr_kernel<4, (kEigMaxM + 31) / 32, 16>;
-    kernel_smem((const void*)bt, backtr_smem<16>(m));
-    bt<<<(m + kBtWarps * 4 - 1) / (kBtWarps * 4), 32 * kBtWarps, backtr_smem<16>(m), c->stream>>>(
-        m, K, Vr, tt, zz);
+    GCG_TRY(backtr_small(c, m, K, Vr, tt, zz));
     vec_fix_kernel<<<m, 256, 0, c->stream>>>(m, Zs, V, ldv);
     g_launches += 4;
     GCG_CHECK_LAUNCH();
@@ -1059,10 +1353,7 @@ int dense_syev_tridiag_range(Ctx* c, int m, const double* A, long long lda, int 
   }
   zz.Z = Z2;
   if (m <= kEigMaxM) {
-    auto bt = backtr_kernel<4, (kEigMaxM + 31) / 32, 16>;
-    kernel_smem((const void*)bt, backtr_smem<16>(m));
-    bt<<<(K + kBtWarps * 4 - 1) / (kBtWarps * 4), 32 * kBtWarps, backtr_smem<16>(m), c->stream>>>(
-        m, K, Vr, tt, zz);
+    GCG_TRY(backtr_small(c, m, K, Vr, tt, zz));
   } else {
     auto bt = backtr_kernel<1, kEigMaxBig / 32, 8>;
     kernel_smem((const void*)bt, backtr_smem<8>(m));

@@ -6,8 +6,11 @@ eigenvector signs fixed so the largest-magnitude entry is positive (first
 index on ties).
 
 Device matrices are row-major float64 tensors.  Full spectra of orders <= 64
-run the one-CTA Jacobi kernel, larger ones cuSOLVER syevd; index ranges run
-cuSOLVER syevdx (see csrc/dense.cu).  The split-range solve of the paper's
+run the one-CTA Jacobi kernel; orders 65..1024 (every BASELINE Rayleigh-Ritz
+order, up to cfg5's 1000) and every index range run csrc/eig.cu: Householder
+tridiagonalisation (one CTA up to 224, multi-CTA above), bisection of the
+requested indices, inverse iteration, back-transformation — no cuSOLVER
+(``_lib.cusolver_calls()`` counts the calls beyond 1024).  The split-range solve of the paper's
 parallel Rayleigh-Ritz is ``sym_eig_range(..., workers=w)``
 on one device, and ``sym_eig_range_split`` across the ranks of a distributed
 solve (each rank one slice, then an ordered all-gather).

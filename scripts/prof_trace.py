@@ -39,3 +39,16 @@ for s, e, nm in ev[lo:hi]:
         print(f"gap {gap:7.1f} us  dur {e - s:7.1f} us  {nm}")
     last = max(last, e)
 print(f"iteration span {ev[hi][0] - ev[lo][0]:.1f} us, idle {tot_gap:.1f} us, events {hi - lo}")
+# whole-solve summary: span, busy (union of kernel intervals), idle
+busy, cur_s, cur_e = 0.0, None, None
+for s, e, nm in ev:
+    if cur_e is None or s > cur_e:
+        if cur_e is not None:
+            busy += cur_e - cur_s
+        cur_s, cur_e = s, e
+    else:
+        cur_e = max(cur_e, e)
+busy += cur_e - cur_s
+span = ev[-1][1] - ev[0][0]
+print(f"solve: span {span / 1e3:.2f} ms  busy {busy / 1e3:.2f} ms  idle {(span - busy) / 1e3:.2f} ms  "
+      f"kernels {len(ev)}  iteration-{it0} gaps {tot_gap:.1f} us")

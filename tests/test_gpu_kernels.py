@@ -372,7 +372,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2111_06552_b200 import device as D
 dev = D.default_context()
-for m in (3, 4, 9, 65, 120, 200, 224):
+for m in (3, 4, 9, 17, 65, 120, 200, 224):
     rng = np.random.default_rng(m)
     a = rng.standard_normal((m, m)); a = (a + a.T) / 2
     w = dev.empty(m); v = dev.empty(m, m)
@@ -386,13 +386,15 @@ print("grid-ok")
 """
 
 
-def test_grid_tridiagonalisation_small_orders():
-    """The multi-CTA tridiagonalisation (GCG_TRIGRID=1 forces it below 225, including
-    the one- and two-row-per-CTA edge cases m = 3, 4, 9) agrees with LAPACK."""
+@pytest.mark.parametrize("mode", ["g", "c", "o"])
+def test_tridiagonalisation_variants_small_orders(mode):
+    """Each tridiagonalisation variant forced below its default range (GCG_TRIMODE:
+    g = co-resident grid, c = one cluster, o = one CTA), including the one- and
+    two-row-per-CTA edge cases m = 3, 4, 9, agrees with LAPACK."""
     import subprocess
     import sys
 
-    env = dict(os.environ, GCG_TRIGRID="1", GCG_SYEV="tri")
+    env = dict(os.environ, GCG_TRIMODE=mode, GCG_SYEV="tri")
     r = subprocess.run([sys.executable, "-c", _GRID_SCRIPT], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "grid-ok" in r.stdout, r.stdout + r.stderr
