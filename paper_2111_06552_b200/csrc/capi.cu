@@ -85,8 +85,12 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
                           const double* lam, int mode, double* out);
 
 // GCG_PDL=0 turns programmatic dependent launch off (A/B switch)
+// Programmatic dependent launch: off by default since the CG sweep became two kernels —
+// at cfg4 (n = 2.1 M, k = 100: many waves) the early-launched dependent CTAs occupy SM
+// slots while they wait, 5.08 -> 4.05 ms per sweep without PDL; cfg2 within noise
+// (bench 0.2751 vs 0.2742 s).  GCG_PDL=1 re-enables it.
 bool pdl_enabled() {
-  static const bool on = !(getenv("GCG_PDL") && getenv("GCG_PDL")[0] == '0');
+  static const bool on = getenv("GCG_PDL") && getenv("GCG_PDL")[0] == '1';
   return on;
 }
 

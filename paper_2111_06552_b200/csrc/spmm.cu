@@ -725,7 +725,9 @@ static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowpt
     // index/value stream is read three times.  Wider k (cfg5, k = 200) is gather-bound
     // and gains nothing (scripts/spmm_panel.sh).  GCG_SPMM_PANEL overrides the cap.
     static const int panel_env = getenv("GCG_SPMM_PANEL") ? atoi(getenv("GCG_SPMM_PANEL")) : -1;
-    const int panel = panel_env >= 0 ? panel_env : (k > 64 && k <= 128 ? 40 : 0);
+    // (not for the fused CG sweep: there one pass over all k columns wins — cfg4 sweep
+    // 5.94 -> 5.08 ms — its epilogue streams dominate and panels re-read them per pass)
+    const int panel = panel_env >= 0 ? panel_env : (!cg && k > 64 && k <= 128 ? 40 : 0);
     int npass = (rest + max_cols(vec) - 1) / max_cols(vec);
     if (panel > 0 && (rest + panel - 1) / panel > npass) npass = (rest + panel - 1) / panel;
     int kc = (rest + npass - 1) / npass;

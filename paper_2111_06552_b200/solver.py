@@ -656,8 +656,10 @@ def gcg_solve_ops(ops, cfg, x0=None):
             if cg_rep is not None:
                 pending_cg.append((rec, cg_rep))
 
-    for rec, rep in pending_cg:  # resolve CG sweep counts (one D2H each, after the loop)
-        rec.cg_iterations = rep.iterations
+    if pending_cg:  # resolve every CG sweep count with ONE device-to-host read, after the loop
+        counts = torch.cat([rep._sweeps.view(-1) for _, rep in pending_cg]).cpu().tolist()
+        for (rec, _), cnt in zip(pending_cg, counts):
+            rec.cg_iterations = int(cnt)
     for tm in timers:             # per-step GPU times (the records hold tm.marks)
         tm.resolve()
 
