@@ -187,7 +187,12 @@ int gcg_col_scale_copy(void* ctx, int64_t n, int64_t k, const double* s, const d
  *                          recv_buf into the ghost rows after;
  *   callback(1, k, user): allreduce — red_buf[0:k] holds this rank's column sums on
  *                          entry and must hold the global sums on return.
- * Both are called from the enqueuing thread, stream-ordered on the context stream. */
+ * Both are called from the enqueuing thread, stream-ordered on the context stream.
+ * With nccl_comm set (gcg_nccl_comm_create) there is no callback: the library
+ * exchanges the halo itself (grouped ncclSend / ncclRecv with each of the npeer
+ * neighbours: send_buf rows [peer_send_off[q], peer_send_off[q+1]) to peer_rank[q],
+ * recv_buf rows [peer_recv_off[q], ...) from it) and sums red_buf with ncclAllReduce,
+ * all on the context stream — no host round trip inside the CG. */
 typedef struct gcg_cg_dist {
   int64_t nghost;
   int64_t nsend;
@@ -197,7 +202,21 @@ typedef struct gcg_cg_dist {
   double* red_buf;         /* device [k] */
   int (*callback)(int op, int k, void* user);
   void* user;
+  void* nccl_comm;              /* ncclComm_t or NULL (host callbacks) */
+  int32_t npeer;
+  const int32_t* peer_rank;     /* host [npeer] */
+  const int64_t* peer_send_off; /* host [npeer + 1], rows of send_buf */
+  const int64_t* peer_recv_off; /* host [npeer + 1], rows of recv_buf */
 } gcg_cg_dist;
+
+/* ---- native NCCL (loaded at run time; gcg_nccl_available() == 0 without it) ---- */
+int gcg_nccl_available(void);                       /* NCCL version code, 0 if absent */
+int gcg_nccl_unique_id(uint8_t* out128);            /* rank 0: the bootstrap id */
+int gcg_nccl_comm_create(void* ctx, int32_t nranks, int32_t rank, const uint8_t* id128,
+                         void** comm);
+int gcg_nccl_comm_destroy(void* comm);
+/* in-place sum of count doubles over the communicator, on the context stream */
+int gcg_nccl_allreduce_sum(void* ctx, void* comm, double* buf, int64_t count);
 
 int gcg_block_cg_dist(void* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
                       const int32_t* colidx, const double* val, double diag_shift, int64_t k,

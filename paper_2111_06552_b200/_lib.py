@@ -22,6 +22,11 @@ _SIGS = {
     "gcg_status_string": [_int],
     "gcg_launch_count": [],
     "gcg_cusolver_calls": [],
+    "gcg_nccl_available": [],
+    "gcg_nccl_unique_id": [_ptr],
+    "gcg_nccl_comm_create": [_ptr, _i32, _i32, _ptr, C.POINTER(_ptr)],
+    "gcg_nccl_comm_destroy": [_ptr],
+    "gcg_nccl_allreduce_sum": [_ptr, _ptr, _ptr, _i64],
     "gcg_ctx_create": [C.POINTER(_ptr), _ptr],
     "gcg_ctx_destroy": [_ptr],
     "gcg_ctx_set_stream": [_ptr, _ptr],
@@ -137,6 +142,11 @@ class CgDist(C.Structure):
         ("red_buf", C.c_void_p),
         ("callback", CG_DIST_CALLBACK),
         ("user", C.c_void_p),
+        ("nccl_comm", C.c_void_p),
+        ("npeer", C.c_int32),
+        ("peer_rank", C.c_void_p),
+        ("peer_send_off", C.c_void_p),
+        ("peer_recv_off", C.c_void_p),
     ]
 
 _lib = None

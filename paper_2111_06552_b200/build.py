@@ -21,7 +21,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libgcgb200.so")
-SOURCES = ["capi.cu", "spmm.cu", "blas.cu", "tsgemm.cu", "cg.cu", "dense.cu", "mmio.cu", "orth.cu", "gen.cu", "eig.cu"]
+SOURCES = ["capi.cu", "spmm.cu", "blas.cu", "tsgemm.cu", "cg.cu", "dense.cu", "mmio.cu", "orth.cu", "gen.cu", "eig.cu", "nccl.cu"]
 HEADERS = ["common.cuh", "async.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
     f"-I{os.path.join(ROOT, 'include')}",
 ]
-LINK_LIBS = ["-lcusolver", "-lcublas", "-lcudart"]
+LINK_LIBS = ["-lcusolver", "-lcublas", "-lcudart", "-ldl"]
 
 
 def _nvcc():

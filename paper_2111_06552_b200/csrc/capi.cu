@@ -532,7 +532,10 @@ int gcg_block_cg_dist(void* p, int64_t n, int64_t nnz, const int32_t* rowptr,
                       double* d_relres, const gcg_cg_dist* dist) {
   Ctx* c = CTX(p);
   if (!c || n <= 0 || k <= 0 || ldr < k || ldx < k || max_iters < 0 || !dist ||
-      !dist->callback || !dist->red_buf)
+      (!dist->callback && !dist->nccl_comm) || !dist->red_buf)
+    return GCG_ERR_ARG;
+  if (dist->nccl_comm && dist->npeer > 0 &&
+      (!dist->peer_rank || !dist->peer_send_off || !dist->peer_recv_off))
     return GCG_ERR_ARG;
   if (!d_sweeps || !d_converged || !d_frozen || !d_relres) return GCG_ERR_ARG;
   return block_cg_launch(c, n, nnz, rowptr, colidx, val, diag_shift, (int)k, rhs, ldr, nullptr, 0, x, ldx,

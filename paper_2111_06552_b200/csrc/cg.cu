@@ -315,9 +315,16 @@ int gather_rows_launch(Ctx* c, int nidx, const int* idx, int k, const double* X,
 // Row-partitioned runs: refresh the ghost rows [n, n + nghost) of a block
 // (ld) from the neighbours — gather the owned rows they need into send_buf,
 // let the host exchange send_buf -> recv_buf, scatter into the ghost rows.
+int nccl_cg_halo(Ctx* c, const gcg_cg_dist* d, int k);
+int nccl_cg_allreduce(Ctx* c, const gcg_cg_dist* d, int k);
+
 static int dist_halo(Ctx* c, const gcg_cg_dist* d, long long n, int k, double* X, long long ld) {
   if (d->nsend > 0) GCG_TRY(gather_rows_launch(c, d->nsend, d->send_idx, k, X, ld, d->send_buf, k));
-  if (d->callback(0, k, d->user) != 0) return GCG_ERR_ARG;
+  if (d->nccl_comm) {
+    GCG_TRY(nccl_cg_halo(c, d, k));  // grouped send / recv on the context stream
+  } else if (d->callback(0, k, d->user) != 0) {
+    return GCG_ERR_ARG;
+  }
   if (d->nghost > 0) GCG_TRY(copy_launch(c, d->nghost, k, d->recv_buf, k, X + n * ld, ld));
   return GCG_OK;
 }
@@ -327,6 +334,7 @@ static int dist_halo(Ctx* c, const gcg_cg_dist* d, long long n, int k, double* X
 static int dist_reduce(Ctx* c, const gcg_cg_dist* d, const double* part, int nparts, int k) {
   GCG_TRY(reduce_partials(c, part, nparts, k, d->red_buf, 1, 0));
   ++g_launches;
+  if (d->nccl_comm) return nccl_cg_allreduce(c, d, k);
   if (d->callback(1, k, d->user) != 0) return GCG_ERR_ARG;
   return GCG_OK;
 }

@@ -173,6 +173,37 @@ def slab_problem(dev, comm, cfg, scale=None, plane_align=True):
     return DistProblem(dev, part, comm, n, A=A), meta
 
 
+class NativeNccl:
+    """One ncclComm_t created inside libgcgb200 (gcg_nccl_comm_create), bootstrapped by
+    broadcasting rank 0's unique id over the torch process group."""
+
+    def __init__(self, comm):
+        dev = D.default_context()
+        if not _lib.load().gcg_nccl_available():
+            raise _lib.DeviceError("libnccl.so.2 could not be loaded for the native communicator")
+        uid = (C.c_uint8 * 128)()
+        if comm.rank == 0:
+            _lib.call("gcg_nccl_unique_id", uid)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev.device)
+        dist.broadcast(t, src=0, group=comm.group)
+        uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        _lib.call("gcg_nccl_comm_create", dev.h, comm.size, comm.rank, uid, C.byref(h))
+        self.handle = h
+        self.dev = dev
+
+    def allreduce_sum(self, t):
+        """In-place sum of a contiguous float64 device tensor, on the library stream."""
+        _lib.call("gcg_nccl_allreduce_sum", self.dev.h, self.handle, C.c_void_p(t.data_ptr()),
+                  t.numel())
+        return t
+
+    def close(self):
+        if self.handle:
+            _lib.load().gcg_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
 class Comm:
     """Collectives over a torch.distributed process group.
 
@@ -184,7 +215,7 @@ class Comm:
     fewer bytes at large rank counts.  GCG_DIST_REDUCE selects the default.
     """
 
-    def __init__(self, group=None, reduce=None):
+    def __init__(self, group=None, reduce=None, native=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
@@ -193,6 +224,19 @@ class Comm:
         self.reduce = reduce or os.environ.get("GCG_DIST_REDUCE", "allgather")
         if self.reduce not in ("allgather", "allreduce"):
             raise ValueError(f"unknown reduce mode {self.reduce!r}")
+        # the library's own NCCL communicator (nccl.cu) for the block-CG halo and
+        # reductions, so a distributed CG runs without host callbacks; on by default
+        # with the NCCL backend (GCG_NATIVE_NCCL=0 keeps the Python callbacks)
+        if native is None:
+            native = self.backend == "nccl" and os.environ.get("GCG_NATIVE_NCCL", "1") != "0"
+        self.native = None
+        if native:
+            self.native = NativeNccl(self)
+
+    def close(self):
+        if self.native is not None:
+            self.native.close()
+            self.native = None
 
     def _host(self, t):
         return t.cpu() if (self.staged and t.is_cuda) else t
@@ -382,8 +426,26 @@ class DistOps(LocalOps):
         d = _lib.CgDist(prob.nghost, prob.nsend, C.c_void_p(prob.send_idx.data_ptr()),
                         C.c_void_p(send.data_ptr()), C.c_void_p(recv.data_ptr()),
                         C.c_void_p(red.data_ptr()), cb, None)
+        keep = []
+        if comm.native is not None:
+            # the library exchanges the halo and sums the k-vectors itself (nccl.cu)
+            peers = [q for q in range(comm.size) if q != comm.rank and
+                     (prob.send_counts[q] or prob.part.recv_counts[q])]
+            pr = (C.c_int32 * max(1, len(peers)))(*peers)
+            so = (C.c_int64 * (len(peers) + 1))(*([int(prob.send_offs[q]) for q in peers] +
+                                                  [int(prob.send_offs[peers[-1] + 1]) if peers else 0]))
+            ro = (C.c_int64 * (len(peers) + 1))(*([int(prob.recv_offs[q]) for q in peers] +
+                                                  [int(prob.recv_offs[peers[-1] + 1]) if peers else 0]))
+            keep = [pr, so, ro]
+            d.callback = _lib.CG_DIST_CALLBACK()
+            d.nccl_comm = comm.native.handle
+            d.npeer = len(peers)
+            d.peer_rank = C.cast(pr, C.c_void_p)
+            d.peer_send_off = C.cast(so, C.c_void_p)
+            d.peer_recv_off = C.cast(ro, C.c_void_p)
         D.block_cg_dist(dev, prob.A, vals, shift, rhs, x, max_iters, rel_tol, sweeps, conv, frozen,
                         relres, d)
+        del keep
 
 
 
