@@ -207,12 +207,12 @@ class NativeNccl:
 class Comm:
     """Collectives over a torch.distributed process group.
 
-    reduce="allgather" (default): sums are all-gathered and added in rank order on
-    every rank — bit-identical on all ranks and independent of the collective
-    algorithm (the reference's deterministic mode, multivec.py:84-112).
-    reduce="allreduce": one NCCL allreduce (the paper's SUBMAT allreduce,
-    PAPER.md:1126-1163) — identical on all ranks for a given NCCL configuration,
-    fewer bytes at large rank counts.  GCG_DIST_REDUCE selects the default.
+    reduce="allgather" (default on host-staged backends): sums are all-gathered and
+    added in rank order on every rank — bit-identical on all ranks and independent of
+    the collective algorithm (the reference's deterministic mode, multivec.py:84-112).
+    reduce="allreduce" (default with NCCL): one NCCL allreduce (the paper's SUBMAT
+    allreduce) — every rank receives the same reduced bits, 1/P of
+    the all-gather's bytes.  GCG_DIST_REDUCE overrides.
     """
 
     def __init__(self, group=None, reduce=None, native=None):
@@ -221,7 +221,10 @@ class Comm:
         self.size = dist.get_world_size(group)
         self.backend = dist.get_backend(group)
         self.staged = self.backend != "nccl"
-        self.reduce = reduce or os.environ.get("GCG_DIST_REDUCE", "allgather")
+        # NCCL: one allreduce (the paper's SUBMAT allreduce; every rank receives the same
+        # reduced bits); host-staged backends: the all-gather + rank-ordered sum
+        self.reduce = reduce or os.environ.get(
+            "GCG_DIST_REDUCE", "allreduce" if self.backend == "nccl" else "allgather")
         if self.reduce not in ("allgather", "allreduce"):
             raise ValueError(f"unknown reduce mode {self.reduce!r}")
         # the library's own NCCL communicator (nccl.cu) for the block-CG halo and
