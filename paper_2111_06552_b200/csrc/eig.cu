@@ -1000,6 +1000,7 @@ __global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
       const double* rowj1 = cl.map_shared_rank(S + (size_t)slt1 * m, own1);
 #pragma unroll
       for (int q = 0; q < kTbSlots; ++q) {
+        if (j + 1 + q * NT >= m) break;  // uniform: no thread of the CTA has slot q
         const int i = j + 1 + tid + q * NT;
         pr[q] = i < m ? *cl.map_shared_rank(S + (size_t)slt[q] * m + j, own[q]) : 0.0;
         rw[q] = i < m ? rowj1[i] : 0.0;
@@ -1009,6 +1010,7 @@ __global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
       p1 = __ldcg(a.pbuf + (size_t)par * m + j + 1);
 #pragma unroll
       for (int q = 0; q < kTbSlots; ++q) {
+        if (j + 1 + q * NT >= m) break;  // uniform: no thread of the CTA has slot q
         const int i = j + 1 + tid + q * NT;
         pr[q] = i < m ? __ldcg(a.pbuf + (size_t)par * m + i) : 0.0;
         rw[q] = i < m ? __ldcg(a.rowbuf + (size_t)par * m + i) : 0.0;
@@ -1022,8 +1024,9 @@ __global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
     double sq = 0.0;
 #pragma unroll
     for (int q = 0; q < kTbSlots; ++q) {
-      const int i = j + 1 + tid + q * NT;
       xq[q] = 0.0;
+      if (j + 1 + q * NT >= m) break;
+      const int i = j + 1 + tid + q * NT;
       if (i < m) {
         const double vi = vcur[i];
         const double wi = fma(a2, vi, pr[q]);
@@ -1054,6 +1057,7 @@ __global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
       double* vn = vprev;  // dead after A: v_{j+1}
 #pragma unroll
       for (int q = 0; q < kTbSlots; ++q) {
+        if (j + 1 + q * NT >= m) break;  // uniform: no thread of the CTA has slot q
         const int i = j + 1 + tid + q * NT;
         if (i < m) {
           const double vi = i == j + 1 ? 0.0 : (i == j + 2 ? 1.0 : xq[q] * scal);
@@ -1102,7 +1106,7 @@ __global__ void __launch_bounds__(NT, 1) tridiag_multi_kernel(TgArgs a) {
 }
 
 constexpr int kTgThreads = 256;  // grid variant
-constexpr int kTcThreads = 512;  // cluster variant
+constexpr int kTcThreads = 256;  // cluster variant (m <= 256: one phase-B slot per thread)
 
 // V[i*ldv + j] = sign_j * Z[i*ldz + j] (row-major Z, column j) with the sign rule
 __global__ void vec_fix_rm_kernel(int m, const double* Z, long long ldz, double* V, long long ldv) {
@@ -1164,10 +1168,10 @@ static char tridiag_mode(int m) {
   if (force == 'o' && m <= kEigMaxM) return 'o';
   if (force == 'g') return 'g';
   if (force == 'c' && m <= kTcMaxM) return 'c';
-  // measured (scripts/eig_bench.py, profiles/r02_eig_modes.txt): one CTA up to 128, the
-  // cluster to 256, the co-resident grid above (the cluster's 16 CTAs run out of
-  // parallelism in phase A past ~300)
-  if (m <= 128) return 'o';
+  // measured (scripts/eig_bench.py, profiles/r02_eig_modes.txt): the 8-CTA cluster from
+  // m = 100 (0.385 vs 0.436 ms one-CTA) to 256, the co-resident grid above (a 16-CTA
+  // cluster runs out of phase-A parallelism past ~300); one CTA only for tiny orders
+  if (m < 48) return 'o';
   return m <= 256 ? 'c' : 'g';
 }
 static bool use_grid_tridiag(int m) { return tridiag_mode(m) != 'o'; }
