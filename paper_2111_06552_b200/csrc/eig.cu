@@ -1178,7 +1178,8 @@ static bool use_grid_tridiag(int m) { return tridiag_mode(m) != 'o'; }
 
 static int tridiag_cluster_launch(Ctx* c, int m, const double* A, long long lda, int sym,
                                   double* dd, double* ee, double* tt, double* Vr) {
-  const int C = m <= 256 ? 8 : 16;
+  static const int env_c = getenv("GCG_TRIC") ? atoi(getenv("GCG_TRIC")) : 0;  // A/B
+  const int C = (env_c == 4 || env_c == 8 || env_c == 16) ? env_c : (m <= 256 ? 8 : 16);
   const int R = (m + C - 1) / C;
   TgArgs a = {};
   a.m = m;
