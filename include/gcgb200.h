@@ -68,7 +68,8 @@ int64_t gcg_cusolver_calls(void);
 /* Live kernel timing: between begin and end every SpMM / Gram / LinComb / CG-update /
  * CG-p-update launch on this ctx is bracketed by CUDA events on the ctx stream.
  * end() synchronises and writes out[3*cls + {0,1,2}] = {total ms, launches,
- * algorithmic HBM bytes} for cls = 0..4 in that order. */
+ * algorithmic HBM bytes} for cls = 0..5: SpMM, Gram, LinComb, CG r-update, CG
+ * x-copy-out, fused CG sweep SpMM. */
 int gcg_prof_begin(void* ctx);
 int gcg_prof_end(void* ctx, double* out);
 /* time only every stride-th launch of each class (stride >= 1, default 1): the

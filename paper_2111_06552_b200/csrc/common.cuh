@@ -27,7 +27,7 @@ struct Scratch {
 // Live per-kernel-class timing (CUDA events on the ctx stream around each
 // launch) + algorithmic byte counts, for bench.py's roofline.  Off by default.
 enum ProfClass { PROF_SPMM = 0, PROF_GRAM, PROF_LINCOMB, PROF_CG_UPDATE, PROF_CG_XOUT,
-                 PROF_NCLASS };
+                 PROF_CG_SWEEP, PROF_NCLASS };
 
 struct Prof {
   bool on = false;

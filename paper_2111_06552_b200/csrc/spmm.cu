@@ -803,7 +803,8 @@ static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowpt
     // fused CG sweep: r once (gather) + p, q written (first sweep) / + p, q, x read and
     // written (later sweeps)
     if (cg) bytes = 12.0 * nnz + 4.0 * (n + 1) + (cg->first ? 24.0 : 56.0) * n * kc;
-    const int ps = prof_start(c, PROF_SPMM, bytes);
+    // the fused CG sweep is its own class (its bytes include the x / p / q streams)
+    const int ps = prof_start(c, cg ? PROF_CG_SWEEP : PROF_SPMM, bytes);
     a.prof_skipped = prof_skip_slot(c, ps);
     switch (vec) {
       case 4: launch_vec<4>(c, a, nv, grid, cg); break;

@@ -72,7 +72,7 @@ class Context:
         return t.to(self.device, non_blocking=False)
 
 
-PROF_CLASSES = ("spmm", "gram", "lincomb", "cg_update", "cg_xout")
+PROF_CLASSES = ("spmm", "gram", "lincomb", "cg_update", "cg_xout", "cg_sweep")
 
 
 class KernelProfile:
