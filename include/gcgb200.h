@@ -386,6 +386,13 @@ typedef struct gcg_mm_info {
 } gcg_mm_info;
 int gcg_mm_open(const char* path, int nthreads, void** handle, gcg_mm_info* info);
 int gcg_mm_fetch(void* handle, int64_t* rows, int64_t* cols, double* vals);
+/* COO -> CSR on the device (the assembly half of MatrixMarket ingestion): device
+ * 0-based int64 rows / cols and f64 vals in any order, duplicates allowed ->
+ * rowptr (n + 1), colidx / val (capacity nnz) with sorted columns and duplicates summed
+ * in input order; *nnz_out = stored entries.  Synchronises the context stream. */
+int gcg_coo_to_csr(void* ctx, int64_t n, int64_t ncols, int64_t nnz, const int64_t* rows,
+                   const int64_t* cols, const double* vals, int32_t* rowptr, int32_t* colidx,
+                   double* val, int64_t* nnz_out);
 void gcg_mm_close(void* handle);
 
 #ifdef __cplusplus

@@ -23,6 +23,7 @@ _SIGS = {
     "gcg_launch_count": [],
     "gcg_cusolver_calls": [],
     "gcg_nccl_available": [],
+    "gcg_coo_to_csr": [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, C.POINTER(_i64)],
     "gcg_nccl_unique_id": [_ptr],
     "gcg_nccl_comm_create": [_ptr, _i32, _i32, _ptr, C.POINTER(_ptr)],
     "gcg_nccl_comm_destroy": [_ptr],

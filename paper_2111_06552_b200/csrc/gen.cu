@@ -14,6 +14,7 @@
 
 #include <string.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -277,6 +278,45 @@ static inline double __longlong_as_double_host(unsigned long long b) {
 
 using namespace gcg;
 
+// ---- COO -> CSR on the device (MatrixMarket ingestion, io.py:108-250) ----------------
+// keys row * ncols + col, stable radix sort (duplicates keep their file order), one
+// segment-head thread sums each run of equal keys in that order, row lengths counted and
+// scanned into the row pointers.
+__global__ void coo_keys_kernel(long long nnz, long long ncols, const long long* __restrict__ rows,
+                                const long long* __restrict__ cols, unsigned long long* keys,
+                                int* idx) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    keys[e] = (unsigned long long)rows[e] * (unsigned long long)ncols + (unsigned long long)cols[e];
+    idx[e] = (int)e;
+  }
+}
+// head[e] = 1 where a new key starts (sorted keys)
+__global__ void coo_heads_kernel(long long nnz, const unsigned long long* __restrict__ keys,
+                                 int* head) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
+}
+// seg = inclusive scan of head (1-based unique index); each head sums its run in order
+__global__ void coo_reduce_kernel(long long nnz, long long ncols,
+                                  const unsigned long long* __restrict__ keys,
+                                  const int* __restrict__ idx, const int* __restrict__ seg,
+                                  const double* __restrict__ vals, int* row_len, int* colidx,
+                                  double* val) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e > 0 && keys[e] == keys[e - 1]) continue;
+    const unsigned long long k = keys[e];
+    double s = vals[idx[e]];
+    for (long long f = e + 1; f < nnz && keys[f] == k; ++f) s += vals[idx[f]];
+    const int u = seg[e] - 1;
+    colidx[u] = (int)(k % (unsigned long long)ncols);
+    val[u] = s;
+    atomicAdd(row_len + (k / (unsigned long long)ncols), 1);
+  }
+}
+
 extern "C" {
 
 int gcg_stencil_nnz(int64_t n0, int64_t n1, int64_t n2, int32_t noff, const int32_t* offs,
@@ -417,6 +457,74 @@ int gcg_varcoef7_weights(void* ctx, int64_t N, const double* kc, double* out) {
   varcoef7_weights_kernel<<<grid_for(n, 256, 8, c->num_sms), 256, 0, c->stream>>>((int)N, kc, out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+
+// COO (device, 0-based int64 row / col, any order, duplicates allowed) -> CSR with sorted
+// column indices and duplicates summed (in input order).  rowptr: n + 1 entries;
+// colidx / val: capacity nnz (the first *nnz_out used).
+int gcg_coo_to_csr(void* ctx, int64_t n, int64_t ncols, int64_t nnz, const int64_t* rows,
+                   const int64_t* cols, const double* vals, int32_t* rowptr, int32_t* colidx,
+                   double* val, int64_t* nnz_out) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || n < 0 || ncols <= 0 || nnz < 0 || !rowptr || !nnz_out || nnz >= (1LL << 31) ||
+      n >= (1LL << 31))
+    return GCG_ERR_ARG;
+  if (nnz > 0 && (!rows || !cols || !vals || !colidx || !val)) return GCG_ERR_ARG;
+  GCG_TRY(cuda_status(cudaMemsetAsync(rowptr, 0, sizeof(int32_t) * (size_t)(n + 1), c->stream)));
+  if (nnz == 0) {
+    *nnz_out = 0;
+    return cuda_status(cudaStreamSynchronize(c->stream));
+  }
+  const int N = (int)nnz;
+  // workspace: keys[2] (u64), idx[2] (int), head, seg (int) | cub temp
+  const size_t kb = sizeof(unsigned long long) * (size_t)N, ib = sizeof(int) * (size_t)N;
+  size_t t_sort = 0, t_scan = 0, t_scan2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr, N,
+                                  0, 64, c->stream);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan, (int*)nullptr, (int*)nullptr, N, c->stream);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan2, (int*)nullptr, (int*)nullptr, (int)n, c->stream);
+  size_t tmp = t_sort > t_scan ? t_sort : t_scan;
+  if (t_scan2 > tmp) tmp = t_scan2;
+  GCG_TRY(ensure(c->host_tmp2, 2 * kb + 4 * ib + tmp + 256));
+  char* base = (char*)c->host_tmp2.ptr;
+  unsigned long long* k0 = (unsigned long long*)base;
+  unsigned long long* k1 = k0 + N;
+  int* i0 = (int*)(k1 + N);
+  int* i1 = i0 + N;
+  int* head = i1 + N;
+  int* seg = head + N;
+  void* temp = (void*)(((uintptr_t)(seg + N) + 255) & ~(uintptr_t)255);
+  const int grid = grid_for(nnz, 256, 8, c->num_sms);
+  coo_keys_kernel<<<grid, 256, 0, c->stream>>>(nnz, ncols, (const long long*)rows,
+                                               (const long long*)cols, k0, i0);
+  GCG_CHECK_LAUNCH();
+  int bits = 1;
+  while (bits < 64 && ((unsigned long long)n * (unsigned long long)ncols) >> bits) ++bits;
+  size_t ts = t_sort;
+  if (cub::DeviceRadixSort::SortPairs(temp, ts, k0, k1, i0, i1, N, 0, bits, c->stream) !=
+      cudaSuccess)
+    return GCG_ERR_CUDA;
+  coo_heads_kernel<<<grid, 256, 0, c->stream>>>(nnz, k1, head);
+  GCG_CHECK_LAUNCH();
+  size_t tsc = t_scan;
+  if (cub::DeviceScan::InclusiveSum(temp, tsc, head, seg, N, c->stream) != cudaSuccess)
+    return GCG_ERR_CUDA;
+  coo_reduce_kernel<<<grid, 256, 0, c->stream>>>(nnz, ncols, k1, i1, seg, vals, rowptr + 1, colidx,
+                                                 val);
+  GCG_CHECK_LAUNCH();
+  size_t tsc2 = t_scan2;
+  if (n > 0 && cub::DeviceScan::InclusiveSum(temp, tsc2, rowptr + 1, rowptr + 1, (int)n,
+                                             c->stream) != cudaSuccess)
+    return GCG_ERR_CUDA;
+  int uniq = 0;
+  GCG_TRY(cuda_status(cudaMemcpyAsync(&uniq, seg + N - 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                      c->stream)));
+  GCG_TRY(cuda_status(cudaStreamSynchronize(c->stream)));
+  *nnz_out = uniq;
+  g_launches += 5;
   return GCG_OK;
 }
 

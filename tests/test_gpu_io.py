@@ -116,3 +116,65 @@ def test_matrix_market_file_solved_end_to_end(tmp_path):
     exact = P.analytic_eigenvalues(1, 20)
     assert rep.status == "converged"
     assert np.abs(rep.eigenvalues - exact).max() / exact.max() <= 1e-9
+
+
+def _mm_text(path, header, size, entries):
+    with open(path, "w") as fh:
+        fh.write(header + "\n% a comment\n" + size + "\n")
+        for e in entries:
+            fh.write(e + "\n")
+
+
+@pytest.mark.parametrize("case", ["general", "symmetric", "duplicates", "empty_rows", "lap3d"])
+def test_device_matrix_market_ingestion(tmp_path, case):
+    """read_matrix_market_device (native tokeniser + device COO->CSR: stable radix sort,
+    duplicate sums, scanned row pointers) equals the host reader; bit for bit without
+    duplicate entries."""
+    import scipy.sparse
+
+    from paper_2111_06552_b200 import device as D
+    from paper_2111_06552_b200.io import read_matrix_market, read_matrix_market_device, \
+        write_matrix_market
+
+    p = tmp_path / f"{case}.mtx"
+    rng = np.random.default_rng(3)
+    if case == "general":
+        m = scipy.sparse.random(300, 300, density=0.03, random_state=5, format="csr")
+        m = m + m.T + scipy.sparse.eye(300)
+        write_matrix_market(m, p)
+    elif case == "symmetric":
+        ents = [f"{i} {i} {4.0 + i / 7}" for i in range(1, 51)] + \
+               [f"{i + 1} {i} {-1.0 - i / 13}" for i in range(1, 50)]
+        _mm_text(p, "%%MatrixMarket matrix coordinate real symmetric", f"50 50 {len(ents)}", ents)
+    elif case == "duplicates":
+        ents = [f"{i} {i} 1.5" for i in range(1, 41)] + ["3 4 0.1", "4 3 0.1", "3 4 0.2",
+                                                          "4 3 0.2", "3 4 1e-17", "4 3 1e-17"]
+        rng.shuffle(ents)
+        _mm_text(p, "%%MatrixMarket matrix coordinate real general", f"40 40 {len(ents)}", ents)
+    elif case == "empty_rows":
+        ents = ["1 1 2.0", "7 7 3.0", "7 2 -1.0", "2 7 -1.0", "30 30 1.0"]
+        _mm_text(p, "%%MatrixMarket matrix coordinate real general", f"30 30 {len(ents)}", ents)
+    else:
+        write_matrix_market(P.laplacian_3d(12), p)
+    host = read_matrix_market(p)
+    dev = D.default_context()
+    d = read_matrix_market_device(p, dev)
+    assert d.n == host.shape[0] and d.nnz == host.nnz
+    assert np.array_equal(d.rowptr.cpu().numpy(), host.indptr)
+    assert np.array_equal(d.colidx.cpu().numpy(), host.indices)
+    if case == "duplicates":
+        assert np.allclose(d.val.cpu().numpy(), host.data, rtol=1e-15, atol=0)
+    else:
+        assert np.array_equal(d.val.cpu().numpy(), host.data)
+
+
+def test_device_matrix_market_errors_match_host(tmp_path):
+    """Malformed files raise the reference's errors before any device work."""
+    from paper_2111_06552_b200.errors import ParseError
+    from paper_2111_06552_b200.io import read_matrix_market_device
+
+    p = tmp_path / "bad.mtx"
+    _mm_text(p, "%%MatrixMarket matrix coordinate real general", "3 3 2", ["1 1 1.0", "4 1 2.0"])
+    with pytest.raises(ParseError) as e:
+        read_matrix_market_device(p)
+    assert e.value.line == 5
