@@ -244,12 +244,15 @@ int gcg_ritz_finish(void* ctx, int64_t k, const double* sums, const double* lam,
 
 /* ---- small dense (device, row-major) -------------------------------------- */
 /* full symmetric eigendecomposition: w ascending, V[:, j] its eigenvector with the
- * largest-|entry| made positive (dense.py:63-82).  A is read only. */
+ * largest-|entry| made positive (dense.py:63-82).  A is read only.  m <= 64: one-CTA
+ * Jacobi; 65..1024: csrc/eig.cu (Householder tridiagonalisation in one CTA, one
+ * cluster or a co-resident grid; bisection; inverse iteration); cuSOLVER syevd above. */
 int gcg_syev(void* ctx, int64_t m, const double* A, int64_t lda, double* w, double* V,
              int64_t ldv);
 /* eigenpairs il..iu (1-based inclusive, dense.py:86-117 sym_eig_range): w gets
  * iu - il + 1 ascending values, V (m x (iu - il + 1), row-major) the sign-fixed
- * vectors.  cuSOLVER syevdx with an index range (any m). */
+ * vectors.  csrc/eig.cu for 3 <= m <= 1024 (only the requested indices are bisected,
+ * inverse-iterated and back-transformed), cuSOLVER syevdx otherwise. */
 int gcg_syev_range(void* ctx, int64_t m, const double* A, int64_t lda, int64_t il, int64_t iu,
                    double* w, double* V, int64_t ldv);
 /* C = alpha op(A) op(B) + beta C, op = transpose when t* != 0. */
