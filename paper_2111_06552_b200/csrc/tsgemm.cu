@@ -211,13 +211,36 @@ __global__ void gram_finish2_kernel(int k1, int k2, int nslab, const double* __r
 
 static inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+template <int BM, int BN, int WM, int WN, int R>
+static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                      const double* Y, long long ldy, double* part, long long rps, int nslab,
+                      bool vec);
+
 template <int BM, int BN, int WM, int WN>
 static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                     const double* Y, long long ldy, double* part, long long rps, int nslab,
                     bool vec) {
   constexpr int W = frag_stride(BM + BN);
   // rows per stage: as many as fit three stages in ~110 KB (>= 16)
-  constexpr int R = (3 * 64 * W * 8 <= 112 * 1024) ? 64 : ((3 * 32 * W * 8 <= 160 * 1024) ? 32 : 16);
+  constexpr int R0 = (3 * 64 * W * 8 <= 112 * 1024) ? 64 : ((3 * 32 * W * 8 <= 160 * 1024) ? 32 : 16);
+  // wide tiles (BN >= 96, the cfg4 / cfg5 deflation shapes): twice the rows per stage
+  // where three stages still fit 220 KB — half the block barriers per row, measured at
+  // n = 2.1M: 900x100 16.3 -> 15.4 ms, 300x100 5.44 -> 5.15, 600x200 23.9 -> 22.7 (skinny
+  // tiles get slower: 180x20 0.67 -> 1.04 ms, so they keep R0); GCG_GRAM_R2=0 disables
+  constexpr int R2 = (BN >= 96 && 3 * 2 * R0 * W * 8 <= 220 * 1024) ? 2 * R0 : R0;
+  static const bool r2 = !(getenv("GCG_GRAM_R2") && getenv("GCG_GRAM_R2")[0] == '0');
+  if (r2 && R2 != R0) {
+    gram_go_r<BM, BN, WM, WN, R2>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec);
+    return;
+  }
+  gram_go_r<BM, BN, WM, WN, R0>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec);
+}
+
+template <int BM, int BN, int WM, int WN, int R>
+static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
+                      const double* Y, long long ldy, double* part, long long rps, int nslab,
+                      bool vec) {
+  constexpr int W = frag_stride(BM + BN);
   constexpr int RG = 8 / ((BM / WM) * (BN / WN));
   const size_t sm_stage = sizeof(double) * (size_t)kStages * R * W;
   const size_t sm_red = sizeof(double) * (size_t)RG * BM * BN;
