@@ -1,6 +1,7 @@
 """Block-CG sweep timing at a BASELINE shape (development helper): 30 sweeps of
 gcg_block_cg on the device-assembled operator with k = bs random right-hand sides.
     python scripts/cg_bench.py 4"""
+import hashlib
 import sys
 
 import torch
@@ -32,7 +33,8 @@ for cfg in [int(c) for c in (sys.argv[1:] or ["2", "4"])]:
     e1.record(dev.stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    print(f"cfg{cfg} n={n} k={k}: 30 sweeps {ms:.3f} ms = {ms / 30 * 1e3:.1f} us/sweep (sweeps={int(sw.item())})",
+    print(f"cfg{cfg} n={n} k={k}: 30 sweeps {ms:.3f} ms = {ms / 30 * 1e3:.1f} us/sweep (sweeps={int(sw.item())}) "
+          f"x-sha1={hashlib.sha1(x.cpu().numpy().tobytes()).hexdigest()[:10]}",
           flush=True)
     del prob, rhs, x
     torch.cuda.empty_cache()
