@@ -83,7 +83,9 @@ __global__ void col_scale_kernel(long long n, int k, const double* __restrict__ 
 __global__ void __launch_bounds__(256) col_dots_kernel(long long n, int k,
                                                        const double* __restrict__ X, long long ldx,
                                                        const double* __restrict__ Y, long long ldy,
-                                                       long long rows_per_cta, double* part) {
+                                                       long long rows_per_cta, double* part,
+                                                       const int* skip) {
+  if (skip && *skip) return;
   extern __shared__ double sm[];
   const int kc = k < 256 ? k : 256;  // columns handled per pass
   const int lanes = 256 / kc;        // row lanes
@@ -198,7 +200,7 @@ int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, 
   GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)grid * k));
   double* part = (double*)c->partials.ptr;
   col_dots_kernel<<<grid, 256, 256 * sizeof(double), c->stream>>>(n, k, X, ldx, Y, ldy, rpc,
-                                                                   part);
+                                                                   part, c->skip);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   GCG_TRY(reduce_partials(c, part, grid, k, out, 1, 0));

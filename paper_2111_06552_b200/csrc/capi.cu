@@ -302,6 +302,9 @@ int gcg_ctx_destroy(void* p) {
   release(c->buildp);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->mapped) cudaFreeHost(c->mapped);
+  if (c->spec) cudaFree(c->spec);
+  for (cudaEvent_t e : c->spec_ev)
+    if (e) cudaEventDestroy(e);
   if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
   return GCG_OK;

@@ -67,7 +67,33 @@ struct Ctx {
   double* mapped_dev = nullptr;  // device view of the same 64 doubles
   int* sync_flag = nullptr;
   cudaEvent_t ev = nullptr;
+  // speculative passes (orth.cu): while `skip` is set, the Gram / LinComb / column-dot
+  // launchers pass it to their kernels, which return at once when *skip != 0 — a pass
+  // enqueued before the host has read the previous pass's decision is a device no-op
+  // when that decision was "stop"
+  const int* skip = nullptr;
+  int* spec = nullptr;  // device ring of per-pass stop flags (kSpecRing ints)
+  unsigned spec_seq = 0;
+  cudaEvent_t spec_ev[2] = {nullptr, nullptr};
+  // passes the last loop at each call site ran (orth.cu): a pass is speculated only
+  // where the previous loop there went on past it
+  int spec_hist[8] = {2, 2, 2, 2, 2, 2, 2, 2};
 };
+constexpr int kSpecRing = 64;
+
+// kernel side of Ctx::skip: `flag` is the stop flag of the previous pass (nullptr: run),
+// `prof` the profiling slot's no-op marker (launches that did nothing carry no bytes)
+struct Skip {
+  const int* flag;
+  int* prof;
+};
+__device__ __forceinline__ bool skip_now(const Skip& s) {
+  if (s.flag && *s.flag) {
+    if (s.prof && threadIdx.x == 0) *s.prof = 1;
+    return true;
+  }
+  return false;
+}
 
 int ensure(Scratch& s, size_t bytes);
 // allocates the mapped decision slots on first use
@@ -152,6 +178,9 @@ int prof_start(Ctx* c, int cls, double bytes);
 void prof_stop(Ctx* c, int slot);
 // device flag slot of a prof_start pair (nullptr when profiling is off)
 int* prof_skip_slot(Ctx* c, int slot);
+inline Skip skip_of(Ctx* c, int prof_slot) {
+  return Skip{c->skip, c->skip ? prof_skip_slot(c, prof_slot) : nullptr};
+}
 
 // internal launchers shared between translation units
 int reduce_partials(Ctx* c, const double* partials, int nparts, int k, double* out,

@@ -268,7 +268,13 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
 __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* G, long long ldg,
                                                            double dep_tol, double skip_tol,
                                                            double* Q,
-                                                           long long ldq, double* status) {
+                                                           long long ldq, double* status,
+                                                           const int* skip, int* stop_out) {
+  // speculative pass (orth.cu): a no-op whose stop flag propagates the "stop"
+  if (skip && *skip) {
+    if (threadIdx.x == 0 && stop_out) *stop_out = 1;
+    return;
+  }
   extern __shared__ __align__(16) unsigned char smraw[];
   JacSmem& S = *reinterpret_cast<JacSmem*>(smraw);
   const int mp = (m + 1) & ~1;
@@ -290,7 +296,10 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
   __syncthreads();
   // the caller stops when the Gram is already the identity to reorth_tol
   // (orth.py:170-171): skip the factorisation then
-  if (S.red[127] <= skip_tol) return;
+  if (S.red[127] <= skip_tol) {
+    if (threadIdx.x == 0 && stop_out) *stop_out = 1;  // converged: the caller returns
+    return;
+  }
   jac_load(S, m, mp, G, ldg, true);
   jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
   sort_and_sign(m, S.a, S.v, S.w, S.Vs, m, S.rank);
@@ -303,6 +312,9 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
     nbad_s = nb;
     status[1] = (double)nb;
     status[2] = wmax;
+    // the next pass follows on the device only for a full-rank block (dependent
+    // columns are replaced on the host first, orth.py:176-186)
+    if (stop_out) *stop_out = nb != 0;
   }
   __syncthreads();
   const int nb = nbad_s;
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
 
 int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
                        double skip_tol, double* Q,
-                       long long ldq, double* status) {
+                       long long ldq, double* status, int* stop_out) {
   const size_t sm = sizeof(JacSmem);
   static bool attr = false;
   if (!attr) {
@@ -324,7 +336,7 @@ int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep
     attr = true;
   }
   svqb_prepare_kernel<<<1, 256, sm, c->stream>>>(m, G, ldg, dep_tol, skip_tol, Q, ldq,
-                                                                 status);
+                                                                 status, c->skip, stop_out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -575,7 +587,8 @@ int scale_rsqrt_launch(Ctx* c, int m, int off, const double* V, long long ldv, c
 int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
                         double skip_tol, double* Q,
                         long long ldq, double* status) {
-  if (m <= kJacMax) return svqb_prepare_small(c, m, G, ldg, dep_tol, skip_tol, Q, ldq, status);
+  if (m <= kJacMax)
+    return svqb_prepare_small(c, m, G, ldg, dep_tol, skip_tol, Q, ldq, status, nullptr);
   // large leaf: defect, cuSOLVER on the symmetric part, count, scale
   max_offeye_kernel<<<1, 256, 0, c->stream>>>(m, G, ldg, status);
   ++g_launches;
@@ -595,10 +608,24 @@ int svqb_prepare_launch(Ctx* c, int m, const double* G, long long ldg, double de
   return GCG_OK;
 }
 
+// speculative-chain form (orth.cu): small leaves only, stop flag for the next pass
+int svqb_prepare_spec_launch(Ctx* c, int m, const double* G, long long ldg, double dep_tol,
+                             double skip_tol, double* Q, long long ldq, double* status,
+                             int* stop_out) {
+  if (m > kJacMax) return GCG_ERR_ARG;
+  return svqb_prepare_small(c, m, G, ldg, dep_tol, skip_tol, Q, ldq, status, stop_out);
+}
+bool svqb_spec_ok(int m) { return m <= kJacMax; }
+
 // deflation repeat test (orth.py:138-152)
 __global__ void deflate_status_kernel(int K, int w, const double* R, long long ldr,
                                       const double* dnew, long long dstride, double dgks,
-                                      double* status) {
+                                      double* status, const int* skip, double stop_tol,
+                                      int* stop_out) {
+  if (skip && *skip) {  // speculative pass after a "stop": propagate it
+    if (threadIdx.x == 0 && stop_out) *stop_out = 1;
+    return;
+  }
   __shared__ double red[32];
   __shared__ int anyf;
   if (threadIdx.x == 0) anyf = 0;
@@ -622,12 +649,24 @@ __global__ void deflate_status_kernel(int K, int w, const double* R, long long l
     for (int q = 0; q < (int)blockDim.x / 32; ++q) t = fmax(t, red[q]);
     status[0] = t;
     status[1] = (double)anyf;
+    if (stop_out) *stop_out = (t <= stop_tol || anyf == 0) ? 1 : 0;  // orth.py:148-152
   }
 }
 
 int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
                           const double* dnew, long long dstride, double dgks, double* status) {
-  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status);
+  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status,
+                                                  nullptr, 0.0, nullptr);
+  ++g_launches;
+  GCG_CHECK_LAUNCH();
+  return GCG_OK;
+}
+
+int deflate_status_spec_launch(Ctx* c, int K, int w, const double* R, long long ldr,
+                               const double* dnew, long long dstride, double dgks,
+                               double* status, double stop_tol, int* stop_out) {
+  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status,
+                                                  c->skip, stop_tol, stop_out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;

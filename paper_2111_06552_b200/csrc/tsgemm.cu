@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
                                                         long long ldx,
                                                         const double* __restrict__ Y,
                                                         long long ldy, long long rows_per_slab,
-                                                        double* part) {
+                                                        double* part, Skip skip) {
+  if (skip_now(skip)) return;
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int WT = (BM / WM) * (BN / WN);  // warps per output tile
   constexpr int RG = 8 / WT;                 // row groups
@@ -194,7 +195,8 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
 // one warp per output: lanes stride the slabs, fixed shuffle tree (deterministic)
 __global__ void gram_finish2_kernel(int k1, int k2, int nslab, const double* __restrict__ part,
                                     double alpha, double beta, double* G, long long grs,
-                                    long long gcs) {
+                                    long long gcs, const int* skip) {
+  if (skip && *skip) return;
   const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= (long long)k1 * k2) return;
@@ -214,12 +216,12 @@ static inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 template <int BM, int BN, int WM, int WN, int R>
 static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                       const double* Y, long long ldy, double* part, long long rps, int nslab,
-                      bool vec);
+                      bool vec, Skip sk);
 
 template <int BM, int BN, int WM, int WN>
 static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                     const double* Y, long long ldy, double* part, long long rps, int nslab,
-                    bool vec) {
+                    bool vec, Skip sk) {
   constexpr int W = frag_stride(BM + BN);
   // rows per stage: as many as fit three stages in ~110 KB (>= 16)
   constexpr int R0 = (3 * 64 * W * 8 <= 112 * 1024) ? 64 : ((3 * 32 * W * 8 <= 160 * 1024) ? 32 : 16);
@@ -230,16 +232,16 @@ static void gram_go(Ctx* c, long long n, int k1, int k2, const double* X, long l
   constexpr int R2 = (BN >= 96 && 3 * 2 * R0 * W * 8 <= 220 * 1024) ? 2 * R0 : R0;
   static const bool r2 = !(getenv("GCG_GRAM_R2") && getenv("GCG_GRAM_R2")[0] == '0');
   if (r2 && R2 != R0) {
-    gram_go_r<BM, BN, WM, WN, R2>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec);
+    gram_go_r<BM, BN, WM, WN, R2>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec, sk);
     return;
   }
-  gram_go_r<BM, BN, WM, WN, R0>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec);
+  gram_go_r<BM, BN, WM, WN, R0>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec, sk);
 }
 
 template <int BM, int BN, int WM, int WN, int R>
 static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                       const double* Y, long long ldy, double* part, long long rps, int nslab,
-                      bool vec) {
+                      bool vec, Skip sk) {
   constexpr int W = frag_stride(BM + BN);
   constexpr int RG = 8 / ((BM / WM) * (BN / WN));
   const size_t sm_stage = sizeof(double) * (size_t)kStages * R * W;
@@ -254,15 +256,15 @@ static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long
     // operand per stage instead of one cp.async per 16 bytes
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   } else if (vec) {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   } else {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, false>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part);
+    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   }
 }
 
@@ -271,13 +273,13 @@ static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long
 // once; 64 x 64 tiles (2 x 2 warps, 2 row groups) otherwise.
 static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, long long ldx,
                          const double* Y, long long ldy, double* part, long long rps, int nslab,
-                         bool vec, int* bm_out, int* bn_out) {
+                         bool vec, int* bm_out, int* bn_out, Skip sk = Skip{nullptr, nullptr}) {
   const int f1 = (k1 + 63) / 64, f2 = (k2 + 7) / 8;
 #define GO(bm, bn, wm, wn)                                                              \
   do {                                                                                \
     *bm_out = bm;                                                                     \
     *bn_out = bn;                                                                     \
-    if (part) gram_go<bm, bn, wm, wn>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec); \
+    if (part) gram_go<bm, bn, wm, wn>(c, n, k1, k2, X, ldx, Y, ldy, part, rps, nslab, vec, sk); \
     return GCG_OK;                                                                    \
   } while (0)
   if (k1 <= 16 && k2 <= 16) GO(16, 16, 16, 16);
@@ -367,7 +369,8 @@ static int gram_dispatch(Ctx* c, long long n, int k1, int k2, const double* X, l
 template <int FN>
 __global__ void __launch_bounds__(256) gram_sym_kernel(long long n, int k,
                                                        const double* __restrict__ X, long long ldx,
-                                                       long long rps, double* part) {
+                                                       long long rps, double* part, Skip skip) {
+  if (skip_now(skip)) return;
   constexpr int U = 4;  // k-steps in flight
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fa = lane >> 2, fc = lane & 3;
@@ -446,18 +449,19 @@ static int gram_sym_launch(Ctx* c, long long n, int k, const double* X, long lon
   GCG_TRY(ensure(c->partials, sizeof(double) * (size_t)nslab * k * k));
   double* part = (double*)c->partials.ptr;
   const int ps = prof_start(c, PROF_GRAM, 8.0 * n * k);
+  const Skip sk = skip_of(c, ps);
   switch ((k + 7) / 8) {
-    case 1: gram_sym_kernel<1><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
-    case 2: gram_sym_kernel<2><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
-    case 3: gram_sym_kernel<3><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
-    default: gram_sym_kernel<4><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part); break;
+    case 1: gram_sym_kernel<1><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
+    case 2: gram_sym_kernel<2><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
+    case 3: gram_sym_kernel<3><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
+    default: gram_sym_kernel<4><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
   }
   prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   const long long outs = (long long)k * k;
   gram_finish2_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, c->stream>>>(
-      k, k, (int)nslab, part, alpha, beta, G, grs, gcs);
+      k, k, (int)nslab, part, alpha, beta, G, grs, gcs, c->skip);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -490,13 +494,14 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
   double* part = (double*)c->partials.ptr;
   const bool vec = (ldx % 2 == 0) && (ldy % 2 == 0) && al16(X) && al16(Y);
   const int ps = prof_start(c, PROF_GRAM, 8.0 * n * (X == Y ? k1 : k1 + k2));
-  gram_dispatch(c, n, k1, k2, X, ldx, Y, ldy, part, rps, (int)nslab, vec, &BM, &BN);
+  gram_dispatch(c, n, k1, k2, X, ldx, Y, ldy, part, rps, (int)nslab, vec, &BM, &BN,
+                skip_of(c, ps));
   prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   const long long outs = (long long)k1 * k2;
   gram_finish2_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, c->stream>>>(
-      k1, k2, (int)nslab, part, alpha, beta, G, grs, gcs);
+      k1, k2, (int)nslab, part, alpha, beta, G, grs, gcs, c->skip);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -513,7 +518,8 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
                                                            long long ldx,
                                                            const double* __restrict__ C,
                                                            long long ldc, double beta, double* Y,
-                                                           long long ldy) {
+                                                           long long ldy, Skip skip) {
+  if (skip_now(skip)) return;
   constexpr int BK = 16;
   constexpr int FM = WM / 8, FN = WN / 8;
   static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
@@ -639,7 +645,7 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
 template <int BM, int BN, int WM, int WN>
 static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const double* X,
                        long long ldx, const double* C, long long ldc, double beta, double* Y,
-                       long long ldy, bool vec) {
+                       long long ldy, bool vec, Skip sk) {
   const size_t sm =
       sizeof(double) * (size_t)kStages * (BM * frag_stride(16) + 16 * frag_stride(BN));
   dim3 grid((unsigned)((n + BM - 1) / BM), (d + BN - 1) / BN);
@@ -648,15 +654,15 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
     // X row chunks and C rows staged by the bulk-copy engine (one instruction per row)
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   } else if (vec) {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   } else {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, false>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   }
 }
 
@@ -708,7 +714,8 @@ __global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int
                                                          const double* X, long long ldx,
                                                          const double* __restrict__ C,
                                                          long long ldc, double beta, double* Y,
-                                                         long long ldy) {
+                                                         long long ldy, Skip skip) {
+  if (skip_now(skip)) return;
   constexpr int KC = 4 * VEC;
   constexpr int CW = ts_cstride(FN, VEC);
   extern __shared__ __align__(16) double cs[];
@@ -789,7 +796,7 @@ __global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int
 template <int FM, int FN, int VEC>
 static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const double* X,
                           long long ldx, const double* C, long long ldc, double beta, double* Y,
-                          long long ldy) {
+                          long long ldy, Skip sk) {
   auto kern = lincomb_ts_kernel<FM, FN, VEC>;
   const int mp = (m + 4 * VEC - 1) / (4 * VEC) * (4 * VEC);
   const size_t sm = sizeof(double) * (size_t)mp * ts_cstride(FN, VEC);
@@ -799,18 +806,18 @@ static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const
   long long grid = (ntiles + 3) / 4;
   const long long cap = (long long)occ * c->num_sms;
   if (grid > cap) grid = cap;
-  kern<<<(unsigned)grid, 128, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+  kern<<<(unsigned)grid, 128, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
 }
 
 template <int VEC>
 static bool lincomb_ts_dispatch(Ctx* c, long long n, int m, int d, double alpha, const double* X,
                                 long long ldx, const double* C, long long ldc, double beta,
-                                double* Y, long long ldy) {
+                                double* Y, long long ldy, Skip sk) {
   const int fn = (d + 7) / 8;
   const size_t sm = sizeof(double) * (size_t)((m + 4 * VEC - 1) / (4 * VEC) * (4 * VEC)) *
                     ts_cstride(fn, VEC);
   if (fn > 8 || sm > 96 * 1024) return false;
-#define TS(fm, fnn) lincomb_ts_go<fm, fnn, VEC>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy)
+#define TS(fm, fnn) lincomb_ts_go<fm, fnn, VEC>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk)
   static const int fmx = getenv("GCG_TS_FM") ? atoi(getenv("GCG_TS_FM")) : 0;
 #define TSF(fnn, dflt)                    \
   {                                       \
@@ -859,15 +866,16 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   }
   const int ps =
       prof_start(c, PROF_LINCOMB, 8.0 * n * (m + d) + (beta != 0.0 ? 8.0 * n * d : 0.0));
+  const Skip sk = skip_of(c, ps);
   static const bool ts_on = !(getenv("GCG_LINCOMB_TS") && getenv("GCG_LINCOMB_TS")[0] == '0');
   if (ts_on && d <= 64) {
     bool done;
     if (ldx % 4 == 0 && ((uintptr_t)X & 31) == 0)
-      done = lincomb_ts_dispatch<4>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+      done = lincomb_ts_dispatch<4>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
     else if (ldx % 2 == 0 && al16(X))
-      done = lincomb_ts_dispatch<2>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+      done = lincomb_ts_dispatch<2>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
     else
-      done = lincomb_ts_dispatch<1>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy);
+      done = lincomb_ts_dispatch<1>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
     if (done) {
       prof_stop(c, ps);
       ++g_launches;
@@ -879,7 +887,7 @@ int lincomb_launch(Ctx* c, long long n, int m, int d, double alpha, const double
   // One column tile covers all d <= 256 columns, so X is streamed exactly once:
   // d <= 64: 8 warps stacked along rows (BM = 256, warp tile 32 x BN);
   // d  > 64: 2 x 4 warps (BM = 64, warp tile 32 x BN/4).
-#define LC(bm, bn, wm, wn) lincomb_go<bm, bn, wm, wn>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec)
+#define LC(bm, bn, wm, wn) lincomb_go<bm, bn, wm, wn>(c, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, vec, sk)
   static const bool lc112 = !(getenv("GCG_LC112") && getenv("GCG_LC112")[0] == '0');
   if (d <= 8) LC(256, 8, 32, 8);
   else if (d <= 16) LC(256, 16, 32, 16);

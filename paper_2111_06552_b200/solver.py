@@ -528,10 +528,14 @@ def gcg_solve_ops(ops, cfg, x0=None):
     max_m = 0
     status = "max_iterations"
     iters_run = 0
+    # the next iteration's A W and [X P W]' A W, enqueued as soon as STEP 2 has fixed W
+    # (before this iteration's bookkeeping), with the timer they are charged to
+    pre_timer = pre_cross = None
 
     for it in range(1, cfg.max_gcg_iters + 1):
         iters_run = it
-        timer = _Timer(not det and cfg.collect_history, getattr(dev, "stream", None))
+        timer = pre_timer if pre_timer is not None else \
+            _Timer(not det and cfg.collect_history, getattr(dev, "stream", None))
         timers.append(timer)
         d = sx - locked
         m = d + np_ + nw
@@ -543,13 +547,14 @@ def gcg_solve_ops(ops, cfg, x0=None):
         if abar_prev is None:
             S.projected(basis, abar)
         else:
-            cross = None
-            if nw:
+            cross = pre_cross
+            if nw and cross is None:
                 aw = S.apply_a(v[:, sx + np_:sx + np_ + nw])
                 cross = dev.empty(m, nw)
                 ops.gram(basis, aw, cross)
             lam_x = _h2d(dev, lam[locked:sx])
             D.abar_assemble(dev, d, lam_x, p_coupling if np_ else None, cross, abar)
+        pre_timer = pre_cross = None
         abar_defect = None
         if cfg.cross_check_abar and abar_prev is not None:
             naive = dev.empty(m, m)
@@ -690,6 +695,11 @@ def gcg_solve_ops(ops, cfg, x0=None):
                 except AllDependent:
                     nw = 0
             timer.lap("t_step2")
+            if nw and it < cfg.max_gcg_iters:
+                pre_timer = _Timer(not det and cfg.collect_history, getattr(dev, "stream", None))
+                aw = S.apply_a(v[:, sx + np_:sx + np_ + nw])
+                pre_cross = dev.empty(sx - locked + np_ + nw, nw)
+                ops.gram(v[:, locked:sx + np_ + nw], aw, pre_cross)
 
         total_red += iter_red
 
