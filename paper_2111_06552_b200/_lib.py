@@ -12,7 +12,8 @@ import os
 from .errors import GcgError, InvalidShape, NoConvergence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgcgb200.so")
+# GCG_LIB_ALT (development A/B only): another build of the same library next to this file
+LIB_PATH = os.path.join(_HERE, os.environ.get("GCG_LIB_ALT") or "libgcgb200.so")
 
 _i64, _i32, _dbl, _ptr, _int = C.c_int64, C.c_int32, C.c_double, C.c_void_p, C.c_int
 

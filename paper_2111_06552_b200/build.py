@@ -22,7 +22,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libgcgb200.so")
 SOURCES = ["capi.cu", "spmm.cu", "blas.cu", "tsgemm.cu", "cg.cu", "dense.cu", "mmio.cu", "orth.cu", "gen.cu", "eig.cu", "nccl.cu"]
-HEADERS = ["common.cuh", "async.cuh"]
+HEADERS = ["common.cuh", "async.cuh", "cgstate.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

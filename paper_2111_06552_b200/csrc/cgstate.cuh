@@ -51,17 +51,17 @@ __device__ __forceinline__ void cta_column_sums(const double* part, int nparts, 
   const int c = threadIdx.x % k, l = threadIdx.x / k;
   double v = 0.0;
   if (l < L) {
-    // 8 independent loads in flight per round, added in index order
-    constexpr int U = 8;
-    int b = l;
-    for (; b + (U - 1) * L < nparts; b += U * L) {
+    // 16 independent loads in flight per round (the tail round predicated, not serial),
+    // added in index order
+    constexpr int U = 16;
+    for (int b = l; b < nparts; b += U * L) {
       double t[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) t[u] = part[(long long)(b + u * L) * k + c];
+      for (int u = 0; u < U; ++u)
+        t[u] = b + u * L < nparts ? part[(long long)(b + u * L) * k + c] : 0.0;
 #pragma unroll
       for (int u = 0; u < U; ++u) v += t[u];
     }
-    for (; b < nparts; b += L) v += part[(long long)b * k + c];
   }
   sm[threadIdx.x] = v;
   __syncthreads();

@@ -37,6 +37,7 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <vector>
 
+#include "async.cuh"
 #include "cgstate.cuh"
 #include "common.cuh"
 
@@ -71,6 +72,8 @@ struct SpmmArgs {
   int* prof_skipped;  // profiling: set when the launch was a no-op
   int c0;             // first column of this pass (CG mode: index of the per-column state)
   int cg_prefetch;    // CG mode: L2-prefetch the next row step's p, q, x
+  int stages;         // staged CG sweep (CGM 3): ring depth per warp
+  unsigned stage_bytes;  // ... and bytes per stage and stream (a warp step's rows, 128-aligned)
 };
 
 template <int VEC>
@@ -161,6 +164,7 @@ struct VecT<4> {
 constexpr int kSpmmThreads = 256;
 constexpr int kSpmmMaxPass = 256;
 constexpr int kSpmmMaxSlots = 8;  // NV * VEC
+constexpr int kCgMaxStages = 4;   // staged CG sweep: deepest per-warp ring
 // resident CTAs per SM by per-lane accumulator width (<= 64 registers at 4)
 __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
   return doubles > 0 ? 4 : 4;  // every shape: 64 registers, one grid size
@@ -175,11 +179,16 @@ __host__ __device__ constexpr int spmm_min_blocks(int doubles) {
 // no second gather of p), and the p'q partials for the next r-update.
 // CGM: 0 = plain SpMM, 1 = CG sweep at 4 CTAs / SM (64 registers), 2 = CG sweep at
 // 3 CTAs / SM (80 registers: the fused epilogue's values no longer spill the gather
-// pipeline's state)
+// pipeline's state), 3 = CGM 2 with the own-row streams p, q, x staged through shared
+// memory by the bulk copy engine: every warp step's rows are one contiguous run per
+// stream (dense ld = k), so each warp keeps a ring of a.stages steps in flight — one
+// cp.async.bulk per stream and step, completion on the warp's mbarrier — and the only
+// global loads left on a step's critical path are the gathers of r.
 template <int VEC, int NV, bool SELF, int CGM>
-__global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(VEC* NV))
+__global__ void __launch_bounds__(kSpmmThreads, CGM >= 2 ? 3 : spmm_min_blocks(VEC* NV))
     spmm_csr_kernel(SpmmArgs a, CgSweep cg) {
   constexpr bool CG = CGM != 0;
+  constexpr bool STG = CGM == 3;
   pdl_wait();
   pdl_trigger();
   if constexpr (CG) {
@@ -223,12 +232,49 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
 
   // per-lane dot accumulators live in shared memory ([warp][slot][lane]: each
   // lane owns its column slots), keeping registers for gathers in flight
-  __shared__ double sacc[NW][kSpmmMaxSlots][32];
-  __shared__ double sdot[NW][kSpmmMaxPass];
-  if (a.dot_mode) {
+  // (STG: both live in the dynamic staging buffer once the row loop is done)
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  // sdot[warp] (the warp's per-column sums) reuses sacc[warp]'s 2 KB: a warp reads all its
+  // slots into registers before it writes its sums
+  static_assert(kSpmmMaxSlots * 32 == kSpmmMaxPass, "sdot aliases sacc per warp");
+  __shared__ double sacc_st[STG ? 1 : NW][kSpmmMaxSlots][32];
+  double(*sacc)[kSpmmMaxSlots][32] = sacc_st;
+  if constexpr (STG) sacc = reinterpret_cast<double(*)[kSpmmMaxSlots][32]>(dyn_smem);
+  double(*sdot)[kSpmmMaxPass] = reinterpret_cast<double(*)[kSpmmMaxPass]>(sacc);
+  if (!CG && a.dot_mode) {
 #pragma unroll
     for (int q = 0; q < NV * VEC; ++q) sacc[warp][q][lane] = 0.0;
   }
+  // STG: per-warp ring of a.stages stages x {p, q, x} x a.stage_bytes, one mbarrier per stage
+  __shared__ unsigned long long stg_bar[STG ? NW : 1][STG ? kCgMaxStages : 1];
+  unsigned char* stg_buf = nullptr;
+  const bool stg_on = STG && !cg.first;
+  auto stg_issue = [&](long long rbs, int st) {  // lane 0: the own-row streams of step rbs
+    if (rbs < rend) {
+      const long long rows = min((long long)G, rend - rbs);
+      const unsigned bytes = (unsigned)(rows * a.k * sizeof(double));
+      unsigned long long* bar = &stg_bar[STG ? warp : 0][STG ? st : 0];
+      unsigned char* dst = stg_buf + (size_t)st * 3 * a.stage_bytes;
+      const long long o = rbs * (long long)cg.k;
+      mbar_expect(bar, 3 * bytes);
+      bulk_g2s(dst, cg.P + o, bytes, bar);
+      bulk_g2s(dst + a.stage_bytes, cg.Q + o, bytes, bar);
+      bulk_g2s(dst + 2 * a.stage_bytes, cg.x + o, bytes, bar);
+    }
+  };
+  if constexpr (STG) {
+    stg_buf = dyn_smem + (size_t)warp * a.stages * 3 * a.stage_bytes;
+    if (stg_on) {
+      if (lane == 0) {
+        for (int st = 0; st < a.stages; ++st) mbar_init(&stg_bar[warp][st]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < a.stages; ++st) stg_issue(rb + st * stride, st);
+      }
+      __syncwarp();
+    }
+  }
+  int stg_st = 0;
+  unsigned stg_par = 0;
   // CG mode: the p'q accumulators stay in registers (one shared-memory store at the
   // end) — per-row shared read-modify-writes doubled the L1 wavefronts of the sweep
   double dacc[CG ? NV : 1][CG ? VEC : 1];
@@ -237,8 +283,13 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
 #pragma unroll
     for (int e = 0; e < (CG ? VEC : 1); ++e) dacc[q][e] = 0.0;
   constexpr int CGN = CG ? kSpmmMaxPass : 1;
-  __shared__ double cg_be[CGN], cg_al[CGN], cg_sm[CGN];
+  // per-column (alpha, beta) and flags, stored at slot(col) = (col % VEC) * (256 / VEC) +
+  // col / VEC: for a fixed e the lanes of a row group read consecutive slots (one
+  // wavefront, broadcast across the groups) instead of a VEC-strided, bank-conflicting run
+  __shared__ double cg_be[CGN], cg_sm[CGN];
+  __shared__ double2 cg_ab[CGN];
   __shared__ int cg_fl[CGN];  // bit 0: p/q update (active), bit 1: deferred x-update
+  auto cg_slot = [](int col) { return (col % VEC) * (kSpmmMaxPass / VEC) + col / VEC; };
   __shared__ int cg_nact;
   if constexpr (CG) {
     const int K = cg.k;
@@ -268,9 +319,8 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
         }
       }
       if (blockIdx.x == 0) cg.s.rz[(cg.par ^ 1) * K + cc] = rzn;
-      cg_be[cc] = be;
-      cg_al[cc] = al;
-      cg_fl[cc] = pp | (ux << 1);
+      cg_ab[cg_slot(cc)] = make_double2(al, be);
+      cg_fl[cg_slot(cc)] = pp | (ux << 1);
       if (pp) atomicAdd(&cg_nact, 1);
     }
     __syncthreads();
@@ -283,13 +333,15 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
   // prefetched state of the row this lane group handles next
   int nstart = 0, nlen = 0, ncol0 = 0, ncol1 = 0;
   double nval0 = 0.0, nval1 = 0.0;
-  auto fetch_rowptr = [&](long long base, int& st, int& ln) {
+  // (st, en) stay raw until the step that consumes them: an eager en - st would make
+  // the warp wait for the row pointers right where they are requested
+  auto fetch_rowptr = [&](long long base, int& st, int& en) {
     const long long r = base + g;
     st = 0;
-    ln = 0;
+    en = 0;
     if (r < rend) {
       st = __ldg(a.rowptr + r);
-      ln = __ldg(a.rowptr + r + 1) - st;
+      en = __ldg(a.rowptr + r + 1);
     }
   };
   auto fetch_chunk = [&](int st, int ln, int off, int& c0, double& v0, int& c1, double& v1) {
@@ -309,11 +361,12 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
   };
   // pipeline: row pointers two steps ahead, the first index/value chunk one step
   // ahead, so neither load is on a step's critical path (only the X gathers are)
-  int pstart = 0, plen = 0;  // row pointers of the step after next
+  int pstart = 0, pend = 0;  // row pointers of the step after next
   if (rb < rend) {
     fetch_rowptr(rb, nstart, nlen);
+    nlen -= nstart;
     fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
-    if (rb + stride < rend) fetch_rowptr(rb + stride, pstart, plen);
+    if (rb + stride < rend) fetch_rowptr(rb + stride, pstart, pend);
   }
 
   for (; rb < rend; rb += stride) {
@@ -323,15 +376,17 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
     double val0 = nval0, val1 = nval1;
     const long long rbn = rb + stride;
     nstart = pstart;
-    nlen = plen;
+    nlen = pend - pstart;
+    pstart = 0;
+    pend = 0;
     if (rbn < rend) fetch_chunk(nstart, nlen, 0, ncol0, nval0, ncol1, nval1);
-    if (rbn + stride < rend) fetch_rowptr(rbn + stride, pstart, plen);
+    if (rbn + stride < rend) fetch_rowptr(rbn + stride, pstart, pend);
     if constexpr (CG) {
       // the next step's own-row streams (p, q, x) into L2 while this step gathers, so
       // the epilogue's loads are L2 hits instead of exposed HBM latency
       static_assert(CGM >= 0, "");
       const long long rp = rb + (a.cg_prefetch == 2 ? 2 : 1) * stride + g;
-      if (a.cg_prefetch && !cg.first && active && rp < rend) {
+      if (!STG && a.cg_prefetch && !cg.first && active && rp < rend) {
         const long long o = rp * (long long)cg.k + a.c0;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
@@ -412,6 +467,14 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
             for (int e = 0; e < VEC; ++e) acc[q][e] = fma(v[u], xv[u][q][e], acc[q][e]);
       }
     }
+    // STG: this step's p, q, x have landed in the warp's stage (read below, in place)
+    const unsigned char* stg_src = nullptr;
+    if constexpr (STG) {
+      if (stg_on) {
+        mbar_wait(&stg_bar[warp][stg_st], stg_par);
+        stg_src = stg_buf + (size_t)stg_st * 3 * a.stage_bytes + (size_t)g * k * sizeof(double);
+      }
+    }
     if constexpr (CG) {
       if (active && r < rend) {
         auto ldv = [&](const double* p, double* o) {
@@ -428,6 +491,15 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
           } else {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) o[e] = p[e];
+          }
+        };
+        auto ldsm = [&](const unsigned char* p, double* o) {  // 32 bytes of a staged row
+          const double2* v = reinterpret_cast<const double2*>(p);
+#pragma unroll
+          for (int e = 0; e < VEC / 2; ++e) {
+            const double2 t = v[e];
+            o[2 * e] = t.x;
+            o[2 * e + 1] = t.y;
           }
         };
         auto stv = [&](double* p, const double* o) {
@@ -451,7 +523,7 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
           bool anyp = false, anyx = false;
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
-            fl[e] = cg_fl[gc + e];
+            fl[e] = cg_fl[cg_slot(gc + e)];
             anyp |= (fl[e] & 1) != 0;
             anyx |= (fl[e] & 2) != 0;
           }
@@ -464,22 +536,34 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
               if (fl[e] & 1) dacc[CG ? q : 0][CG ? e : 0] = fma(rv[e], y[e], dacc[CG ? q : 0][CG ? e : 0]);
           } else if (anyp || anyx) {
             double pv[VEC];
-            lds(cg.P + o, pv);
+            if constexpr (STG) {
+              ldsm(stg_src + c * sizeof(double), pv);
+            } else {
+              lds(cg.P + o, pv);
+            }
             if (anyx) {
               double xv[VEC];
-              lds(cg.x + o, xv);
+              if constexpr (STG) {
+                ldsm(stg_src + 2 * a.stage_bytes + c * sizeof(double), xv);
+              } else {
+                lds(cg.x + o, xv);
+              }
 #pragma unroll
               for (int e = 0; e < VEC; ++e)
-                if (fl[e] & 2) xv[e] = fma(cg_al[gc + e], pv[e], xv[e]);
+                if (fl[e] & 2) xv[e] = fma(cg_ab[cg_slot(gc + e)].x, pv[e], xv[e]);
               stv(cg.x + o, xv);
             }
             if (anyp) {
               double qv[VEC];
-              lds(cg.Q + o, qv);
+              if constexpr (STG) {
+                ldsm(stg_src + a.stage_bytes + c * sizeof(double), qv);
+              } else {
+                lds(cg.Q + o, qv);
+              }
 #pragma unroll
               for (int e = 0; e < VEC; ++e) {
                 if (fl[e] & 1) {
-                  const double be = cg_be[gc + e];
+                  const double be = cg_ab[cg_slot(gc + e)].y;
                   pv[e] = fma(be, pv[e], rv[e]);
                   qv[e] = fma(be, qv[e], y[e]);
                   dacc[CG ? q : 0][CG ? e : 0] = fma(pv[e], qv[e], dacc[CG ? q : 0][CG ? e : 0]);
@@ -488,6 +572,17 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
               stv(cg.P + o, pv);
               stv(cg.Q + o, qv);
             }
+          }
+        }
+      }
+      if constexpr (STG) {
+        // the stage goes back to the copy engine for the step a.stages ahead
+        if (stg_on) {
+          __syncwarp();
+          if (lane == 0) stg_issue(rb + a.stages * stride, stg_st);
+          if (++stg_st == a.stages) {
+            stg_st = 0;
+            stg_par ^= 1u;
           }
         }
       }
@@ -552,6 +647,7 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
   }
 
   if (a.dot_mode == 0) return;
+  if constexpr (STG) __syncthreads();  // every warp is done with its stages: reuse them
   if constexpr (CG) {
 #pragma unroll
     for (int q = 0; q < NV; ++q)
@@ -560,15 +656,25 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM == 2 ? 3 : spmm_min_blocks(V
   }
   // reduce over the row groups of the warp (fixed order g = 0..G-1), then warps
   __syncwarp();
+  double gsum[NV][VEC];
+  if (g0 == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        double v = 0.0;
+        for (int gg = 0; gg < G; ++gg) v += sacc[warp][q * VEC + e][gg * LPR + sub];
+        gsum[q][e] = v;
+      }
+  }
+  __syncwarp();
   if (g0 == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const int c = (q * LPR + sub) * VEC + e;
-        double v = 0.0;
-        for (int gg = 0; gg < G; ++gg) v += sacc[warp][q * VEC + e][gg * LPR + sub];
-        if (c < k) sdot[warp][c] = v;
+        if (c < k) sdot[warp][c] = gsum[q][e];
       }
   }
   __syncthreads();
@@ -616,6 +722,22 @@ static int cg_minb() {
 template <int VEC, int NV>
 static void launch_one(Ctx* c, const SpmmArgs& a, int grid, const CgSweep* cg) {
   if (cg) {
+    if constexpr (VEC == 4) {
+      if (a.stages > 0) {
+        const size_t ring = (size_t)(kSpmmThreads / 32) * a.stages * 3 * a.stage_bytes;
+        const size_t tail = sizeof(double) * (kSpmmThreads / 32) * (kSpmmMaxSlots * 32);
+        const size_t smem = ring > tail ? ring : tail;
+        static size_t smem_set = 0;  // opt in once per size class (> 48 KB)
+        if (smem > smem_set) {
+          cudaFuncSetAttribute(spmm_csr_kernel<VEC, NV, false, 3>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          smem_set = smem;
+        }
+        pdl_launch(spmm_csr_kernel<VEC, NV, false, 3>, dim3(grid), dim3(kSpmmThreads), smem,
+                   c->stream, a, *cg);
+        return;
+      }
+    }
     if (cg_minb() == 4)
       pdl_launch(spmm_csr_kernel<VEC, NV, false, 1>, dim3(grid), dim3(kSpmmThreads), 0,
                  c->stream, a, *cg);
@@ -795,6 +917,23 @@ static int spmm_launch_core(Ctx* c, long long n, long long nnz, const int* rowpt
              (gamma == 0.0 || (aligned_to(a.Z, vb) && ldz % vec == 0)) &&
              (beta == 0.0 || (aligned_to(a.Yin, vb) && ldyin % vec == 0)) &&
              (dot_mode != 1 || (aligned_to(a.W, vb) && ldw % vec == 0));
+    // staged CG sweep (CGM 3): one pass over all k columns, 32-byte lanes, dense blocks
+    // (ld = k, so a warp step's rows of p / q / x are one 16-byte-aligned run each)
+    // Measured (scripts/gpu_cg_stage_ab.sh): wide blocks, one row per warp step (cfg4,
+    // k = 100: 4.22 -> 3.80 ms per sweep with a one-stage ring) gain; at k = 20 (six rows
+    // per warp step) the gathers, not the streams, bound the step and the ring's
+    // shared-memory reads cost 2-3 %.  GCG_CG_STAGES overrides (0 = off).
+    static const int cg_stages_env = getenv("GCG_CG_STAGES") ? atoi(getenv("GCG_CG_STAGES")) : -1;
+    const int cg_stages = cg_stages_env >= 0 ? cg_stages_env : (32 / lpr == 1 ? 1 : 0);
+    a.stages = 0;
+    a.stage_bytes = 0;
+    if (cg && cg_stages > 0 && vec == 4 && a.vepi && kc == k && kc == cg->k &&
+        cg_minb() == 3 && aligned_to(cg->P, 32) && aligned_to(cg->Q, 32) && aligned_to(cg->x, 32)) {
+      a.stage_bytes = (unsigned)(((size_t)(32 / lpr) * kc * sizeof(double) + 127) / 128 * 128);
+      a.stages = cg_stages > kCgMaxStages ? kCgMaxStages : cg_stages;
+      // at most 3 CTAs x ring within the 227 KB of shared memory
+      while (a.stages > 1 && (size_t)(kSpmmThreads / 32) * a.stages * 3 * a.stage_bytes > 66 * 1024) --a.stages;
+    }
     // algorithmic bytes: index/value stream + X once + Y once + each extra distinct stream
     double bytes = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * kc;
     if (gamma != 0.0 && Z != X) bytes += 8.0 * n * kc;
