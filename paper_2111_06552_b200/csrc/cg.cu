@@ -26,6 +26,7 @@
 
 #include <stdlib.h>
 
+#include "async.cuh"
 #include "cgstate.cuh"
 #include "common.cuh"
 
@@ -217,6 +218,117 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
   }
 }
 
+// The r-update as a bulk-copy pipeline: one CTA per SM walks a contiguous row range in
+// stages of ~16 KB per stream; thread 0 keeps kUpdStages stages of r and q in flight
+// (cp.async.bulk into shared memory, completion on the stage's mbarrier) — issued before
+// the prologue, so the fixed-order reduction of the sweep's p'q partials and the alpha
+// decisions overlap the first loads, and HBM latency is covered by bytes in flight
+// instead of by resident warps.  Same per-element arithmetic as cg_update_kernel; the
+// ||r||^2 partials are one row per CTA (148 instead of 512 for the sweep's prologue).
+constexpr int kUpdStages = 4;
+__global__ void __launch_bounds__(256, 1)
+    cg_update_bulk_kernel(long long n, int k, double* r, const double* __restrict__ q,
+                          long long rows_per_cta, int rows_per_stage, const double* spart, int nsp,
+                          double* part, CgState s, int par, int* prof_skipped) {
+  extern __shared__ __align__(128) unsigned char upd_smem[];
+  __shared__ unsigned long long full[kUpdStages];
+  pdl_wait();
+  pdl_trigger();
+  if (*s.skip2) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *s.skip1 = 1;  // propagate: the next sweep SpMM is a no-op too
+      if (prof_skipped) *prof_skipped = 1;
+    }
+    return;
+  }
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  long long r1 = r0 + rows_per_cta;
+  if (r1 > n) r1 = n;
+  const long long nrows = r1 > r0 ? r1 - r0 : 0;
+  const int nst = (int)((nrows + rows_per_stage - 1) / rows_per_stage);
+  const size_t sbytes = (size_t)rows_per_stage * k * sizeof(double);  // per stream
+  auto issue = [&](int st) {  // thread 0: stage st of this CTA's rows into slot st % kUpdStages
+    const long long row = r0 + (long long)st * rows_per_stage;
+    const long long rows = (r1 - row) < rows_per_stage ? (r1 - row) : rows_per_stage;
+    const unsigned bytes = (unsigned)(rows * k * sizeof(double));
+    const int slot = st % kUpdStages;
+    unsigned char* dst = upd_smem + (size_t)slot * 2 * sbytes;
+    mbar_expect(&full[slot], 2 * bytes);
+    bulk_g2s(dst, r + row * k, bytes, &full[slot]);
+    bulk_g2s(dst + sbytes, q + row * k, bytes, &full[slot]);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kUpdStages; ++i) mbar_init(&full[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < kUpdStages && i < nst; ++i) issue(i);
+  }
+  __shared__ double sm[256];
+  __shared__ double s_al[256];
+  __shared__ int s_up[256];
+  __shared__ int nup;
+  if (threadIdx.x == 0) nup = 0;
+  cta_column_sums(spart, nsp, k, sm, s_al);
+  if (threadIdx.x < k) {
+    const int cc = threadIdx.x;
+    const double den = s_al[cc];
+    int u = 0;
+    double al = 0.0;
+    if (!s.conv[cc] && !s.frozen[cc]) {
+      if (den <= 0.0) {
+        if (blockIdx.x == 0) s.frozen[cc] = 1;
+      } else {
+        al = s.rz[par * k + cc] / den;
+        u = 1;
+      }
+    }
+    s_al[cc] = al;
+    s_up[cc] = u;
+    if (u) atomicAdd(&nup, 1);
+    if (blockIdx.x == 0) {
+      s.alpha[cc] = al;
+      s.upd[cc] = u;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *s.sweeps += 1;
+    *s.pending = 1;
+    if (nup == 0) *s.skip1 = 1;  // every column froze: nothing left to sweep
+  }
+  const int lanes = 256 / k;
+  const int c = threadIdx.x % k;
+  const int rl = threadIdx.x / k;
+  const bool upd = rl < lanes && s_up[c];
+  const double al = s_al[c];
+  double acc = 0.0;
+  for (int st = 0; st < nst; ++st) {
+    const int slot = st % kUpdStages;
+    mbar_wait(&full[slot], (unsigned)((st / kUpdStages) & 1));
+    const long long row = r0 + (long long)st * rows_per_stage;
+    const int rows = (int)((r1 - row) < rows_per_stage ? (r1 - row) : rows_per_stage);
+    const double* sr = reinterpret_cast<const double*>(upd_smem + (size_t)slot * 2 * sbytes);
+    const double* sq = reinterpret_cast<const double*>(upd_smem + (size_t)slot * 2 * sbytes + sbytes);
+    if (upd) {
+      double* rout = r + row * k + c;
+#pragma unroll 4
+      for (int i = rl; i < rows; i += lanes) {
+        const double nr = fma(-al, sq[i * k + c], sr[i * k + c]);
+        rout[(long long)i * k] = nr;
+        acc = fma(nr, nr, acc);
+      }
+    }
+    __syncthreads();  // every thread is done with the slot: refill it
+    if (threadIdx.x == 0 && st + kUpdStages < nst) issue(st + kUpdStages);
+  }
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double t = 0.0;
+    for (int l = 0; l < lanes; ++l) t += sm[l * k + threadIdx.x];
+    part[(long long)blockIdx.x * k + threadIdx.x] = t;
+  }
+}
+
 // After the last sweep (256 threads, one CTA): when the last r-update's stop test is
 // still owed (no sweep SpMM followed it), reduce its ||r||^2 partials exactly as the
 // sweep SpMM's prologue would and test; then the report (cg.py:98-99).
@@ -350,6 +462,29 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
   long long rpc = (n + ugrid - 1) / ugrid;
   ugrid = (int)((n + rpc - 1) / rpc);
   const int nparts_max = sgrid > ugrid ? sgrid : ugrid;
+  // bulk-copy r-update: one CTA per SM over an even number of rows, stages of <= 16 KB per
+  // stream in whole row-lane rounds (GCG_CG_UPD_BULK=0: the register-streamed kernel)
+  // (even k only: bulk copies move 16-byte multiples, and a range's last stage may hold an
+  // odd number of rows)
+  static const bool upd_bulk_env = !(getenv("GCG_CG_UPD_BULK") && getenv("GCG_CG_UPD_BULK")[0] == '0');
+  const bool upd_bulk = upd_bulk_env && k % 2 == 0;
+  long long brpc = ((n + c->num_sms - 1) / c->num_sms + 1) & ~1LL;
+  if (brpc < 64) brpc = 64;
+  const int bgrid = (int)((n + brpc - 1) / brpc);
+  int brps = (int)(16384 / (sizeof(double) * k));
+  if (brps >= 256 / k) brps -= brps % (256 / k);
+  brps &= ~1;
+  if (brps < 2) brps = 2;
+  const size_t bsmem = (size_t)kUpdStages * 2 * brps * k * sizeof(double);
+  if (upd_bulk) {
+    static size_t smem_set = 0;
+    if (bsmem > smem_set) {
+      GCG_TRY(cuda_status(cudaFuncSetAttribute(cg_update_bulk_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem)));
+      smem_set = bsmem;
+    }
+  }
+  const int rgrid = upd_bulk ? bgrid : ugrid;  // CTAs (= partial rows) of the r-update
   const long long nghost = dist ? dist->nghost : 0;
   // workspace: R and X ((n + ghosts) x k: both are gathered by an SpMM), P, Q (n x k)
   // + partials + state.  The iterate lives in the dense X (ld = k) during the sweeps —
@@ -431,15 +566,20 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
     }
     // r-update: alpha = r'r / p'q (freeze on p'q <= 0), r -= alpha q, ||r||^2 partials
     const int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
-    pdl_launch(cg_update_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, R, (const double*)Q,
-               (long long)rpc, red, nred, upart, s, (it & 1) ^ 1, prof_skip_slot(c, ps));
+    if (upd_bulk)
+      pdl_launch(cg_update_bulk_kernel, dim3(bgrid), dim3(256), bsmem, c->stream, n, k, R,
+                 (const double*)Q, (long long)brpc, brps, red, nred, upart, s, (it & 1) ^ 1,
+                 prof_skip_slot(c, ps));
+    else
+      pdl_launch(cg_update_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, R, (const double*)Q,
+                 (long long)rpc, red, nred, upart, s, (it & 1) ^ 1, prof_skip_slot(c, ps));
     prof_stop(c, ps);
     ++g_launches;
     GCG_CHECK_LAUNCH();
     rred = upart;
-    nrred = ugrid;
+    nrred = rgrid;
     if (dist) {
-      GCG_TRY(dist_reduce(c, dist, upart, ugrid, k));
+      GCG_TRY(dist_reduce(c, dist, upart, rgrid, k));
       rred = dist->red_buf;
       nrred = 1;
     }
