@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
     }
   }
   pdl_wait();
-  pdl_trigger();
   if (*s.skip2) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       *s.skip1 = 1;  // propagate: the next sweep SpMM is a no-op too
@@ -209,6 +208,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
       acc = fma(nr, nr, acc);
     }
   }
+  pdl_trigger();  // late: see spmm_csr_kernel
   sm[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < kc) {
@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ __align__(128) unsigned char upd_smem[];
   __shared__ unsigned long long full[kUpdStages];
   pdl_wait();
-  pdl_trigger();
   if (*s.skip2) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       *s.skip1 = 1;  // propagate: the next sweep SpMM is a no-op too
@@ -320,6 +319,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();  // every thread is done with the slot: refill it
     if (threadIdx.x == 0 && st + kUpdStages < nst) issue(st + kUpdStages);
   }
+  pdl_trigger();  // late: see spmm_csr_kernel
   sm[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < k) {

@@ -190,7 +190,6 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM >= 2 ? 3 : spmm_min_blocks(V
   constexpr bool CG = CGM != 0;
   constexpr bool STG = CGM == 3;
   pdl_wait();
-  pdl_trigger();
   if constexpr (CG) {
     if (*cg.s.skip1) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -646,6 +645,10 @@ __global__ void __launch_bounds__(kSpmmThreads, CGM >= 2 ? 3 : spmm_min_blocks(V
     }
   }
 
+  // the successor may start launching while this grid drains (it still waits for this
+  // grid's completion before touching memory): an early trigger would let its CTAs take
+  // SM slots from this kernel's for the whole run
+  pdl_trigger();
   if (a.dot_mode == 0) return;
   if constexpr (STG) __syncthreads();  // every warp is done with its stages: reuse them
   if constexpr (CG) {
