@@ -211,31 +211,47 @@ int col_dots_launch(Ctx* c, long long n, int k, const double* X, long long ldx, 
 // ---------------------------------------------------------------------------
 // small dense GEMM (row-major; matrices of order <= a few thousand)
 
+// One 16 x 16 output tile per CTA, K walked in slabs of 64: every thread requests its
+// four A and four B elements of a slab before the barrier (eight independent loads in
+// flight instead of two), so an order-200 product costs 4 exposed memory latencies, not
+// 13 — these launches are latency-bound (a few hundred kflop).  The k-order of each
+// output's fma chain is unchanged.
+constexpr int kGemmKT = 64;
 __global__ void dgemm_small_kernel(int ta, int tb, int M, int N, int K, double alpha,
                                    const double* __restrict__ A, long long lda,
                                    const double* __restrict__ B, long long ldb, double beta,
                                    double* C, long long ldc) {
-  __shared__ double As[16][17];
-  __shared__ double Bs[16][17];
+  __shared__ double As[16][kGemmKT + 1];
+  __shared__ double Bs[kGemmKT][17];
   const int row = blockIdx.y * 16 + threadIdx.y;
   const int col = blockIdx.x * 16 + threadIdx.x;
   double acc = 0.0;
-  for (int kb = 0; kb < K; kb += 16) {
-    {
-      const int kk = kb + threadIdx.x;  // A(row, kk)
-      double v = 0.0;
-      if (row < M && kk < K) v = ta ? A[(long long)kk * lda + row] : A[(long long)row * lda + kk];
-      As[threadIdx.y][threadIdx.x] = v;
+  for (int kb = 0; kb < K; kb += kGemmKT) {
+    double av[kGemmKT / 16], bv[kGemmKT / 16];
+#pragma unroll
+    for (int u = 0; u < kGemmKT / 16; ++u) {
+      const int ka = kb + u * 16 + threadIdx.x;  // A(row, ka)
+      av[u] = 0.0;
+      if (row < M && ka < K) av[u] = ta ? A[(long long)ka * lda + row] : A[(long long)row * lda + ka];
+      const int kk = kb + u * 16 + threadIdx.y;  // B(kk, col)
+      bv[u] = 0.0;
+      if (col < N && kk < K) bv[u] = tb ? B[(long long)col * ldb + kk] : B[(long long)kk * ldb + col];
     }
-    {
-      const int kk = kb + threadIdx.y;  // B(kk, col)
-      double v = 0.0;
-      if (col < N && kk < K) v = tb ? B[(long long)col * ldb + kk] : B[(long long)kk * ldb + col];
-      Bs[threadIdx.y][threadIdx.x] = v;
+#pragma unroll
+    for (int u = 0; u < kGemmKT / 16; ++u) {
+      As[threadIdx.y][u * 16 + threadIdx.x] = av[u];
+      Bs[u * 16 + threadIdx.y][threadIdx.x] = bv[u];
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 16; ++q) acc = fma(As[threadIdx.y][q], Bs[q][threadIdx.x], acc);
+    const int kend = K - kb < kGemmKT ? K - kb : kGemmKT;
+    if (kend == kGemmKT) {
+#pragma unroll 16
+      for (int q = 0; q < kGemmKT; ++q) acc = fma(As[threadIdx.y][q], Bs[q][threadIdx.x], acc);
+    } else {
+      // same chain as the 16-wide slabs of the previous kernel: zero-padded up to a multiple of 16
+      const int kpad = (kend + 15) / 16 * 16;
+      for (int q = 0; q < kpad; ++q) acc = fma(As[threadIdx.y][q], Bs[q][threadIdx.x], acc);
+    }
     __syncthreads();
   }
   if (row < M && col < N) {

@@ -10,7 +10,7 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
     -o gpurun_out/full_${tag}_sweep $SHORT > gpurun_out/ncu_${tag}_sweep.log 2>&1
 echo "sweep rc=$?"
 python scripts/ncu_summary.py gpurun_out/full_${tag}_sweep.ncu-rep > gpurun_out/ncu_sum_${tag}_sweep.txt 2>&1
-[ -n "${NOUPD:-}" ] || ncu --set full --clock-control none --import-source on -k regex:cg_update_kernel -s ${SKIP:-60} -c 1 \
+[ -n "${NOUPD:-}" ] || ncu --set full --clock-control none --import-source on -k regex:cg_update -s ${SKIP:-60} -c 1 \
     -o gpurun_out/full_${tag}_update $SHORT > gpurun_out/ncu_${tag}_update.log 2>&1
 echo "update rc=$?"
 python scripts/ncu_summary.py gpurun_out/full_${tag}_update.ncu-rep > gpurun_out/ncu_sum_${tag}_update.txt 2>&1

@@ -441,6 +441,41 @@ def test_block_cg_vs_oracle(dev, golden):
     assert np.abs(rep.relative_residuals - golden["cg_relres"]).max() <= 1e-10
 
 
+@pytest.mark.parametrize("shape,k", [
+    ((13, 11, 9), 100),   # one row per warp step: the staged (bulk-copied p/q/x) sweep
+    ((13, 11, 9), 72),    # staged, 18 lanes per row
+    ((15, 15, 15), 20),   # six rows per warp step, bulk r-update with a ragged last stage
+    ((17, 9), 21),        # odd k: register-streamed r-update
+    ((7, 7, 7), 256),     # widest single pass
+    ((41, 37), 64),
+])
+def test_block_cg_shapes_vs_oracle(dev, shape, k):
+    """The fused sweep variants (prefetching / staged) and both r-update kernels against the
+    oracle's cg.py restatement: sweep counts, per-column flags and iterates (cg.py:33-99)."""
+    from paper_2111_06552_b200.cg import block_cg
+    from paper_2111_06552_b200.operators import DeviceProblem
+
+    offs = [(0,) * len(shape)] + [tuple(s * (i == ax) for i in range(len(shape)))
+                                  for ax in range(len(shape)) for s in (-1, 1)]
+    a = P.stencil_csr(shape, offs, [2.0 * len(shape)] + [-1.0] * (2 * len(shape)))
+    n = a.shape[0]
+    rng = np.random.default_rng(k)
+    rhs = rng.standard_normal((n, k))
+    rhs[:, 1] = 0.0                               # zero right-hand side: converged at sweep 0
+    rhs[:, 2] *= 1e-3
+    x0 = 0.1 * rng.standard_normal((n, k))
+    x0[:, 1] = 0.0
+    theta = -0.3
+    oa = O.Csr(a)
+    want, wrep = O.block_cg(lambda y: O.shifted_apply(oa, None, theta, y), rhs, x0, 12, 0.05)
+    x = rm(dev, x0)
+    _, rep = block_cg(dev, DeviceProblem(dev, a), theta, rm(dev, rhs), x, 12, 0.05)
+    assert rep.iterations == wrep.iterations
+    assert np.array_equal(np.asarray(rep.converged, bool), np.asarray(wrep.converged, bool))
+    assert rel_err(host(x), want) <= 1e-10
+    assert np.abs(rep.relative_residuals - wrep.relative_residuals).max() <= 1e-10
+
+
 def test_block_cg_semantics(dev):
     """test_cg.py cases: zero-rhs column, indefinite freeze, iteration cap."""
     from paper_2111_06552_b200.cg import block_cg
