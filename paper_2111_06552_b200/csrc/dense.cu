@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
                                                            double* Q,
                                                            long long ldq, double* status,
                                                            const int* skip, int* stop_out) {
+  pdl_wait();
+  pdl_trigger();  // one CTA: let the successor's CTAs become resident while it runs
   // speculative pass (orth.cu): a no-op whose stop flag propagates the "stop"
   if (skip && *skip) {
     if (threadIdx.x == 0 && stop_out) *stop_out = 1;
@@ -335,8 +337,8 @@ int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep
                          (int)sm);
     attr = true;
   }
-  svqb_prepare_kernel<<<1, 256, sm, c->stream>>>(m, G, ldg, dep_tol, skip_tol, Q, ldq,
-                                                                 status, c->skip, stop_out);
+  pdl_launch(svqb_prepare_kernel, dim3(1), dim3(256), sm, c->stream, m, G, ldg, dep_tol, skip_tol, Q,
+             ldq, status, c->skip, stop_out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -622,6 +624,8 @@ __global__ void deflate_status_kernel(int K, int w, const double* R, long long l
                                       const double* dnew, long long dstride, double dgks,
                                       double* status, const int* skip, double stop_tol,
                                       int* stop_out) {
+  pdl_wait();
+  pdl_trigger();  // one CTA: let the successor's CTAs become resident while it runs
   if (skip && *skip) {  // speculative pass after a "stop": propagate it
     if (threadIdx.x == 0 && stop_out) *stop_out = 1;
     return;
@@ -655,8 +659,8 @@ __global__ void deflate_status_kernel(int K, int w, const double* R, long long l
 
 int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
                           const double* dnew, long long dstride, double dgks, double* status) {
-  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status,
-                                                  nullptr, 0.0, nullptr);
+  pdl_launch(deflate_status_kernel, dim3(1), dim3(256), 0, c->stream, K, w, R, ldr, dnew, dstride, dgks,
+             status, (const int*)nullptr, 0.0, (int*)nullptr);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -665,8 +669,8 @@ int deflate_status_launch(Ctx* c, int K, int w, const double* R, long long ldr,
 int deflate_status_spec_launch(Ctx* c, int K, int w, const double* R, long long ldr,
                                const double* dnew, long long dstride, double dgks,
                                double* status, double stop_tol, int* stop_out) {
-  deflate_status_kernel<<<1, 256, 0, c->stream>>>(K, w, R, ldr, dnew, dstride, dgks, status,
-                                                  c->skip, stop_tol, stop_out);
+  pdl_launch(deflate_status_kernel, dim3(1), dim3(256), 0, c->stream, K, w, R, ldr, dnew, dstride, dgks,
+             status, c->skip, stop_tol, stop_out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;

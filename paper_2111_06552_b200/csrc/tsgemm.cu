@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
                                                         const double* __restrict__ Y,
                                                         long long ldy, long long rows_per_slab,
                                                         double* part, Skip skip) {
+  pdl_wait();  // launched with programmatic stream serialization: predecessor complete from here on
   if (skip_now(skip)) return;
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int WT = (BM / WM) * (BN / WN);  // warps per output tile
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
+  pdl_trigger();  // late: the successor (the finish kernel) launches while this grid drains
   cp_wait<0>();
   __syncthreads();
   // combine the RG row groups in a fixed order
@@ -196,6 +198,8 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
 __global__ void gram_finish2_kernel(int k1, int k2, int nslab, const double* __restrict__ part,
                                     double alpha, double beta, double* G, long long grs,
                                     long long gcs, const int* skip) {
+  pdl_wait();
+  pdl_trigger();  // a small kernel: let the successor's CTAs become resident now
   if (skip && *skip) return;
   const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -256,15 +260,15 @@ static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long
     // operand per stage instead of one cp.async per 16 bytes
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   } else if (vec) {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   } else {
     auto kern = gram_dmma_kernel<BM, BN, WM, WN, R, false>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, k1, k2, X, ldx, Y, ldy, rps, part, sk);
   }
 }
 
@@ -370,6 +374,7 @@ template <int FN>
 __global__ void __launch_bounds__(256) gram_sym_kernel(long long n, int k,
                                                        const double* __restrict__ X, long long ldx,
                                                        long long rps, double* part, Skip skip) {
+  pdl_wait();  // launched with programmatic stream serialization: predecessor complete from here on
   if (skip_now(skip)) return;
   constexpr int U = 4;  // k-steps in flight
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -403,6 +408,7 @@ __global__ void __launch_bounds__(256) gram_sym_kernel(long long n, int k,
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], v[u][i], v[u][j]);
   }
+  pdl_trigger();  // late: the finish kernel launches while this grid drains
   // warp partials: warps 4..7 park theirs, warps 0..3 add them (fixed pairing), then
   // the four pair sums are added in order
   constexpr int KW = 8 * FN;
@@ -451,17 +457,17 @@ static int gram_sym_launch(Ctx* c, long long n, int k, const double* X, long lon
   const int ps = prof_start(c, PROF_GRAM, 8.0 * n * k);
   const Skip sk = skip_of(c, ps);
   switch ((k + 7) / 8) {
-    case 1: gram_sym_kernel<1><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
-    case 2: gram_sym_kernel<2><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
-    case 3: gram_sym_kernel<3><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
-    default: gram_sym_kernel<4><<<(unsigned)nslab, 256, 0, c->stream>>>(n, k, X, ldx, rps, part, sk); break;
+    case 1: pdl_launch(gram_sym_kernel<1>, dim3((unsigned)nslab), dim3(256), 0, c->stream, n, k, X, ldx, rps, part, sk); break;
+    case 2: pdl_launch(gram_sym_kernel<2>, dim3((unsigned)nslab), dim3(256), 0, c->stream, n, k, X, ldx, rps, part, sk); break;
+    case 3: pdl_launch(gram_sym_kernel<3>, dim3((unsigned)nslab), dim3(256), 0, c->stream, n, k, X, ldx, rps, part, sk); break;
+    default: pdl_launch(gram_sym_kernel<4>, dim3((unsigned)nslab), dim3(256), 0, c->stream, n, k, X, ldx, rps, part, sk); break;
   }
   prof_stop(c, ps);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   const long long outs = (long long)k * k;
-  gram_finish2_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, c->stream>>>(
-      k, k, (int)nslab, part, alpha, beta, G, grs, gcs, c->skip);
+  pdl_launch(gram_finish2_kernel, dim3((unsigned)((outs * 32 + 255) / 256)), dim3(256), 0, c->stream, k, k,
+             (int)nslab, (const double*)part, alpha, beta, G, grs, gcs, c->skip);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -500,8 +506,8 @@ int gram_launch(Ctx* c, long long n, int k1, int k2, const double* X, long long 
   ++g_launches;
   GCG_CHECK_LAUNCH();
   const long long outs = (long long)k1 * k2;
-  gram_finish2_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, c->stream>>>(
-      k1, k2, (int)nslab, part, alpha, beta, G, grs, gcs, c->skip);
+  pdl_launch(gram_finish2_kernel, dim3((unsigned)((outs * 32 + 255) / 256)), dim3(256), 0, c->stream, k1, k2,
+             (int)nslab, (const double*)part, alpha, beta, G, grs, gcs, c->skip);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -519,6 +525,7 @@ __global__ void __launch_bounds__(256) lincomb_dmma_kernel(long long n, int m, i
                                                            const double* __restrict__ C,
                                                            long long ldc, double beta, double* Y,
                                                            long long ldy, Skip skip) {
+  pdl_wait();  // launched with programmatic stream serialization: predecessor complete from here on
   if (skip_now(skip)) return;
   constexpr int BK = 16;
   constexpr int FM = WM / 8, FN = WN / 8;
@@ -654,15 +661,15 @@ static void lincomb_go(Ctx* c, long long n, int m, int d, double alpha, const do
     // X row chunks and C rows staged by the bulk-copy engine (one instruction per row)
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   } else if (vec) {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, true>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   } else {
     auto kern = lincomb_dmma_kernel<BM, BN, WM, WN, false>;
     kernel_smem((const void*)kern, sm);
-    kern<<<grid, 256, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
+    pdl_launch(kern, grid, dim3(256), sm, c->stream, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
   }
 }
 
@@ -715,6 +722,7 @@ __global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int
                                                          const double* __restrict__ C,
                                                          long long ldc, double beta, double* Y,
                                                          long long ldy, Skip skip) {
+  pdl_wait();  // launched with programmatic stream serialization: predecessor complete from here on
   if (skip_now(skip)) return;
   constexpr int KC = 4 * VEC;
   constexpr int CW = ts_cstride(FN, VEC);
@@ -731,6 +739,7 @@ __global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
 
   for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += wstride) {
+    if (t + wstride >= ntiles) pdl_trigger();  // this warp's last tile: the successor may launch
     const long long r0 = t * 8 * FM;
     const double* xr[FM];
     bool rok[FM];
@@ -806,7 +815,7 @@ static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const
   long long grid = (ntiles + 3) / 4;
   const long long cap = (long long)occ * c->num_sms;
   if (grid > cap) grid = cap;
-  kern<<<(unsigned)grid, 128, sm, c->stream>>>(n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
+  pdl_launch(kern, dim3((unsigned)grid), dim3(128), sm, c->stream, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
 }
 
 template <int VEC>
