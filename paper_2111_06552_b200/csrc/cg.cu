@@ -228,8 +228,9 @@ __global__ void __launch_bounds__(256) cg_update_kernel(long long n, int k, doub
 constexpr int kUpdStages = 4;
 __global__ void __launch_bounds__(256, 1)
     cg_update_bulk_kernel(long long n, int k, double* r, const double* __restrict__ q,
-                          long long rows_per_cta, int rows_per_stage, const double* spart, int nsp,
-                          double* part, CgState s, int par, int* prof_skipped) {
+                          long long rows_per_cta, int rows_per_stage, int order,
+                          const double* spart, int nsp, double* part, CgState s, int par,
+                          int* prof_skipped) {
   extern __shared__ __align__(128) unsigned char upd_smem[];
   __shared__ unsigned long long full[kUpdStages];
   pdl_wait();
@@ -240,14 +241,28 @@ __global__ void __launch_bounds__(256, 1)
     }
     return;
   }
-  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  // order 0: one contiguous row range per CTA; 1 / 2: stage-sized chunks dealt round-robin
+  // over the CTAs, walked from the last rows down (1) or from the first up (2) — the grid
+  // then moves through the block as one window, in the direction opposite to the sweep
+  // SpMM's (whose last-written rows of q are the freshest lines in L2)
+  long long r0 = (long long)blockIdx.x * rows_per_cta;
   long long r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
   const long long nrows = r1 > r0 ? r1 - r0 : 0;
-  const int nst = (int)((nrows + rows_per_stage - 1) / rows_per_stage);
+  int nst = (int)((nrows + rows_per_stage - 1) / rows_per_stage);
+  const long long nch = (n + rows_per_stage - 1) / rows_per_stage;
+  if (order) {
+    r1 = n;
+    nst = blockIdx.x < nch ? (int)((nch - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+  }
+  auto stage_row = [&](int st) -> long long {
+    if (!order) return r0 + (long long)st * rows_per_stage;
+    const long long j = (long long)blockIdx.x + (long long)st * gridDim.x;
+    return (order == 1 ? nch - 1 - j : j) * rows_per_stage;
+  };
   const size_t sbytes = (size_t)rows_per_stage * k * sizeof(double);  // per stream
   auto issue = [&](int st) {  // thread 0: stage st of this CTA's rows into slot st % kUpdStages
-    const long long row = r0 + (long long)st * rows_per_stage;
+    const long long row = stage_row(st);
     const long long rows = (r1 - row) < rows_per_stage ? (r1 - row) : rows_per_stage;
     const unsigned bytes = (unsigned)(rows * k * sizeof(double));
     const int slot = st % kUpdStages;
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(256, 1)
   for (int st = 0; st < nst; ++st) {
     const int slot = st % kUpdStages;
     mbar_wait(&full[slot], (unsigned)((st / kUpdStages) & 1));
-    const long long row = r0 + (long long)st * rows_per_stage;
+    const long long row = stage_row(st);
     const int rows = (int)((r1 - row) < rows_per_stage ? (r1 - row) : rows_per_stage);
     const double* sr = reinterpret_cast<const double*>(upd_smem + (size_t)slot * 2 * sbytes);
     const double* sq = reinterpret_cast<const double*>(upd_smem + (size_t)slot * 2 * sbytes + sbytes);
@@ -484,6 +499,7 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
       smem_set = bsmem;
     }
   }
+  static const int upd_order = getenv("GCG_CG_UPD_ORDER") ? atoi(getenv("GCG_CG_UPD_ORDER")) : 1;
   const int rgrid = upd_bulk ? bgrid : ugrid;  // CTAs (= partial rows) of the r-update
   const long long nghost = dist ? dist->nghost : 0;
   // workspace: R and X ((n + ghosts) x k: both are gathered by an SpMM), P, Q (n x k)
@@ -568,7 +584,7 @@ int block_cg_chunk(Ctx* c, long long n, long long nnz, const int* rowptr, const 
     const int ps = prof_start(c, PROF_CG_UPDATE, 24.0 * n * k);
     if (upd_bulk)
       pdl_launch(cg_update_bulk_kernel, dim3(bgrid), dim3(256), bsmem, c->stream, n, k, R,
-                 (const double*)Q, (long long)brpc, brps, red, nred, upart, s, (it & 1) ^ 1,
+                 (const double*)Q, (long long)brpc, brps, upd_order, red, nred, upart, s, (it & 1) ^ 1,
                  prof_skip_slot(c, ps));
     else
       pdl_launch(cg_update_kernel, dim3(ugrid), dim3(256), 0, c->stream, n, k, R, (const double*)Q,
