@@ -59,6 +59,8 @@ __host__ __device__ constexpr int frag_stride(int w) { return ((w + 11) / 16) * 
 // ---------------------------------------------------------------------------
 // Gram: CTA tile BM x BN; warps tile it WM x WN; the remaining warps split rows.
 
+__constant__ int c_ts_desc = 0;  // GCG_LC_DESC=1: lincomb_ts_kernel walks its row tiles downwards
+
 template <int BM, int BN, int WM, int WN, int R, bool VEC16, bool BULK = false>
 __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int k2,
                                                         const double* __restrict__ X,
@@ -76,14 +78,20 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
   constexpr int V = VEC16 ? 2 : 1;
   extern __shared__ __align__(16) double smg[];
   const int tm0 = blockIdx.x * BM, tn0 = blockIdx.y * BN;
-  const long long r0 = (long long)blockIdx.z * rows_per_slab;
-  long long r1 = r0 + rows_per_slab;
+  // rows_per_slab > 0: slab z owns one contiguous row range; < 0: the R-row stages are dealt
+  // round-robin over the slabs (stage ch of slab z = rows ((ch * nslab + z) * R ...)), so the
+  // grid walks X and Y as one ascending window — the LinComb that follows walks the same
+  // rows downwards and starts on the lines this kernel left in L2
+  const bool inter = rows_per_slab < 0;
+  const long long r0 = inter ? (long long)blockIdx.z * R : (long long)blockIdx.z * rows_per_slab;
+  long long r1 = inter ? n : r0 + rows_per_slab;
   if (r1 > n) r1 = n;
+  const long long cstride = inter ? (long long)gridDim.z * R : (long long)R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wt = warp % WT, rg = warp / WT;
   const int wm0 = (wt / (BN / WN)) * WM, wn0 = (wt % (BN / WN)) * WN;
   const int vx = min(BM, k1 - tm0), vy = min(BN, k2 - tn0);
-  const int nch = (int)((r1 - r0 + R - 1) / R);
+  const int nch = r1 > r0 ? (int)((r1 - r0 + cstride - 1) / cstride) : 0;
   const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column (m or n)
   // Bulk mode: row runs that start 8 bytes past a 16-byte boundary (views at an odd
   // column of an even-ld arena) are copied from one element earlier, so the tile
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int k1, int
     __syncthreads();
   }
   auto load = [&](int ch, int st) {
-    const long long rb = r0 + (long long)ch * R;
+    const long long rb = r0 + (long long)ch * cstride;
     if constexpr (BULK) {
       // one bulk copy per row segment (threads 0.. for X, 128.. for Y); an odd
       // trailing column and the rows past the slab end are filled by plain stores
@@ -252,6 +260,12 @@ static void gram_go_r(Ctx* c, long long n, int k1, int k2, const double* X, long
   const size_t sm_red = sizeof(double) * (size_t)RG * BM * BN;
   const size_t sm = sm_stage > sm_red ? sm_stage : sm_red;
   dim3 grid((k1 + BM - 1) / BM, (k2 + BN - 1) / BN, nslab);
+  // GCG_GRAM_INTER=1: stages dealt round-robin over the slabs (one ascending window over
+  // the rows; with GCG_LC_DESC=1 the LinComb that follows starts on this kernel's L2 tail).
+  // Measured: -2 % per cfg2 iteration (LinComb 50.9 -> 49.3 ms), nothing at cfg3 / cfg4
+  // (basis >> L2); off by default (one contiguous range per slab)
+  static const bool inter_on = getenv("GCG_GRAM_INTER") && getenv("GCG_GRAM_INTER")[0] == '1';
+  if (inter_on) rps = -1;
   static const bool bulk_on = !(getenv("GCG_GRAM_BULK") && getenv("GCG_GRAM_BULK")[0] == '0');
   // bulk staging needs every row run at the same 16-byte phase: even leading dimensions
   // (a run starting 8 bytes past a boundary is copied from one element earlier)
@@ -740,7 +754,9 @@ __global__ void __launch_bounds__(128) lincomb_ts_kernel(long long n, int m, int
 
   for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += wstride) {
     if (t + wstride >= ntiles) pdl_trigger();  // this warp's last tile: the successor may launch
-    const long long r0 = t * 8 * FM;
+    // tiles from the last rows down (c_ts_desc): the Gram before this LinComb walked the
+    // same X upwards, its last rows are still in L2
+    const long long r0 = (c_ts_desc ? ntiles - 1 - t : t) * 8 * FM;
     const double* xr[FM];
     bool rok[FM];
 #pragma unroll
@@ -815,6 +831,11 @@ static void lincomb_ts_go(Ctx* c, long long n, int m, int d, double alpha, const
   long long grid = (ntiles + 3) / 4;
   const long long cap = (long long)occ * c->num_sms;
   if (grid > cap) grid = cap;
+  static const bool desc_set = [] {
+    const int v = getenv("GCG_LC_DESC") && getenv("GCG_LC_DESC")[0] == '1';
+    return cudaMemcpyToSymbol(c_ts_desc, &v, sizeof(int)) == cudaSuccess;
+  }();
+  (void)desc_set;
   pdl_launch(kern, dim3((unsigned)grid), dim3(128), sm, c->stream, n, m, d, alpha, X, ldx, C, ldc, beta, Y, ldy, sk);
 }
 
