@@ -88,7 +88,9 @@ def test_solver_matches_reference_golden(golden, golden_meta, name):
     hres = host_residuals(a, b, rep.eigenvalues, rep.eigenvectors, kind)
     assert hres.max() < 1.01 * tol
     # rounding can move the step at which a degenerate cluster crosses tol
-    assert abs(rep.iterations - meta["iterations"]) <= max(4, int(0.15 * meta["iterations"]))
+    # (measured: 7 of the 9 cases take exactly the reference's count, fem8_baseline 39 vs 41,
+    # varcoef10_moving 74 vs 70 — scripts/iter_counts.py)
+    assert abs(rep.iterations - meta["iterations"]) <= 4
     if f"s_{name}_vectors" in golden:
         res_abs = 0.0 if kind == "relative" else tol * max(1.0, float(np.abs(want).max()))
         ratio = cluster_angles(want, golden[f"s_{name}_vectors"], rep.eigenvectors, b, res_abs)
@@ -120,7 +122,7 @@ def test_cfg2_baseline_against_reference_run():
     exact = P.analytic_eigenvalues(2, 100)
     assert np.abs(rep.eigenvalues - exact).max() / exact.max() <= 1e-9
     assert rep.residuals.max() <= 1e-8
-    assert abs(rep.iterations - ref["iterations"]) <= 5
+    assert abs(rep.iterations - ref["iterations"]) <= 2  # 42 or 43 with the summation order; reference 43
 
 
 @pytest.mark.slow
@@ -144,7 +146,7 @@ def test_cfg3_baseline_against_reference_run():
     assert rep.status == "converged"
     assert np.abs(rep.eigenvalues - want).max() / np.abs(want).max() <= 1e-9
     assert rep.residuals.max() <= 1e-8
-    assert abs(rep.iterations - ref["iterations"]) <= max(4, ref["iterations"] // 7)
+    assert abs(rep.iterations - ref["iterations"]) <= 3  # measured 43 = the reference's 43
     # P1 eigenvalues are upper bounds of the continuum ones (3 pi^2 smallest)
     assert rep.eigenvalues[0] >= 3 * np.pi ** 2 * (1 - 1e-12)
 
