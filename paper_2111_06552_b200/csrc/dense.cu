@@ -39,12 +39,13 @@ constexpr int kJacMax = 64;
 // reading and writing each element once, together with V <- V J.  Two
 // barriers per round; each thread's block / row assignments are fixed for the
 // whole solve and kept in registers (no integer division in the loop).
-constexpr int kJacThreads = 256;
-constexpr int kJacMaxBlk = (kJacMax / 2) * (kJacMax / 2) / kJacThreads;  // 4
-constexpr int kJacMaxVrow = kJacMax * (kJacMax / 2) / kJacThreads;       // 8
-
+// kJacThreads threads for orders up to MMAX: 256 threads serve order 64 (4 blocks and 8 V
+// items per thread); orders <= 32 can run on 128 threads (2 and 4) with cheaper barriers.
+template <int kJacThreads, int MMAX>
 __device__ void jacobi_sweeps(int mp, double (*a)[kJacMax + 1], double (*v)[kJacMax + 1],
                               double* cs, double* sn, int* pp, int* qq, double* red) {
+  constexpr int kJacMaxBlk = ((MMAX / 2) * (MMAX / 2) + kJacThreads - 1) / kJacThreads;
+  constexpr int kJacMaxVrow = (MMAX * (MMAX / 2) + kJacThreads - 1) / kJacThreads;
   const int tid = threadIdx.x;
   const int half = mp / 2;
   // fixed work lists: blocks (P <= R) and V items (row i, pair R)
@@ -210,6 +211,14 @@ __device__ void sort_and_sign(int m, double (*a)[kJacMax + 1], double (*v)[kJacM
   __syncthreads();
 }
 
+// threads of the one-CTA Jacobi by order (GCG_JAC_NT=64|128|256 forces it for orders <= 32)
+static int jac_threads(int m) {
+  static const int env = getenv("GCG_JAC_NT") ? atoi(getenv("GCG_JAC_NT")) : 0;
+  if (m > 32) return 256;
+  if (env == 64 || env == 128 || env == 256) return env;
+  return 128;  // measured: order 16 86.9 -> 72.3 us, order 20 111 -> 100 us (64 threads: 93 / 155 us)
+}
+
 struct JacSmem {
   double a[kJacMax][kJacMax + 1];
   double v[kJacMax][kJacMax + 1];
@@ -235,13 +244,14 @@ __device__ void jac_load(JacSmem& S, int m, int mp, const double* A, long long l
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) syev_jacobi_kernel(int m, const double* A, long long lda,
-                                                          double* w, double* V, long long ldv) {
+template <int NT, int MMAX>
+__global__ void __launch_bounds__(NT) syev_jacobi_kernel(int m, const double* A, long long lda,
+                                                         double* w, double* V, long long ldv) {
   extern __shared__ __align__(16) unsigned char smraw[];
   JacSmem& S = *reinterpret_cast<JacSmem*>(smraw);
   const int mp = (m + 1) & ~1;
   jac_load(S, m, mp, A, lda, false);
-  jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
+  jacobi_sweeps<NT, MMAX>(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
   sort_and_sign(m, S.a, S.v, w, V, ldv, S.rank);
 }
 
@@ -251,11 +261,18 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
   const size_t sm = sizeof(JacSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(syev_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(syev_jacobi_kernel<256, kJacMax>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(syev_jacobi_kernel<128, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    cudaFuncSetAttribute(syev_jacobi_kernel<64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     attr = true;
   }
-
-  syev_jacobi_kernel<<<1, 256, sm, c->stream>>>(m, A, lda, w, V, ldv);
+  const int nt = jac_threads(m);
+  if (nt == 64) syev_jacobi_kernel<64, 32><<<1, 64, sm, c->stream>>>(m, A, lda, w, V, ldv);
+  else if (nt == 128) syev_jacobi_kernel<128, 32><<<1, 128, sm, c->stream>>>(m, A, lda, w, V, ldv);
+  else syev_jacobi_kernel<256, kJacMax><<<1, 256, sm, c->stream>>>(m, A, lda, w, V, ldv);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
@@ -265,7 +282,8 @@ int dense_syev_jacobi(Ctx* c, int m, const double* A, long long lda, double* w, 
 // SVQB leaf step, fused (orth.py:155-188): defect of the raw Gram, Jacobi on
 // its symmetric part, dependence count and the coefficient matrix
 // Q = V[:, nbad:] / sqrt(lambda[nbad:]).
-__global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* G, long long ldg,
+template <int NT, int MMAX>
+__global__ void __launch_bounds__(NT) svqb_prepare_kernel(int m, const double* G, long long ldg,
                                                            double dep_tol, double skip_tol,
                                                            double* Q,
                                                            long long ldq, double* status,
@@ -303,7 +321,7 @@ __global__ void __launch_bounds__(256) svqb_prepare_kernel(int m, const double* 
     return;
   }
   jac_load(S, m, mp, G, ldg, true);
-  jacobi_sweeps(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
+  jacobi_sweeps<NT, MMAX>(mp, S.a, S.v, S.cs, S.sn, S.pp, S.qq, S.red);
   sort_and_sign(m, S.a, S.v, S.w, S.Vs, m, S.rank);
   __shared__ int nbad_s;
   if (threadIdx.x == 0) {
@@ -333,12 +351,24 @@ int svqb_prepare_small(Ctx* c, int m, const double* G, long long ldg, double dep
   const size_t sm = sizeof(JacSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(svqb_prepare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(svqb_prepare_kernel<256, kJacMax>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(svqb_prepare_kernel<128, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    cudaFuncSetAttribute(svqb_prepare_kernel<64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     attr = true;
   }
-  pdl_launch(svqb_prepare_kernel, dim3(1), dim3(256), sm, c->stream, m, G, ldg, dep_tol, skip_tol, Q,
-             ldq, status, c->skip, stop_out);
+  const int nt = jac_threads(m);
+  if (nt == 64)
+    pdl_launch(svqb_prepare_kernel<64, 32>, dim3(1), dim3(64), sm, c->stream, m, G, ldg, dep_tol,
+               skip_tol, Q, ldq, status, c->skip, stop_out);
+  else if (nt == 128)
+    pdl_launch(svqb_prepare_kernel<128, 32>, dim3(1), dim3(128), sm, c->stream, m, G, ldg, dep_tol,
+               skip_tol, Q, ldq, status, c->skip, stop_out);
+  else
+    pdl_launch(svqb_prepare_kernel<256, kJacMax>, dim3(1), dim3(256), sm, c->stream, m, G, ldg,
+               dep_tol, skip_tol, Q, ldq, status, c->skip, stop_out);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
