@@ -661,21 +661,47 @@ __global__ void deflate_status_kernel(int K, int w, const double* R, long long l
     return;
   }
   __shared__ double red[32];
+  __shared__ double colsum[256];
   __shared__ int anyf;
   if (threadIdx.x == 0) anyf = 0;
+  // one pass over R: thread (lane l, column c) takes rows l, l + L, ... (L = 256 / w lanes
+  // per column when w <= 256), so a column's K loads are spread over L threads instead of
+  // one thread walking it; the lane sums of a column are added in lane order
   double mx = 0.0;
-  for (long long e = threadIdx.x; e < (long long)K * w; e += blockDim.x)
-    mx = fmax(mx, fabs(R[(e / w) * ldr + (e % w)]));
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  for (int col = threadIdx.x; col < w; col += blockDim.x) {
+  if (w <= (int)blockDim.x) {
+    const int L = (int)blockDim.x / w;
+    const int c = threadIdx.x % w, l = threadIdx.x / w;
     double lost = 0.0;
-    for (int r = 0; r < K; ++r) {
-      const double x = R[(long long)r * ldr + col];
-      lost += x * x;
+    if (l < L) {
+      for (int r = l; r < K; r += L) {
+        const double x = R[(long long)r * ldr + c];
+        mx = fmax(mx, fabs(x));
+        lost += x * x;
+      }
     }
-    if (lost > dgks * fmax(dnew[col * dstride], 1e-300)) atomicExch(&anyf, 1);
+    colsum[threadIdx.x] = lost;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < w) {
+      double t = 0.0;
+      for (int q = 0; q < L; ++q) t += colsum[q * w + threadIdx.x];
+      if (t > dgks * fmax(dnew[threadIdx.x * dstride], 1e-300)) atomicExch(&anyf, 1);
+    }
+  } else {
+    for (long long e = threadIdx.x; e < (long long)K * w; e += blockDim.x)
+      mx = fmax(mx, fabs(R[(e / w) * ldr + (e % w)]));
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    for (int col = threadIdx.x; col < w; col += blockDim.x) {
+      double lost = 0.0;
+      for (int r = 0; r < K; ++r) {
+        const double x = R[(long long)r * ldr + col];
+        lost += x * x;
+      }
+      if (lost > dgks * fmax(dnew[col * dstride], 1e-300)) atomicExch(&anyf, 1);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
