@@ -296,6 +296,7 @@ int gcg_ctx_destroy(void* p) {
   release(c->partials);
   release(c->eigwork);
   release(c->cg);
+  release(c->cgpad);
   release(c->host_tmp);
   release(c->host_tmp2);
   release(c->host_tmp3);

@@ -43,6 +43,7 @@ int spmm_grid(Ctx* c, long long n);
 int spmm_cg_sweep_launch(Ctx* c, long long n, long long nnz, const int* rowptr,
                          const int* colidx, const double* val, int k, const double* R,
                          double shift, double* partials, int* grid_out, const CgSweep& cg);
+int fill_launch(Ctx* c, long long n, int k, double v, double* Y, long long ldy);
 int copy_launch(Ctx* c, long long n, int k, const double* X, long long ldx, double* Y,
                 long long ldy);
 
@@ -427,8 +428,38 @@ int block_cg_launch(Ctx* c, long long n, long long nnz, const int* rowptr, const
   // blocks (block_size > 256, e.g. nev > 1280) run in column chunks, each with
   // the same sweep count as the joint run (the reported count is the max)
   if (kc > 256) kc = (k + (k + 255) / 256 - 1) / ((k + 255) / 256);
+  // A column count that is not a multiple of 4 (the last iterations of a solve, when
+  // fewer than block_size pairs are left) loses the 32-byte row gathers and the bulk
+  // r-update: at cfg2 a sweep pair costs 142 / 110 / 123 us at k = 19 / 18 / 17 against
+  // 88 us at k = 20.  Such a block runs padded with zero right-hand sides instead — a zero
+  // column converges at sweep 0 and is never touched again (cg.py:56-60), the other
+  // columns' recurrences are unchanged.  GCG_CG_PAD=0 disables; not for row-partitioned
+  // runs (their halo buffers are sized for k).
+  static const bool pad_on = !(getenv("GCG_CG_PAD") && getenv("GCG_CG_PAD")[0] == '0');
   for (int c0 = 0; c0 < k; c0 += kc) {
     const int w = (k - c0) < kc ? (k - c0) : kc;
+    const int wp = (w + 3) & ~3;
+    if (pad_on && !dist && w > 4 && wp != w && wp <= 256) {
+      const size_t blk = (size_t)n * wp;
+      GCG_TRY(ensure(c->cgpad, sizeof(double) * (2 * blk + wp) + 2 * (size_t)wp + 256));
+      double* rhs_p = (double*)c->cgpad.ptr;
+      double* x_p = rhs_p + blk;
+      double* relres_p = x_p + blk;
+      int8_t* conv_p = (int8_t*)(relres_p + wp);
+      int8_t* frozen_p = conv_p + wp;
+      GCG_TRY(fill_launch(c, n, wp - w, 0.0, rhs_p + w, wp));
+      GCG_TRY(fill_launch(c, n, wp - w, 0.0, x_p + w, wp));
+      GCG_TRY(copy_launch(c, n, w, rhs + c0, ldr, rhs_p, wp));
+      GCG_TRY(copy_launch(c, n, w, x0 ? x0 + c0 : x + c0, x0 ? ldx0 : ldx, x_p, wp));
+      GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, wp, rhs_p, wp, nullptr, 0, x_p,
+                             wp, max_iters, rel_tol, d_sweeps, conv_p, frozen_p, relres_p, nullptr));
+      GCG_TRY(copy_launch(c, n, w, x_p, wp, x + c0, ldx));
+      GCG_TRY(cuda_status(cudaMemcpyAsync(d_conv + c0, conv_p, (size_t)w, cudaMemcpyDeviceToDevice, c->stream)));
+      GCG_TRY(cuda_status(cudaMemcpyAsync(d_frozen + c0, frozen_p, (size_t)w, cudaMemcpyDeviceToDevice, c->stream)));
+      GCG_TRY(cuda_status(cudaMemcpyAsync(d_relres + c0, relres_p, sizeof(double) * (size_t)w,
+                                          cudaMemcpyDeviceToDevice, c->stream)));
+      continue;
+    }
     GCG_TRY(block_cg_chunk(c, n, nnz, rowptr, colidx, val, shift, w, rhs + c0, ldr,
                            x0 ? x0 + c0 : nullptr, ldx0, x + c0, ldx, max_iters, rel_tol,
                            d_sweeps, d_conv + c0, d_frozen + c0, d_relres + c0, dist));

@@ -53,6 +53,7 @@ struct Ctx {
   Scratch partials;   // per-CTA partial sums for deterministic reductions
   Scratch eigwork;    // cuSOLVER work + info
   Scratch cg;         // block-CG vectors r, p, q and per-column state
+  Scratch cgpad;      // block CG on a column count padded to a multiple of 4 (rhs, iterate)
   Scratch host_tmp;   // device staging for the host-buffer (reference FFI) entry points
   Scratch host_tmp2;
   Scratch host_tmp3;

@@ -2,6 +2,7 @@
 gcg_block_cg on the device-assembled operator with k = bs random right-hand sides.
     python scripts/cg_bench.py 4"""
 import hashlib
+import os
 import sys
 
 import torch
@@ -15,6 +16,7 @@ for cfg in [int(c) for c in (sys.argv[1:] or ["2", "4"])]:
     prob, meta = device_baseline_problem(dev, cfg)
     n = prob.A.n
     k = meta.block_size or -(-meta.num_eigen // 5)
+    k = int(os.environ.get("CG_BENCH_K", k))
     g = torch.Generator(device=dev.device)
     g.manual_seed(0)
     rhs = torch.randn(n, k, dtype=torch.float64, device=dev.device, generator=g)

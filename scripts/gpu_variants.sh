@@ -11,3 +11,4 @@ run GCG_CG_STAGES=0 GCG_PDL=0 GCG_CG_UPD_BULK=0
 run GCG_GRAM_INTER=1 GCG_LC_DESC=1 GCG_CG_UPD_ORDER=2
 run GCG_JAC_NT=256
 run GCG_JAC_NT=64
+run GCG_CG_PAD=0

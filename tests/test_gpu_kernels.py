@@ -445,7 +445,10 @@ def test_block_cg_vs_oracle(dev, golden):
     ((13, 11, 9), 100),   # one row per warp step: the staged (bulk-copied p/q/x) sweep
     ((13, 11, 9), 72),    # staged, 18 lanes per row
     ((15, 15, 15), 20),   # six rows per warp step, bulk r-update with a ragged last stage
-    ((17, 9), 21),        # odd k: register-streamed r-update
+    ((17, 9), 21),        # odd k: runs padded to 24 columns (zero right-hand sides)
+    ((15, 15, 15), 19),   # padded to 20
+    ((9, 9, 9), 5),       # padded to 8
+    ((9, 9, 9), 3),       # k <= 4: unpadded, scalar gathers and the register-streamed r-update
     ((7, 7, 7), 256),     # widest single pass
     ((41, 37), 64),
 ])
