@@ -411,7 +411,6 @@ def orth_against(ops, x, basis, b=None, cfg=None):
     cfg = cfg if cfg is not None else OrthConfig()
     if x.shape[1] == 0:
         return OrthOutcome(0, [], 0)
-    st = _State(ops, x, b, cfg, 0, x.shape[1])
     have_basis = basis is not None and basis.shape[1] > 0
     if have_basis:
         if basis.shape[0] != x.shape[0]:
@@ -424,6 +423,7 @@ def orth_against(ops, x, basis, b=None, cfg=None):
         if out.num_kept <= 0:
             raise AllDependent("every column in the block is linearly dependent")
         return out
+    st = _State(ops, x, b, cfg, 0, x.shape[1])
     if have_basis:
         _deflate_against(st, basis, 0, x.shape[1])
     inner = recursive_orth_svd(ops, x, 1, x.shape[1], b=b, cfg=cfg)

@@ -562,7 +562,6 @@ def gcg_solve_ops(ops, cfg, x0=None):
             D.symmetrize(dev, naive)
             D.max_abs_diff(dev, abar, naive, S.scalar)
             abar_defect = float(S.scalar[0].item())
-        timer.lap("t_step3")
 
         if cfg.rr_split and ops.size > 1:
             # split-range RR: rank r solves a slice of 1..d, all-gather
@@ -585,9 +584,9 @@ def gcg_solve_ops(ops, cfg, x0=None):
             lam_new = lam_new_dev.cpu().numpy()
         c = locked + newly
         total_locked = stored + c
-        timer.lap("t_step4")
 
         if total_locked >= ne:
+            timer.lap("t_step4")
             S.update_in_place(basis, coeffs, v[:, locked:sx])
             lam[locked:sx] = lam_new
             locked = c
