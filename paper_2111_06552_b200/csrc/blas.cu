@@ -223,6 +223,8 @@ __global__ void dgemm_small_kernel(int ta, int tb, int M, int N, int K, double a
                                    double* C, long long ldc) {
   __shared__ double As[16][kGemmKT + 1];
   __shared__ double Bs[kGemmKT][17];
+  pdl_wait();     // launched with programmatic stream serialization (chains of tiny products)
+  pdl_trigger();  // a few CTAs: the successor may become resident at once
   const int row = blockIdx.y * 16 + threadIdx.y;
   const int col = blockIdx.x * 16 + threadIdx.x;
   double acc = 0.0;
@@ -265,8 +267,8 @@ int dgemm_launch(Ctx* c, int ta, int tb, int M, int N, int K, double alpha, cons
                  long long ldc) {
   if (M <= 0 || N <= 0) return GCG_OK;
   dim3 block(16, 16), grid((N + 15) / 16, (M + 15) / 16);
-  dgemm_small_kernel<<<grid, block, 0, c->stream>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta,
-                                                    C, ldc);
+  pdl_launch(dgemm_small_kernel, grid, block, 0, c->stream, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta,
+             C, ldc);
   ++g_launches;
   GCG_CHECK_LAUNCH();
   return GCG_OK;
